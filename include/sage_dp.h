@@ -1,0 +1,233 @@
+/*
+ * sage_dp.h — C-ABI of the B200-native SAGE data plane (libsagedp.so).
+ *
+ * The reference (arxiv 2404.14691, pkg/src/gslsim) has no native code and no FFI:
+ * its data plane exists only as a model.  Each entry point below replaces one
+ * modelled seam of that simulator; the file:line it replaces is cited on the
+ * declaration (paths relative to /root/reference/pkg/src/gslsim/).  The Python
+ * host layer (paper_2404_14691_b200/) keeps the reference's registration /
+ * invocation API and calls these through ctypes.
+ *
+ * Conventions
+ *   - every call returns int status: SAGE_OK (0) or a negative SAGE_E* code;
+ *     no C++ exception crosses the ABI; sage_last_error() gives the message
+ *     (thread-local).
+ *   - handles are opaque uint64 (0 is never a valid handle).
+ *   - device pointers travel as uint64; host pointers as void*.
+ *   - the library owns device memory, pinned staging, streams and events;
+ *     the caller owns host source buffers until the op's end event completes.
+ *   - completions are POLLED (sage_event_poll); the library never calls back
+ *     into the host language.
+ *   - all times are microseconds on the library clock (CLOCK_MONOTONIC,
+ *     epoch = sage_init); device event times are converted onto it.
+ */
+#ifndef SAGE_DP_H
+#define SAGE_DP_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAGE_ABI_VERSION 1
+
+/* ---- status codes -------------------------------------------------------- */
+#define SAGE_OK          0
+#define SAGE_EINVAL     -1  /* bad argument (reference: ValueError)                     */
+#define SAGE_ENOMEM     -2  /* pool budget exceeded (reference: resources.Denied value) */
+#define SAGE_ECUDA      -3  /* CUDA driver/runtime error                                */
+#define SAGE_ENOTREADY  -4  /* event/op not complete yet (poll again)                   */
+#define SAGE_ESTATE     -5  /* double/unknown free, not initialised (SimulationError)   */
+#define SAGE_ECHECKSUM  -6  /* landed bytes do not match the expected checksum          */
+#define SAGE_ENODEV     -7  /* no such GPU / no GPU visible                              */
+
+typedef uint64_t sage_handle;
+
+/* ---- lifecycle ----------------------------------------------------------- *
+ * Replaces Simulation.__init__'s device state (simulation.py:99-159): one
+ * pool + staging rings + copy/land/host streams per GPU.                      */
+#define SAGE_INIT_PEER_ACCESS  0x1u   /* map every pool segment for all GPUs (fan-out) */
+int         sage_init(int n_gpus, uint64_t pool_bytes_per_gpu, uint64_t staging_bytes,
+                      uint64_t chunk_bytes, uint32_t flags);
+int         sage_shutdown(void);
+const char *sage_last_error(void);
+int         sage_abi_version(void);
+int         sage_device_count(int *n);
+int64_t     sage_now_us(void);
+/* host threads used for the CPU_LOAD memcpy fan-out (default 8) */
+int         sage_set_host_threads(int n);
+
+/* ---- memory pool ----------------------------------------------------------
+ * Replaces MemoryLedger.try_alloc / free / usage_by_class / fits
+ * (resources.py:271-337) and round_up_umb (resources.py:36-40).  Segments are
+ * cuMemCreate physical allocations mapped with cuMemMap; the ledger charges
+ * round_up(bytes, granularity) against the per-GPU budget exactly like the
+ * reference (granularity 0 = exact), while the physical mapping is rounded to
+ * the VMM page (2 MiB).  A refused allocation returns SAGE_ENOMEM and writes
+ * the shortfall (the reference's Denied.shortfall_umb, in bytes).            */
+#define SAGE_CLASS_CONTEXT         0
+#define SAGE_CLASS_READ_ONLY       1
+#define SAGE_CLASS_WRITABLE        2
+#define SAGE_CLASS_INSTANCE_FIXED  3
+#define SAGE_ALLOC_ACCOUNT_ONLY    0x100  /* OR into cls: charge the ledger, map nothing
+                                             (FixedGSL instances allocate in their own context) */
+int sage_pool_configure(int gpu, uint64_t capacity_bytes, uint64_t granularity_bytes);
+int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *dptr,
+                    uint64_t *shortfall);
+int sage_pool_free(sage_handle h);
+int sage_pool_effective(int gpu, uint64_t bytes, uint64_t *effective);
+int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total,
+                    uint64_t *physical_total, uint64_t *capacity);
+/* map an existing segment into another GPU's address space is implicit when
+ * SAGE_INIT_PEER_ACCESS is set; this returns the (shared) VA               */
+int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes);
+
+/* ---- pinned host buffers (the Stage-2 CPU read-only cache, sharing.py:226-228) */
+int sage_host_alloc(uint64_t bytes, sage_handle *h, void **ptr);
+int sage_host_free(sage_handle h);
+
+/* ---- segment layouts ------------------------------------------------------
+ * A layout maps a PACKED host stream (tensors back to back at arbitrary byte
+ * offsets, the "DB" record of ref PAPER.md:345-347 Request/Data) onto the
+ * landed segment (each tensor at a 16-B aligned offset, zero padding between
+ * extents).  dst_off must be ascending, dst_off[0] == 0, 16-B aligned, with
+ * dst_off[i] + len[i] <= dst_off[i+1]; src_off[i] + len[i] <= packed_bytes;
+ * seg_bytes is a multiple of 16.  n == 0 is the empty segment.              */
+int sage_layout_create(const uint64_t *src_off, const uint64_t *dst_off, const uint64_t *len,
+                       uint32_t n, uint64_t packed_bytes, uint64_t seg_bytes, sage_handle *layout);
+int sage_layout_destroy(sage_handle layout);
+/* number of land launches (chunks) a load of this layout takes */
+int sage_layout_chunks(sage_handle layout, uint32_t *n_chunks);
+
+/* ---- events ---------------------------------------------------------------
+ * Every asynchronous op returns an END event; stage begin/end times are read
+ * back from events.  Replaces Token.subscribe / set_ready
+ * (functions.py:281-301): a follower's SYNC_WAIT is a device-side wait on the
+ * leader's END event — no host hop.                                          */
+int sage_event_query(sage_handle ev);                  /* SAGE_OK or SAGE_ENOTREADY */
+int sage_event_sync(sage_handle ev);
+int sage_event_time(sage_handle ev, int64_t *t_us);    /* completion time, library clock */
+int sage_event_release(sage_handle ev);
+/* poll n events; done[i] = 1 when complete.  Blocks up to timeout_us until at
+ * least one is complete.  Returns the number complete (>= 0) or an error.    */
+int sage_event_poll(const sage_handle *evs, int n, uint8_t *done, int64_t timeout_us);
+
+/* ---- streams / context pool -----------------------------------------------
+ * Replaces the GPU_CTX stage node (functions.py:258-264, 285.1 ms at :59).
+ * SAGE: a slot of the pre-created stream pool of the (already live) primary
+ * context.  FixedGSL: sage_fixedgsl_submit creates a fresh context per
+ * invocation (cuCtxCreate), the honest serial baseline.                       */
+int sage_ctx_acquire(int gpu, sage_handle *slot);
+int sage_ctx_release(sage_handle slot);
+/* bind a function context segment on the slot's stream (zero its header and
+ * publish the function's descriptor); waits on `wait` events first          */
+int sage_ctx_bind(sage_handle slot, uint64_t ctx_dptr, uint64_t ctx_bytes,
+                  const sage_handle *wait, int n_wait, sage_handle *begin_ev,
+                  sage_handle *end_ev);
+/* make the slot's stream wait for events (the SYNC_WAIT node)                */
+int sage_stream_wait(sage_handle slot, const sage_handle *evs, int n);
+int sage_slot_record(sage_handle slot, sage_handle *ev);
+
+/* ---- loads ----------------------------------------------------------------
+ * Replaces the CPU_LOAD -> GPU_LOAD chain (functions.py:257-268) and
+ * Channel.begin_transfer (resources.py:137-149): the packed host stream goes
+ * through the pinned staging ring (CPU memcpy fan-out = CPU_LOAD), chunked
+ * double-buffered H2D on the copy engine (= GPU_LOAD) and the sm_100a `land`
+ * kernel (unpack + 64-bit content checksum) into dst.                        */
+#define SAGE_LOAD_SRC_PINNED   0x1u  /* src is pinned/registered: skip the staging memcpy */
+#define SAGE_LOAD_SRC_DEVICE   0x2u  /* src is a device pointer (HBM-resident): no PCIe   */
+#define SAGE_LOAD_SRC_PEER     0x4u  /* src is a device pointer on another GPU: NVLink    */
+typedef struct {
+  int32_t gpu;
+  uint32_t flags;
+  uint64_t dst;              /* device pointer of the landed segment                  */
+  sage_handle layout;        /* 0 = identity: dst gets the packed bytes, padded to 16 */
+  const void *src;           /* packed stream (host, or device address cast to ptr)   */
+  uint64_t src_bytes;        /* must equal the layout's packed_bytes                  */
+  const sage_handle *wait;   /* events the load must wait for (serial plans)          */
+  int32_t n_wait;
+  int32_t src_gpu;           /* SAGE_LOAD_SRC_PEER: owner GPU of src                  */
+} sage_load_desc;
+typedef struct {
+  int64_t cpu_begin_us, cpu_end_us;   /* CPU_LOAD (staging memcpy); -1 if none        */
+  int64_t gpu_begin_us, gpu_end_us;   /* GPU_LOAD (first copy .. last land)          */
+  uint64_t host_bytes;                /* bytes memcpy'd into pinned staging          */
+  uint64_t link_bytes;                /* bytes over PCIe (or NVLink for PEER)        */
+  uint64_t landed_bytes;              /* segment bytes written by land               */
+  uint64_t checksum;                  /* content checksum of the landed segment      */
+  uint32_t chunks;
+  int32_t status;
+} sage_load_info;
+int sage_segment_load(const sage_load_desc *d, sage_handle *load, sage_handle *end_ev);
+int sage_load_info_get(sage_handle load, sage_load_info *out);   /* ENOTREADY until done */
+int sage_load_release(sage_handle load);
+/* recompute the checksum of a landed segment on the device (verify / dedup) */
+int sage_segment_checksum(int gpu, uint64_t dptr, uint64_t bytes, uint64_t *checksum);
+/* D2H a landed segment into a pinned host buffer on the copy stream
+ * (Stage1 -> Stage2 read-only cache, sharing.py:217-229)                     */
+int sage_d2h_cache(int gpu, uint64_t src_dptr, void *host_dst, uint64_t bytes,
+                   const sage_handle *wait, int n_wait, sage_handle *end_ev);
+/* peer copy of a landed segment to another GPU over NVLink (fan-out)         */
+int sage_fanout(int src_gpu, uint64_t src_dptr, int dst_gpu, uint64_t dst_dptr, uint64_t bytes,
+                const sage_handle *wait, int n_wait, sage_handle *end_ev);
+
+/* ---- function bodies (the COMPUTE node, functions.py:276) ----------------- */
+#define SAGE_BODY_TOUCH    0  /* read RO + input, write a digest (synthetic functions) */
+#define SAGE_BODY_SGEMM    1  /* C[M,N] = A[M,K] . B[K,N], A = RO, bf16 in / fp32 out   */
+#define SAGE_BODY_STENCIL  2  /* 7-point 3-D Jacobi, coefficients RO, fp32               */
+#define SAGE_BODY_SPMV     3  /* CSR y = A.x, A = RO, fp32                              */
+#define SAGE_BODY_SPIN     4  /* occupy the SMs for args[0] microseconds                */
+typedef struct {
+  int32_t body;
+  int32_t pad_;
+  uint64_t ro;        /* landed read-only segment (device)              */
+  uint64_t input;     /* landed input (device)                          */
+  uint64_t out;       /* writable output (device)                       */
+  uint64_t ro_bytes, input_bytes, out_bytes;
+  int64_t  args[8];   /* body-specific shape parameters                 */
+} sage_body_desc;
+int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handle *begin_ev,
+                sage_handle *end_ev);
+/* D2H the result on the slot's stream (the RETURN node)                      */
+int sage_return(sage_handle slot, uint64_t src_dptr, void *host_dst, uint64_t bytes,
+                sage_handle *begin_ev, sage_handle *end_ev);
+
+/* ---- FixedGSL serial baseline (policies.py:102-126, functions.py:261-267) ---
+ * One invocation = fresh cuCtxCreate + cudaMalloc + pageable synchronous
+ * per-tensor cudaMemcpy + body + D2H + context teardown, run on a library
+ * worker thread; completion is polled through its end event.                 */
+typedef struct {
+  int32_t gpu;
+  int32_t pad_;
+  sage_handle layout;            /* RO layout (0 = identity)                         */
+  const void *ro_src; uint64_t ro_src_bytes;
+  const void *input;  uint64_t input_bytes;
+  uint64_t alloc_bytes;          /* device bytes the instance reserves (1 GiB-rounded) */
+  sage_body_desc body;           /* ro/input/out pointers are filled in by the worker */
+  void *result; uint64_t result_bytes;
+} sage_fixedgsl_desc;
+typedef struct {
+  int64_t t[16];                 /* begin/end per reference Stage (functions.py:164-176
+                                    order: container,cpu_ctx,cpu_load,gpu_ctx,gpu_load,
+                                    sync_wait,compute,return); -1 = absent            */
+  uint64_t checksum;             /* checksum of the RO bytes as loaded                */
+  int64_t teardown_us;           /* cuCtxDestroy time (after completion)              */
+  int32_t status;
+  int32_t pad_;
+} sage_fixedgsl_info;
+int sage_fixedgsl_submit(const sage_fixedgsl_desc *d, sage_handle *job, sage_handle *end_ev);
+int sage_fixedgsl_info_get(sage_handle job, sage_fixedgsl_info *out);
+int sage_fixedgsl_release(sage_handle job);
+
+/* ---- test support (never on the product path) ------------------------------
+ * Runs the chunk planner and the land byte semantics on the host so the
+ * planner can be checked against the oracle without a GPU.                   */
+int sage_debug_emulate_land(sage_handle layout, const void *packed, uint64_t packed_bytes, void *seg_out,
+                            uint64_t chunk_bytes, uint64_t *checksum);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAGE_DP_H */

@@ -1,0 +1,150 @@
+/*
+ * sage_oracle.c — CPU restatement of the SAGE data-plane byte arithmetic.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library, and
+ * only as the checker / the CPU reference arm.  The product path
+ * (paper_2404_14691_b200/, libsagedp.so) never links or calls it.
+ *
+ * What it restates
+ *   The reference (pkg/src/gslsim) models a read-only load as bytes pushed
+ *   through a channel (functions.py:257-268, resources.py:137-149) and never
+ *   materialises data.  The real plane lands a packed "DB" record
+ *   (ref PAPER.md:345-347, Request/Data with RO type) into a segment whose
+ *   tensors sit at 16-byte aligned offsets, and computes a 64-bit content
+ *   checksum so the sharing manager can verify/deduplicate segments
+ *   (sharing.py:136-177 decides WHO loads; this decides WHAT was loaded).
+ *   Parity status: segment contents and checksums have no reference golden
+ *   vectors (SURVEY.md §8c "parity unpinned" rows); this file is the
+ *   specification, and tests/golden/ pins it with committed vectors.
+ *
+ * Checksum (order independent, so any GPU reduction tree is bit exact):
+ *   words w_j = little-endian uint32 at byte 4j of the LANDED segment
+ *   k_j   = (uint32)j * 0x9E3779B1 ^ (uint32)(j >> 32) * 0x85EBCA77
+ *   h_j   = fmix32(w_j ^ k_j)               (murmur3 finaliser)
+ *   g_j   = (h_j ^ (h_j >> 15)) * 0x2C1B3C6D
+ *   sum   = Σ_j ((uint64)g_j << 32 | h_j)  mod 2^64
+ *
+ * Land (unpack):  seg[dst_off[i] + b] = packed[src_off[i] + b] for b < len[i];
+ *   every other segment byte is zero.
+ *
+ * Host-only loading path (the CPU baseline of BASELINE.md "CPU-baseline
+ * plan" item 2): per invocation copy the DB record into a private buffer,
+ * unpack it through the layout and checksum it, fanned out over T threads.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+static inline uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+  return h;
+}
+
+static inline uint64_t word_term(uint32_t w, uint64_t j) {
+  uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
+  uint32_t h = fmix32(w ^ k);
+  uint32_t g = (h ^ (h >> 15)) * 0x2C1B3C6Du;
+  return ((uint64_t)g << 32) | h;
+}
+
+/* checksum of `bytes` (multiple of 4) starting at word index word_base */
+uint64_t oracle_checksum(const uint8_t *p, uint64_t bytes, uint64_t word_base) {
+  uint64_t s = 0, n = bytes / 4;
+  for (uint64_t j = 0; j < n; ++j) {
+    uint32_t w;
+    memcpy(&w, p + 4 * j, 4);
+    s += word_term(w, word_base + j);
+  }
+  return s;
+}
+
+/* validate a layout; 0 ok, -1 bad */
+int oracle_layout_check(const uint64_t *src_off, const uint64_t *dst_off, const uint64_t *len,
+                        uint32_t n, uint64_t packed_bytes, uint64_t seg_bytes) {
+  if (seg_bytes % 16) return -1;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (dst_off[i] % 16) return -1;
+    if (i == 0 && dst_off[0] != 0) return -1;
+    if (src_off[i] + len[i] > packed_bytes || src_off[i] + len[i] < src_off[i]) return -1;
+    uint64_t end = dst_off[i] + len[i];
+    uint64_t lim = (i + 1 < n) ? dst_off[i + 1] : seg_bytes;
+    if (end > lim) return -1;
+    if (i + 1 < n && dst_off[i + 1] < dst_off[i]) return -1;
+  }
+  return 0;
+}
+
+/* unpack packed -> seg (seg_bytes, zero padded); returns the checksum */
+uint64_t oracle_land(const uint8_t *packed, const uint64_t *src_off, const uint64_t *dst_off,
+                     const uint64_t *len, uint32_t n, uint8_t *seg, uint64_t seg_bytes) {
+  uint64_t cur = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (dst_off[i] > cur) memset(seg + cur, 0, dst_off[i] - cur);
+    memcpy(seg + dst_off[i], packed + src_off[i], len[i]);
+    cur = dst_off[i] + len[i];
+  }
+  if (seg_bytes > cur) memset(seg + cur, 0, seg_bytes - cur);
+  return oracle_checksum(seg, seg_bytes, 0);
+}
+
+/* ---- host-only loading path, multi-threaded (CPU baseline) ---------------- */
+typedef struct {
+  const uint8_t *db;
+  const uint64_t *src_off, *dst_off, *len;
+  uint32_t n;
+  uint64_t packed_bytes, seg_bytes;
+  int n_inv;
+  uint8_t **scratch;      /* per thread: private host copy + landed segment */
+  uint64_t *sums;         /* per invocation checksum out */
+  int next;
+  pthread_mutex_t mu;
+} hostpath_job;
+
+typedef struct { hostpath_job *job; int tid; } hostpath_arg;
+
+static void *hostpath_worker(void *argp) {
+  hostpath_arg *a = (hostpath_arg *)argp;
+  hostpath_job *J = a->job;
+  uint8_t *priv = J->scratch[a->tid];
+  uint8_t *seg = priv + ((J->packed_bytes + 63) & ~(uint64_t)63);
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    int i = J->next++;
+    pthread_mutex_unlock(&J->mu);
+    if (i >= J->n_inv) break;
+    memcpy(priv, J->db, J->packed_bytes);                       /* CPU_LOAD: DB -> host  */
+    J->sums[i] = oracle_land(priv, J->src_off, J->dst_off, J->len, J->n, seg, J->seg_bytes);
+  }
+  return NULL;
+}
+
+/* Run n_inv independent host-only loads of one DB record on `threads`
+ * threads.  Returns 0, or -1 on allocation failure.                          */
+int oracle_hostpath_run(const uint8_t *db, const uint64_t *src_off, const uint64_t *dst_off,
+                        const uint64_t *len, uint32_t n, uint64_t packed_bytes,
+                        uint64_t seg_bytes, int n_inv, int threads, uint64_t *sums) {
+  if (threads < 1) threads = 1;
+  hostpath_job J = {db, src_off, dst_off, len, n, packed_bytes, seg_bytes, n_inv, NULL, sums, 0,
+                    PTHREAD_MUTEX_INITIALIZER};
+  J.scratch = (uint8_t **)calloc((size_t)threads, sizeof(uint8_t *));
+  pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+  hostpath_arg *args = (hostpath_arg *)calloc((size_t)threads, sizeof(hostpath_arg));
+  int rc = 0;
+  if (!J.scratch || !th || !args) { rc = -1; goto out; }
+  for (int t = 0; t < threads; ++t) {
+    J.scratch[t] = (uint8_t *)malloc(((packed_bytes + 63) & ~(uint64_t)63) + seg_bytes + 64);
+    if (!J.scratch[t]) { rc = -1; goto out; }
+    memset(J.scratch[t], 0, ((packed_bytes + 63) & ~(uint64_t)63) + seg_bytes + 64);  /* fault in */
+  }
+  for (int t = 0; t < threads; ++t) {
+    args[t].job = &J; args[t].tid = t;
+    pthread_create(&th[t], NULL, hostpath_worker, &args[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+out:
+  if (J.scratch) for (int t = 0; t < threads; ++t) free(J.scratch[t]);
+  free(J.scratch); free(th); free(args);
+  return rc;
+}

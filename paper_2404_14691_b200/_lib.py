@@ -1,0 +1,186 @@
+"""ctypes binding of libsagedp.so (include/sage_dp.h).
+
+This is the product path: there is no fallback.  If the shared library is
+missing the import of `lib()` raises, and every data-plane call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libsagedp.so"
+
+SAGE_OK = 0
+SAGE_EINVAL = -1
+SAGE_ENOMEM = -2
+SAGE_ECUDA = -3
+SAGE_ENOTREADY = -4
+SAGE_ESTATE = -5
+SAGE_ECHECKSUM = -6
+SAGE_ENODEV = -7
+
+SAGE_INIT_PEER_ACCESS = 0x1
+CLASS_CONTEXT, CLASS_READ_ONLY, CLASS_WRITABLE, CLASS_INSTANCE_FIXED = 0, 1, 2, 3
+ALLOC_ACCOUNT_ONLY = 0x100
+LOAD_SRC_PINNED, LOAD_SRC_DEVICE, LOAD_SRC_PEER = 0x1, 0x2, 0x4
+BODY_TOUCH, BODY_SGEMM, BODY_STENCIL, BODY_SPMV, BODY_SPIN = 0, 1, 2, 3, 4
+
+u64 = C.c_uint64
+i64 = C.c_int64
+H = C.c_uint64  # sage_handle
+
+
+class SageError(RuntimeError):
+    def __init__(self, code: int, what: str, msg: str):
+        super().__init__(f"{what} failed ({code}): {msg}")
+        self.code = code
+
+
+class LoadDesc(C.Structure):
+    _fields_ = [("gpu", C.c_int32), ("flags", C.c_uint32), ("dst", u64), ("layout", H),
+                ("src", C.c_void_p), ("src_bytes", u64), ("wait", C.POINTER(H)), ("n_wait", C.c_int32),
+                ("src_gpu", C.c_int32)]
+
+
+class LoadInfo(C.Structure):
+    _fields_ = [("cpu_begin_us", i64), ("cpu_end_us", i64), ("gpu_begin_us", i64), ("gpu_end_us", i64),
+                ("host_bytes", u64), ("link_bytes", u64), ("landed_bytes", u64), ("checksum", u64),
+                ("chunks", C.c_uint32), ("status", C.c_int32)]
+
+
+class BodyDesc(C.Structure):
+    _fields_ = [("body", C.c_int32), ("pad_", C.c_int32), ("ro", u64), ("input", u64), ("out", u64),
+                ("ro_bytes", u64), ("input_bytes", u64), ("out_bytes", u64), ("args", i64 * 8)]
+
+
+class FixedGSLDesc(C.Structure):
+    _fields_ = [("gpu", C.c_int32), ("pad_", C.c_int32), ("layout", H), ("ro_src", C.c_void_p),
+                ("ro_src_bytes", u64), ("input", C.c_void_p), ("input_bytes", u64), ("alloc_bytes", u64),
+                ("body", BodyDesc), ("result", C.c_void_p), ("result_bytes", u64)]
+
+
+class FixedGSLInfo(C.Structure):
+    _fields_ = [("t", i64 * 16), ("checksum", u64), ("teardown_us", i64), ("status", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
+_SIGS = {
+    "sage_init": (C.c_int, [C.c_int, u64, u64, u64, C.c_uint32]),
+    "sage_shutdown": (C.c_int, []),
+    "sage_last_error": (C.c_char_p, []),
+    "sage_abi_version": (C.c_int, []),
+    "sage_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "sage_now_us": (i64, []),
+    "sage_set_host_threads": (C.c_int, [C.c_int]),
+    "sage_pool_configure": (C.c_int, [C.c_int, u64, u64]),
+    "sage_pool_alloc": (C.c_int, [C.c_int, u64, C.c_int, C.POINTER(H), C.POINTER(u64), C.POINTER(u64)]),
+    "sage_pool_free": (C.c_int, [H]),
+    "sage_pool_effective": (C.c_int, [C.c_int, u64, C.POINTER(u64)]),
+    "sage_pool_usage": (C.c_int, [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+    "sage_pool_dptr": (C.c_int, [H, C.POINTER(u64), C.POINTER(u64)]),
+    "sage_host_alloc": (C.c_int, [u64, C.POINTER(H), C.POINTER(C.c_void_p)]),
+    "sage_host_free": (C.c_int, [H]),
+    "sage_layout_create": (C.c_int, [C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.c_uint32, u64, u64,
+                                     C.POINTER(H)]),
+    "sage_layout_destroy": (C.c_int, [H]),
+    "sage_layout_chunks": (C.c_int, [H, C.POINTER(C.c_uint32)]),
+    "sage_event_query": (C.c_int, [H]),
+    "sage_event_sync": (C.c_int, [H]),
+    "sage_event_time": (C.c_int, [H, C.POINTER(i64)]),
+    "sage_event_release": (C.c_int, [H]),
+    "sage_event_poll": (C.c_int, [C.POINTER(H), C.c_int, C.POINTER(C.c_uint8), i64]),
+    "sage_ctx_acquire": (C.c_int, [C.c_int, C.POINTER(H)]),
+    "sage_ctx_release": (C.c_int, [H]),
+    "sage_ctx_bind": (C.c_int, [H, u64, u64, C.POINTER(H), C.c_int, C.POINTER(H), C.POINTER(H)]),
+    "sage_stream_wait": (C.c_int, [H, C.POINTER(H), C.c_int]),
+    "sage_slot_record": (C.c_int, [H, C.POINTER(H)]),
+    "sage_segment_load": (C.c_int, [C.POINTER(LoadDesc), C.POINTER(H), C.POINTER(H)]),
+    "sage_load_info_get": (C.c_int, [H, C.POINTER(LoadInfo)]),
+    "sage_load_release": (C.c_int, [H]),
+    "sage_segment_checksum": (C.c_int, [C.c_int, u64, u64, C.POINTER(u64)]),
+    "sage_d2h_cache": (C.c_int, [C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
+    "sage_fanout": (C.c_int, [C.c_int, u64, C.c_int, u64, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
+    "sage_launch": (C.c_int, [H, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
+    "sage_return": (C.c_int, [H, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),
+    "sage_fixedgsl_submit": (C.c_int, [C.POINTER(FixedGSLDesc), C.POINTER(H), C.POINTER(H)]),
+    "sage_fixedgsl_info_get": (C.c_int, [H, C.POINTER(FixedGSLInfo)]),
+    "sage_fixedgsl_release": (C.c_int, [H]),
+    "sage_debug_emulate_land": (C.c_int, [H, C.c_void_p, u64, C.c_void_p, u64, C.POINTER(u64)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libsagedp.so (raises if it was not built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.sage_abi_version() != 1:
+            raise RuntimeError("libsagedp ABI mismatch")
+        _lib = L
+        return L
+
+
+_generation = 0
+
+
+def generation() -> int:
+    """Bumped by every sage_init: native handles from older generations are dead."""
+    return _generation
+
+
+def init(n_gpus: int = 1, pool_bytes: int = 0, staging_bytes: int = 0, chunk_bytes: int = 0,
+         flags: int = 0, host_threads: int | None = None) -> None:
+    global _generation
+    L = lib()
+    check(L.sage_set_host_threads(host_threads or host_threads_default()), "sage_set_host_threads")
+    check(L.sage_init(n_gpus, pool_bytes, staging_bytes, chunk_bytes, flags), "sage_init")
+    _generation += 1
+
+
+def shutdown() -> None:
+    global _generation
+    check(lib().sage_shutdown(), "sage_shutdown")
+    _generation += 1
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def last_error() -> str:
+    return (lib().sage_last_error() or b"").decode(errors="replace")
+
+
+def check(rc: int, what: str) -> int:
+    if rc < 0 and rc != SAGE_ENOTREADY:
+        raise SageError(rc, what, last_error())
+    return rc
+
+
+def handles(seq) -> tuple:
+    """(array pointer, count) for a sequence of handles (None-safe)."""
+    seq = [h for h in (seq or ()) if h]
+    if not seq:
+        return None, 0
+    arr = (H * len(seq))(*seq)
+    return arr, len(seq)
+
+
+def host_threads_default() -> int:
+    return max(2, min(8, (os.cpu_count() or 4) // 2))

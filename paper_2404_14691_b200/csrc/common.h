@@ -1,0 +1,157 @@
+// common.h — internals shared by the libsagedp translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/sage_dp.h"
+
+namespace sage {
+
+// ---------------------------------------------------------------- errors ----
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+int cu_fail(CUresult r, const char *what);
+
+#define SAGE_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e__ = (call);                             \
+    if (e__ != cudaSuccess) return ::sage::cuda_fail(e__, #call); \
+  } while (0)
+#define SAGE_CU(call)                                     \
+  do {                                                    \
+    CUresult r__ = (call);                                \
+    if (r__ != CUDA_SUCCESS) return ::sage::cu_fail(r__, #call); \
+  } while (0)
+#define SAGE_TRY(call)                                    \
+  do {                                                    \
+    int rc__ = (call);                                    \
+    if (rc__ != SAGE_OK) return rc__;                     \
+  } while (0)
+
+// ------------------------------------------------------- driver entry pts ---
+struct Driver {
+  PFN_cuMemCreate_v10020 MemCreate = nullptr;
+  PFN_cuMemRelease_v10020 MemRelease = nullptr;
+  PFN_cuMemAddressReserve_v10020 MemAddressReserve = nullptr;
+  PFN_cuMemAddressFree_v10020 MemAddressFree = nullptr;
+  PFN_cuMemMap_v10020 MemMap = nullptr;
+  PFN_cuMemUnmap_v10020 MemUnmap = nullptr;
+  PFN_cuMemSetAccess_v10020 MemSetAccess = nullptr;
+  PFN_cuMemGetAllocationGranularity_v10020 MemGetAllocationGranularity = nullptr;
+  PFN_cuCtxCreate_v3020 CtxCreate = nullptr;
+  PFN_cuCtxDestroy_v4000 CtxDestroy = nullptr;
+  PFN_cuCtxSetCurrent_v4000 CtxSetCurrent = nullptr;
+  PFN_cuCtxGetCurrent_v4000 CtxGetCurrent = nullptr;
+  PFN_cuDevicePrimaryCtxRetain_v7000 DevicePrimaryCtxRetain = nullptr;
+};
+extern Driver drv;
+int load_driver();
+
+// ------------------------------------------------------------------ clock ---
+int64_t host_now_us();   // CLOCK_MONOTONIC µs since sage_init
+
+// ---------------------------------------------------------------- handles ---
+enum class Kind : uint8_t { Event = 1, Slot, Alloc, Host, Layout, Load, Job };
+inline sage_handle make_handle(Kind k, uint64_t id) { return ((uint64_t)k << 56) | id; }
+inline Kind handle_kind(sage_handle h) { return (Kind)(h >> 56); }
+
+// --------------------------------------------------------------- events -----
+struct Event {
+  int gpu = -1;
+  cudaEvent_t ev = nullptr;      // device event (null for host jobs)
+  std::atomic<int> host_done{0}; // host job completion (FixedGSL)
+  int64_t host_time = -1;        // host job completion time
+  bool recorded = false;
+};
+int event_new(int gpu, sage_handle *h, Event **out);        // device event
+int event_new_host(sage_handle *h, Event **out);            // host-completed event
+Event *event_get(sage_handle h);
+int event_record(Event *e, cudaStream_t s);
+int event_time_us(Event *e, int64_t *t);                    // requires completion
+
+// --------------------------------------------------------------- per GPU ----
+struct Layout;
+
+struct ChunkScratch {  // per-load device accumulator + pinned result
+  unsigned long long *d_acc = nullptr;   // ring of accumulators on device
+  unsigned long long *h_res = nullptr;   // pinned mirror
+  uint32_t n = 0;
+  std::atomic<uint64_t> next{0};
+};
+
+struct Gpu {
+  int id = -1;
+  int sm_count = 0;
+  CUcontext primary = nullptr;
+  cudaStream_t copy = nullptr, land = nullptr, host = nullptr, d2h = nullptr, aux = nullptr;
+  std::vector<cudaStream_t> slots;        // pre-created stream pool (the "context pool")
+  std::vector<int> slot_free;             // free slot indices
+  std::mutex slot_mu;
+  // staging rings
+  uint32_t ring = 0;
+  uint64_t chunk = 0;
+  uint8_t *pin = nullptr;                 // ring * (chunk + 64) pinned
+  uint8_t *dstage = nullptr;              // ring * (chunk + 64) device
+  std::vector<cudaEvent_t> ev_cpu, ev_h2d, ev_land;  // per ring slot
+  uint64_t chunk_seq = 0;                 // global chunk sequence (ring position)
+  std::mutex load_mu;                     // serialises load enqueue (ring order)
+  ChunkScratch scratch;
+  // clock anchor
+  cudaEvent_t anchor = nullptr;
+  int64_t anchor_us = 0;
+  std::mutex anchor_mu;
+  // pool
+  struct Pool *pool = nullptr;
+  // misc scratch for checksum verify
+  unsigned long long *d_verify = nullptr;
+};
+
+struct State {
+  bool up = false;
+  int n_gpus = 0;
+  uint64_t chunk = 8ull << 20;
+  uint32_t flags = 0;
+  std::vector<std::unique_ptr<Gpu>> gpus;
+  int host_threads = 8;
+};
+extern State st;
+Gpu *gpu_get(int g);
+int require_up();
+
+// host memcpy fan-out pool (CPU_LOAD)
+void parallel_memcpy(void *dst, const void *src, size_t bytes);
+void pool_threads_start(int n);
+void pool_threads_stop();
+
+// pool internals (pool.cu)
+int pool_create(Gpu *g, uint64_t capacity);
+void pool_destroy(Gpu *g);
+
+// device state (pool.cu)
+int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chunk);
+void gpu_teardown(Gpu *G);
+int slot_stream(sage_handle h, Gpu **G, cudaStream_t *s);
+// bodies (bodies.cu)
+int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count);
+int touch_all_kernels();
+
+// layouts (land.cu)
+int layouts_destroy_all();
+
+}  // namespace sage

@@ -1,0 +1,763 @@
+// land.cu — segment layouts, the chunk planner, the sm_100a `land` kernel and
+// the load pipeline (CPU_LOAD memcpy -> H2D on the copy engine -> land).
+//
+// Replaces the CPU_LOAD -> GPU_LOAD chain of plan_invocation
+// (functions.py:257-268) and the fluid Channel it charged
+// (resources.py:82-234).  Byte semantics follow oracle/sage_oracle.c
+// (oracle_land / oracle_checksum); tests/ check bit-exactness.
+//
+// Data layout in HBM
+//   packed stream  P[0, packed)      tensors back to back (the DB record)
+//   landed segment S[0, seg)         tensor i at dst_off[i] (16-B aligned),
+//                                    zero padding up to the next extent
+//   device staging ring              `ring` slots of (chunk + 256) bytes; slot
+//                                    for chunk k holds P[sb_k, se_k) with
+//                                    sb_k = c_k - 16 (k > 0) so every 16-B
+//                                    destination vector assigned to chunk k
+//                                    finds all its source bytes in its slot.
+//
+// Work assignment: destination vector v (16 B) of tensor i is landed by the
+// chunk that holds its LAST source byte (padding vectors go with the tensor's
+// last data byte).  Per chunk that is one contiguous run of vectors per
+// tensor (an Item); the planner emits Items + a prefix sum of their lengths.
+#include "common.h"
+
+#include <algorithm>
+
+namespace sage {
+
+struct __align__(16) LandItem {
+  unsigned long long dst_vec0;  // first destination vector (segment relative)
+  long long src_rel0;           // source byte of that vector, relative to the slot base
+  long long data0;              // data bytes of the tensor from that vector on (<=0: padding)
+  unsigned int nvec;
+  unsigned int pad_;
+};
+
+struct ChunkPlan {
+  uint64_t sb = 0, se = 0;       // packed range held by the slot
+  uint32_t item_begin = 0, item_end = 0;
+  uint32_t prefix_begin = 0;     // index into prefix (item_end - item_begin + 1 entries)
+  uint32_t nvec = 0;
+};
+
+struct Plan {
+  uint64_t chunk = 0;
+  std::vector<ChunkPlan> chunks;
+  std::vector<LandItem> items;
+  std::vector<uint32_t> prefix;
+  // device copies per gpu
+  std::vector<LandItem *> d_items;
+  std::vector<uint32_t *> d_prefix;
+};
+
+struct Tensor { uint64_t src, dst, len, ext_end; };
+
+struct Layout {
+  std::vector<Tensor> t;
+  uint64_t packed = 0, seg = 0;
+  Plan chunked, whole;
+};
+
+static std::mutex g_lay_mu;
+static std::unordered_map<uint64_t, Layout *> g_layouts;
+static std::atomic<uint64_t> g_lay_next{1};
+
+// ------------------------------------------------------------- planner -----
+static uint64_t vec_key(const Tensor &T, uint64_t q) {
+  // last source byte needed by vector q of tensor T (T.len > 0)
+  uint64_t r = 16 * q;
+  uint64_t last = (r + 15 < T.len) ? r + 15 : T.len - 1;
+  return T.src + last;
+}
+
+// first vector q in [0, V) with key(q) >= c
+static uint64_t lower_vec(const Tensor &T, uint64_t V, uint64_t c) {
+  uint64_t lo = 0, hi = V;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) / 2;
+    if (vec_key(T, mid) >= c) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+static int build_plan(const Layout &L, uint64_t chunk, Plan *P) {
+  P->chunk = chunk;
+  P->chunks.clear(); P->items.clear(); P->prefix.clear();
+  uint64_t nchunks = L.packed == 0 ? 1 : (L.packed + chunk - 1) / chunk;
+  P->chunks.resize(nchunks);
+  for (uint64_t k = 0; k < nchunks; ++k) {
+    ChunkPlan &C = P->chunks[k];
+    uint64_t ck = k * chunk;
+    C.sb = k == 0 ? 0 : ck - 16;
+    C.se = std::min<uint64_t>(L.packed, (k + 1) * chunk);
+  }
+  // per chunk, collect items of every tensor
+  std::vector<std::vector<LandItem>> per(nchunks);
+  for (const Tensor &T : L.t) {
+    uint64_t V = (T.ext_end - T.dst) / 16;
+    if (V == 0) continue;
+    if (T.len == 0) {  // pure padding extent: chunk 0
+      LandItem I{T.dst / 16, 0, 0, (unsigned)V, 0};
+      per[0].push_back(I);
+      continue;
+    }
+    for (uint64_t k = 0; k < nchunks; ++k) {
+      uint64_t c0 = k * chunk, c1 = (k + 1 == nchunks) ? ~0ull : (k + 1) * chunk;
+      uint64_t qb = k == 0 ? 0 : lower_vec(T, V, c0);
+      uint64_t qe = (k + 1 == nchunks) ? V : lower_vec(T, V, c1);
+      if (qe <= qb) continue;
+      uint64_t sb = P->chunks[k].sb;
+      for (uint64_t q = qb; q < qe;) {  // split runs so nvec fits 32 bits
+        uint64_t n = std::min<uint64_t>(qe - q, 1u << 30);
+        LandItem I;
+        I.dst_vec0 = T.dst / 16 + q;
+        I.src_rel0 = (long long)(T.src + 16 * q) - (long long)sb;
+        I.data0 = (long long)T.len - (long long)(16 * q);
+        I.nvec = (unsigned)n;
+        I.pad_ = 0;
+        per[k].push_back(I);
+        q += n;
+      }
+      (void)c1;
+    }
+  }
+  for (uint64_t k = 0; k < nchunks; ++k) {
+    ChunkPlan &C = P->chunks[k];
+    C.item_begin = (uint32_t)P->items.size();
+    C.prefix_begin = (uint32_t)P->prefix.size();
+    uint64_t acc = 0;
+    P->prefix.push_back(0);
+    for (auto &I : per[k]) {
+      P->items.push_back(I);
+      acc += I.nvec;
+      if (acc > 0xFFFFFFF0ull) return fail(SAGE_EINVAL, "chunk too large for the land planner");
+      P->prefix.push_back((uint32_t)acc);
+    }
+    C.item_end = (uint32_t)P->items.size();
+    C.nvec = (uint32_t)acc;
+  }
+  return SAGE_OK;
+}
+
+static int plan_upload(Plan *P, int gpu) {
+  if ((int)P->d_items.size() <= gpu) { P->d_items.resize(gpu + 1, nullptr); P->d_prefix.resize(gpu + 1, nullptr); }
+  if (P->d_items[gpu]) return SAGE_OK;
+  cudaSetDevice(gpu);
+  size_t ni = std::max<size_t>(1, P->items.size()), np = std::max<size_t>(1, P->prefix.size());
+  SAGE_CUDA(cudaMalloc((void **)&P->d_items[gpu], ni * sizeof(LandItem)));
+  SAGE_CUDA(cudaMalloc((void **)&P->d_prefix[gpu], np * sizeof(uint32_t)));
+  if (!P->items.empty())
+    SAGE_CUDA(cudaMemcpy(P->d_items[gpu], P->items.data(), P->items.size() * sizeof(LandItem), cudaMemcpyHostToDevice));
+  SAGE_CUDA(cudaMemcpy(P->d_prefix[gpu], P->prefix.data(), P->prefix.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  return SAGE_OK;
+}
+
+static void plan_free(Plan *P) {
+  for (size_t g = 0; g < P->d_items.size(); ++g) {
+    if (P->d_items[g]) { cudaSetDevice((int)g); cudaFree(P->d_items[g]); }
+    if (P->d_prefix[g]) cudaFree(P->d_prefix[g]);
+  }
+  P->d_items.clear(); P->d_prefix.clear();
+}
+
+static int layout_build(const uint64_t *src_off, const uint64_t *dst_off, const uint64_t *len, uint32_t n,
+                        uint64_t packed, uint64_t seg, uint64_t chunk, Layout *L) {
+  if (seg % 16) return fail(SAGE_EINVAL, "layout: seg_bytes must be a multiple of 16");
+  if (n && (!src_off || !dst_off || !len)) return fail(SAGE_EINVAL, "layout: null arrays");
+  L->packed = packed;
+  L->seg = seg;
+  L->t.resize(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (dst_off[i] % 16) return fail(SAGE_EINVAL, "layout: dst_off must be 16-byte aligned");
+    if (i == 0 && dst_off[0] != 0) return fail(SAGE_EINVAL, "layout: dst_off[0] must be 0");
+    if (src_off[i] + len[i] < src_off[i] || src_off[i] + len[i] > packed)
+      return fail(SAGE_EINVAL, "layout: tensor exceeds the packed stream");
+    uint64_t lim = (i + 1 < n) ? dst_off[i + 1] : seg;
+    if (i + 1 < n && dst_off[i + 1] < dst_off[i]) return fail(SAGE_EINVAL, "layout: dst_off must ascend");
+    if (dst_off[i] + len[i] > lim) return fail(SAGE_EINVAL, "layout: tensor overlaps the next extent");
+    L->t[i] = Tensor{src_off[i], dst_off[i], len[i], lim};
+  }
+  if (n == 0 && seg) return fail(SAGE_EINVAL, "layout: empty layout must have seg_bytes == 0");
+  SAGE_TRY(build_plan(*L, chunk, &L->chunked));
+  SAGE_TRY(build_plan(*L, packed ? packed : 1, &L->whole));
+  return SAGE_OK;
+}
+
+static Layout *layout_get(sage_handle h) {
+  if (handle_kind(h) != Kind::Layout) return nullptr;
+  std::lock_guard<std::mutex> lk(g_lay_mu);
+  auto it = g_layouts.find(h & ((1ull << 56) - 1));
+  return it == g_layouts.end() ? nullptr : it->second;
+}
+
+static void identity_clear();
+int layouts_destroy_all() {
+  identity_clear();
+  std::lock_guard<std::mutex> lk(g_lay_mu);
+  for (auto &kv : g_layouts) {
+    plan_free(&kv.second->chunked);
+    plan_free(&kv.second->whole);
+    delete kv.second;
+  }
+  g_layouts.clear();
+  return SAGE_OK;
+}
+
+// ------------------------------------------------------------- kernels -----
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+  return h;
+}
+__device__ __forceinline__ unsigned long long word_term(uint32_t w, unsigned long long j) {
+  uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
+  uint32_t h = fmix32(w ^ k);
+  uint32_t g = (h ^ (h >> 15)) * 0x2C1B3C6Du;
+  return ((unsigned long long)g << 32) | h;
+}
+__device__ __forceinline__ unsigned long long vec_term(uint4 v, unsigned long long j0) {
+  return word_term(v.x, j0) + word_term(v.y, j0 + 1) + word_term(v.z, j0 + 2) + word_term(v.w, j0 + 3);
+}
+
+__device__ __forceinline__ uint32_t sel4(uint32_t ws, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return ws == 0 ? a : ws == 1 ? b : ws == 2 ? c : d;
+}
+// bytes [sh, sh + 16) of the 32-byte concatenation a|b
+__device__ __forceinline__ uint4 funnel16(uint4 a, uint4 b, uint32_t sh) {
+  uint32_t ws = sh >> 2, bs = (sh & 3u) * 8u;
+  uint32_t r0 = sel4(ws, a.x, a.y, a.z, a.w);
+  uint32_t r1 = sel4(ws, a.y, a.z, a.w, b.x);
+  uint32_t r2 = sel4(ws, a.z, a.w, b.x, b.y);
+  uint32_t r3 = sel4(ws, a.w, b.x, b.y, b.z);
+  uint32_t r4 = sel4(ws, b.x, b.y, b.z, b.w);
+  uint4 o;
+  o.x = __funnelshift_r(r0, r1, bs);
+  o.y = __funnelshift_r(r1, r2, bs);
+  o.z = __funnelshift_r(r2, r3, bs);
+  o.w = __funnelshift_r(r3, r4, bs);
+  return o;
+}
+__device__ __forceinline__ uint32_t keep_bytes(uint32_t w, long long nb) {
+  return nb >= 4 ? w : nb <= 0 ? 0u : (w & ((1u << (8 * (uint32_t)nb)) - 1u));
+}
+
+__device__ __forceinline__ void block_reduce_add(unsigned long long v, unsigned long long *out) {
+  __shared__ unsigned long long red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? red[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(out, v);
+  }
+}
+
+struct LandArgs {
+  const LandItem *items;
+  const uint32_t *prefix;  // n_items + 1 entries, chunk local
+  uint32_t n_items;
+  uint32_t total_vec;
+  const uint8_t *slot;     // 16-B aligned base holding packed [sb, se)
+  unsigned long long slot_bytes;  // se - sb (valid bytes)
+  uint8_t *dst;            // segment base (16-B aligned)
+  unsigned long long *acc; // checksum accumulator
+};
+
+constexpr int kLandThreads = 256;
+constexpr int kLandU = 4;  // vectors per lane per tile
+
+__global__ void __launch_bounds__(kLandThreads) land_kernel(const __grid_constant__ LandArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t tile = 32u * kLandU;
+  const uint8_t *slot_end = a.slot + a.slot_bytes;
+  unsigned long long acc = 0;
+  for (uint64_t t0 = (uint64_t)warp * tile; t0 < a.total_vec; t0 += (uint64_t)nwarps * tile) {
+    // warp-uniform binary search: last item with prefix <= t0
+    uint32_t lo = 0, hi = a.n_items;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(a.prefix + mid) <= t0) lo = mid; else hi = mid;
+    }
+    uint32_t it = lo;
+    uint32_t cur = __ldg(a.prefix + it), nxt = __ldg(a.prefix + it + 1);
+    LandItem I = a.items[it];
+    long long s[kLandU], d[kLandU];
+    unsigned long long dv[kLandU];
+    bool ok[kLandU];
+#pragma unroll
+    for (int u = 0; u < kLandU; ++u) {
+      uint32_t v = (uint32_t)t0 + u * 32u + lane;
+      ok[u] = v < a.total_vec;
+      if (ok[u]) {
+        while (v >= nxt) {  // crosses into the next run (rare: run boundaries)
+          ++it;
+          cur = nxt;
+          nxt = __ldg(a.prefix + it + 1);
+          I = a.items[it];
+        }
+        uint32_t loc = v - cur;
+        s[u] = I.src_rel0 + 16ll * loc;
+        d[u] = I.data0 - 16ll * loc;
+        dv[u] = I.dst_vec0 + loc;
+      } else {
+        s[u] = 0; d[u] = 0; dv[u] = 0;
+      }
+    }
+    uint4 A[kLandU], B[kLandU];
+#pragma unroll
+    for (int u = 0; u < kLandU; ++u) {
+      A[u] = make_uint4(0, 0, 0, 0);
+      B[u] = make_uint4(0, 0, 0, 0);
+      if (ok[u] && d[u] > 0) {
+        const uint8_t *p = a.slot + s[u];
+        const uint4 *q = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
+        A[u] = __ldg(q);
+        if ((reinterpret_cast<uintptr_t>(p) & 15) && reinterpret_cast<const uint8_t *>(q + 1) < slot_end)
+          B[u] = __ldg(q + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kLandU; ++u) {
+      if (!ok[u]) continue;
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (d[u] > 0) {
+        uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(a.slot + s[u]) & 15);
+        o = sh ? funnel16(A[u], B[u], sh) : A[u];
+        if (d[u] < 16) {
+          o.x = keep_bytes(o.x, d[u]);
+          o.y = keep_bytes(o.y, d[u] - 4);
+          o.z = keep_bytes(o.z, d[u] - 8);
+          o.w = keep_bytes(o.w, d[u] - 12);
+        }
+      }
+      reinterpret_cast<uint4 *>(a.dst)[dv[u]] = o;
+      acc += vec_term(o, dv[u] * 4ull);
+    }
+  }
+  block_reduce_add(acc, a.acc);
+}
+
+// checksum of a landed segment (verify / dedup): read-only pass
+__global__ void __launch_bounds__(256) checksum_kernel(const uint4 *__restrict__ p, unsigned long long nvec,
+                                                       unsigned long long *out) {
+  unsigned long long acc = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 v0 = __ldg(p + i), v1 = __ldg(p + i + stride), v2 = __ldg(p + i + 2 * stride), v3 = __ldg(p + i + 3 * stride);
+    acc += vec_term(v0, i * 4) + vec_term(v1, (i + stride) * 4) + vec_term(v2, (i + 2 * stride) * 4) +
+           vec_term(v3, (i + 3 * stride) * 4);
+  }
+  for (; i < nvec; i += stride) acc += vec_term(__ldg(p + i), i * 4);
+  block_reduce_add(acc, out);
+}
+
+static int land_grid(Gpu *G, uint32_t total_vec) {
+  uint64_t tiles = (total_vec + 32ull * kLandU - 1) / (32ull * kLandU);
+  uint64_t blocks = (tiles + (kLandThreads / 32) - 1) / (kLandThreads / 32);
+  uint64_t cap = (uint64_t)G->sm_count * 8;
+  return (int)std::max<uint64_t>(1, std::min(blocks, cap));
+}
+
+// --------------------------------------------------------------- loads -----
+struct Load {
+  int gpu = -1;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  std::atomic<int64_t> cpu_begin{-1}, cpu_end{-1};
+  uint64_t host_bytes = 0, link_bytes = 0, landed = 0;
+  uint32_t chunks = 0;
+  uint32_t acc_idx = 0;
+  bool has_gpu_begin = false;
+};
+
+static std::mutex g_load_mu;
+static std::unordered_map<uint64_t, Load *> g_loads;
+static std::atomic<uint64_t> g_load_next{1};
+
+struct HostCopyArg {
+  Load *L;
+  void *dst;
+  const void *src;
+  size_t bytes;
+};
+
+static void CUDART_CB host_copy_fn(void *p) {
+  auto *a = static_cast<HostCopyArg *>(p);
+  int64_t t0 = host_now_us();
+  int64_t expect = -1;
+  a->L->cpu_begin.compare_exchange_strong(expect, t0);
+  parallel_memcpy(a->dst, a->src, a->bytes);
+  a->L->cpu_end.store(host_now_us());
+  delete a;
+}
+
+static int raw_event_time(Gpu *G, cudaEvent_t ev, int64_t *t) {
+  std::lock_guard<std::mutex> lk(G->anchor_mu);
+  if (host_now_us() - G->anchor_us > 2000000) {
+    cudaSetDevice(G->id);
+    int64_t h0 = host_now_us();
+    SAGE_CUDA(cudaEventRecord(G->anchor, G->aux));
+    SAGE_CUDA(cudaEventSynchronize(G->anchor));
+    G->anchor_us = (h0 + host_now_us()) / 2;
+  }
+  float ms = 0.f;
+  SAGE_CUDA(cudaEventElapsedTime(&ms, G->anchor, ev));
+  *t = G->anchor_us + (int64_t)llround((double)ms * 1000.0);
+  return SAGE_OK;
+}
+
+static int wait_list(cudaStream_t s, const sage_handle *w, int n) {
+  for (int i = 0; i < n; ++i) {
+    Event *e = event_get(w[i]);
+    if (!e) return fail(SAGE_ESTATE, "load: unknown wait event");
+    if (!e->ev) {
+      while (!e->host_done.load()) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      continue;
+    }
+    if (!e->recorded) return fail(SAGE_ESTATE, "load: wait on an unrecorded event");
+    SAGE_CUDA(cudaStreamWaitEvent(s, e->ev, 0));
+  }
+  return SAGE_OK;
+}
+
+static int enqueue_land(Gpu *G, const Plan &P, const ChunkPlan &C, int gpu, const uint8_t *slot,
+                        uint8_t *dst, unsigned long long *acc) {
+  if (C.nvec == 0) return SAGE_OK;
+  LandArgs a;
+  a.items = P.d_items[gpu] + C.item_begin;
+  a.prefix = P.d_prefix[gpu] + C.prefix_begin;
+  a.n_items = C.item_end - C.item_begin;
+  a.total_vec = C.nvec;
+  a.slot = slot;
+  a.slot_bytes = C.se - C.sb;
+  a.dst = dst;
+  a.acc = acc;
+  land_kernel<<<land_grid(G, C.nvec), kLandThreads, 0, G->land>>>(a);
+  SAGE_CUDA(cudaGetLastError());
+  return SAGE_OK;
+}
+
+int layout_tensors(sage_handle h, std::vector<uint64_t> *src, std::vector<uint64_t> *dst,
+                   std::vector<uint64_t> *len, uint64_t *packed, uint64_t *seg) {
+  Layout *L = layout_get(h);
+  if (!L) return fail(SAGE_ESTATE, "unknown layout");
+  for (const Tensor &T : L->t) { src->push_back(T.src); dst->push_back(T.dst); len->push_back(T.len); }
+  *packed = L->packed;
+  *seg = L->seg;
+  return SAGE_OK;
+}
+
+// identity layouts (input payloads, cache reloads, fan-out) are cached by size
+static std::mutex g_ident_mu;
+static std::unordered_map<uint64_t, Layout *> g_ident;
+static int identity_layout(uint64_t bytes, Layout **out) {
+  std::lock_guard<std::mutex> lk(g_ident_mu);
+  auto it = g_ident.find(bytes);
+  if (it != g_ident.end()) { *out = it->second; return SAGE_OK; }
+  auto *lay = new Layout();
+  uint64_t z = 0, n = bytes;
+  int rc = layout_build(&z, &z, &n, bytes ? 1u : 0u, bytes, (bytes + 15) & ~15ull, st.chunk, lay);
+  for (int g = 0; rc == SAGE_OK && g < st.n_gpus; ++g) {
+    rc = plan_upload(&lay->chunked, g);
+    if (rc == SAGE_OK) rc = plan_upload(&lay->whole, g);
+  }
+  if (rc != SAGE_OK) { plan_free(&lay->chunked); plan_free(&lay->whole); delete lay; return rc; }
+  g_ident[bytes] = lay;
+  *out = lay;
+  return SAGE_OK;
+}
+static void identity_clear() {
+  std::lock_guard<std::mutex> lk(g_ident_mu);
+  for (auto &kv : g_ident) { plan_free(&kv.second->chunked); plan_free(&kv.second->whole); delete kv.second; }
+  g_ident.clear();
+}
+
+}  // namespace sage
+
+using namespace sage;
+
+extern "C" {
+
+int sage_layout_create(const uint64_t *src_off, const uint64_t *dst_off, const uint64_t *len, uint32_t n,
+                       uint64_t packed_bytes, uint64_t seg_bytes, sage_handle *layout) {
+  if (!layout) return fail(SAGE_EINVAL, "layout_create: null out");
+  auto *L = new Layout();
+  int rc = layout_build(src_off, dst_off, len, n, packed_bytes, seg_bytes, st.up ? st.chunk : (8ull << 20), L);
+  if (rc != SAGE_OK) { delete L; return rc; }
+  if (st.up) {
+    for (int g = 0; g < st.n_gpus; ++g) {
+      rc = plan_upload(&L->chunked, g);
+      if (rc == SAGE_OK) rc = plan_upload(&L->whole, g);
+      if (rc != SAGE_OK) { plan_free(&L->chunked); plan_free(&L->whole); delete L; return rc; }
+    }
+  }
+  uint64_t id = g_lay_next++;
+  {
+    std::lock_guard<std::mutex> lk(g_lay_mu);
+    g_layouts[id] = L;
+  }
+  *layout = make_handle(Kind::Layout, id);
+  return SAGE_OK;
+}
+
+int sage_layout_destroy(sage_handle h) {
+  if (handle_kind(h) != Kind::Layout) return fail(SAGE_EINVAL, "not a layout handle");
+  Layout *L = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_lay_mu);
+    auto it = g_layouts.find(h & ((1ull << 56) - 1));
+    if (it == g_layouts.end()) return fail(SAGE_ESTATE, "double or unknown layout destroy");
+    L = it->second;
+    g_layouts.erase(it);
+  }
+  plan_free(&L->chunked);
+  plan_free(&L->whole);
+  delete L;
+  return SAGE_OK;
+}
+
+int sage_layout_chunks(sage_handle h, uint32_t *n) {
+  Layout *L = layout_get(h);
+  if (!L || !n) return fail(SAGE_ESTATE, "unknown layout");
+  *n = (uint32_t)L->chunked.chunks.size();
+  return SAGE_OK;
+}
+
+int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev) {
+  SAGE_TRY(require_up());
+  if (!d || !load_out || !end_ev) return fail(SAGE_EINVAL, "segment_load: null argument");
+  Gpu *G = gpu_get(d->gpu);
+  if (!G) return fail(SAGE_ENODEV, "segment_load: bad gpu");
+  if (!d->dst) return fail(SAGE_EINVAL, "segment_load: null dst");
+  if (d->src_bytes && !d->src) return fail(SAGE_EINVAL, "segment_load: null src");
+  const bool dev_src = (d->flags & (SAGE_LOAD_SRC_DEVICE | SAGE_LOAD_SRC_PEER)) != 0;
+  if (dev_src && (reinterpret_cast<uintptr_t>(d->src) & 15))
+    return fail(SAGE_EINVAL, "segment_load: device source must be 16-byte aligned");
+  if ((d->flags & SAGE_LOAD_SRC_PEER) && !gpu_get(d->src_gpu))
+    return fail(SAGE_ENODEV, "segment_load: bad src_gpu");
+  if (d->dst & 15) return fail(SAGE_EINVAL, "segment_load: dst must be 16-byte aligned");
+  cudaSetDevice(d->gpu);
+
+  auto *L = new Load();
+  L->gpu = d->gpu;
+  Layout *lay = nullptr;
+  if (d->layout) {
+    lay = layout_get(d->layout);
+    if (!lay) { delete L; return fail(SAGE_ESTATE, "segment_load: unknown layout"); }
+    if (lay->packed != d->src_bytes) { delete L; return fail(SAGE_EINVAL, "segment_load: src_bytes != layout packed_bytes"); }
+  } else {
+    // identity layout: dst receives the packed bytes verbatim, padded to 16
+    int rc = identity_layout(d->src_bytes, &lay);
+    if (rc != SAGE_OK) { delete L; return rc; }
+  }
+  {
+    int rc = plan_upload(&lay->chunked, d->gpu);
+    if (rc == SAGE_OK) rc = plan_upload(&lay->whole, d->gpu);
+    if (rc != SAGE_OK) { delete L; return rc; }
+  }
+  cudaError_t ce;
+  if ((ce = cudaEventCreate(&L->ev_begin)) != cudaSuccess || (ce = cudaEventCreate(&L->ev_end)) != cudaSuccess) {
+    delete L;
+    return cuda_fail(ce, "cudaEventCreate");
+  }
+  Event *E;
+  {
+    int rc = event_new(d->gpu, end_ev, &E);
+    if (rc != SAGE_OK) { delete L; return rc; }
+  }
+  L->landed = lay->seg;
+  L->acc_idx = (uint32_t)(G->scratch.next++ % G->scratch.n);
+  unsigned long long *acc = G->scratch.d_acc + L->acc_idx;
+  uint8_t *dst = reinterpret_cast<uint8_t *>(d->dst);
+
+  std::lock_guard<std::mutex> lk(G->load_mu);  // ring order == enqueue order
+  int rc = SAGE_OK;
+  // the land stream owns the accumulator; user waits gate the first copy/land
+  if ((rc = wait_list(G->land, d->wait, d->n_wait)) != SAGE_OK) return rc;
+  SAGE_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), G->land));
+  if (dev_src) {
+    // HBM-resident (or peer, over NVLink) source: one land over the whole plan
+    SAGE_CUDA(cudaEventRecord(L->ev_begin, G->land));
+    L->has_gpu_begin = true;
+    const Plan &P = lay->whole;
+    L->chunks = (uint32_t)P.chunks.size();
+    if (d->flags & SAGE_LOAD_SRC_PEER) L->link_bytes = d->src_bytes;
+    rc = enqueue_land(G, P, P.chunks[0], d->gpu, static_cast<const uint8_t *>(d->src), dst, acc);
+    if (rc != SAGE_OK) return rc;
+  } else {
+    const Plan &P = lay->chunked;
+    const bool pinned = (d->flags & SAGE_LOAD_SRC_PINNED) != 0;
+    const uint64_t slot_bytes = G->chunk + 256;
+    if ((rc = wait_list(G->copy, d->wait, d->n_wait)) != SAGE_OK) return rc;
+    if (!pinned && (rc = wait_list(G->host, d->wait, d->n_wait)) != SAGE_OK) return rc;
+    L->chunks = (uint32_t)P.chunks.size();
+    for (size_t k = 0; k < P.chunks.size(); ++k) {
+      const ChunkPlan &C = P.chunks[k];
+      const uint64_t n = C.se - C.sb;
+      const uint32_t r = (uint32_t)(G->chunk_seq++ % G->ring);
+      uint8_t *dslot = G->dstage + r * slot_bytes;
+      uint8_t *pslot = G->pin + r * slot_bytes;
+      const uint8_t *src = static_cast<const uint8_t *>(d->src) + C.sb;
+      if (n) {
+        if (!pinned) {
+          // CPU_LOAD: DB record -> pinned staging, once the slot's last H2D is done
+          SAGE_CUDA(cudaStreamWaitEvent(G->host, G->ev_h2d[r], 0));
+          SAGE_CUDA(cudaLaunchHostFunc(G->host, host_copy_fn, new HostCopyArg{L, pslot, src, (size_t)n}));
+          SAGE_CUDA(cudaEventRecord(G->ev_cpu[r], G->host));
+          SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_cpu[r], 0));
+          L->host_bytes += n;
+        }
+        // GPU_LOAD: H2D into the device slot once its last land is done
+        SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_land[r], 0));
+        if (!L->has_gpu_begin) { SAGE_CUDA(cudaEventRecord(L->ev_begin, G->copy)); L->has_gpu_begin = true; }
+        SAGE_CUDA(cudaMemcpyAsync(dslot, pinned ? src : pslot, n, cudaMemcpyHostToDevice, G->copy));
+        SAGE_CUDA(cudaEventRecord(G->ev_h2d[r], G->copy));
+        SAGE_CUDA(cudaStreamWaitEvent(G->land, G->ev_h2d[r], 0));
+        L->link_bytes += n;
+      } else if (!L->has_gpu_begin) {
+        SAGE_CUDA(cudaEventRecord(L->ev_begin, G->land));
+        L->has_gpu_begin = true;
+      }
+      if ((rc = enqueue_land(G, P, C, d->gpu, dslot, dst, acc)) != SAGE_OK) return rc;
+      SAGE_CUDA(cudaEventRecord(G->ev_land[r], G->land));
+    }
+  }
+  SAGE_CUDA(cudaMemcpyAsync(G->scratch.h_res + L->acc_idx, acc, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            G->land));
+  SAGE_CUDA(cudaEventRecord(L->ev_end, G->land));
+  if ((rc = event_record(E, G->land)) != SAGE_OK) return rc;
+  uint64_t id = g_load_next++;
+  {
+    std::lock_guard<std::mutex> lk2(g_load_mu);
+    g_loads[id] = L;
+  }
+  *load_out = make_handle(Kind::Load, id);
+  return SAGE_OK;
+}
+
+int sage_load_info_get(sage_handle h, sage_load_info *out) {
+  if (handle_kind(h) != Kind::Load || !out) return fail(SAGE_EINVAL, "not a load handle");
+  Load *L;
+  {
+    std::lock_guard<std::mutex> lk(g_load_mu);
+    auto it = g_loads.find(h & ((1ull << 56) - 1));
+    if (it == g_loads.end()) return fail(SAGE_ESTATE, "unknown load handle");
+    L = it->second;
+  }
+  cudaSetDevice(L->gpu);
+  cudaError_t q = cudaEventQuery(L->ev_end);
+  if (q == cudaErrorNotReady) return SAGE_ENOTREADY;
+  if (q != cudaSuccess) return cuda_fail(q, "load end event");
+  Gpu *G = gpu_get(L->gpu);
+  memset(out, 0, sizeof *out);
+  out->cpu_begin_us = L->cpu_begin.load();
+  out->cpu_end_us = L->cpu_end.load();
+  SAGE_TRY(raw_event_time(G, L->ev_begin, &out->gpu_begin_us));
+  SAGE_TRY(raw_event_time(G, L->ev_end, &out->gpu_end_us));
+  out->host_bytes = L->host_bytes;
+  out->link_bytes = L->link_bytes;
+  out->landed_bytes = L->landed;
+  out->checksum = G->scratch.h_res[L->acc_idx];
+  out->chunks = L->chunks;
+  out->status = SAGE_OK;
+  return SAGE_OK;
+}
+
+int sage_load_release(sage_handle h) {
+  if (handle_kind(h) != Kind::Load) return fail(SAGE_EINVAL, "not a load handle");
+  Load *L;
+  {
+    std::lock_guard<std::mutex> lk(g_load_mu);
+    auto it = g_loads.find(h & ((1ull << 56) - 1));
+    if (it == g_loads.end()) return fail(SAGE_ESTATE, "double or unknown load release");
+    L = it->second;
+    g_loads.erase(it);
+  }
+  cudaSetDevice(L->gpu);
+  cudaEventSynchronize(L->ev_end);  // host copies reference L until the end
+  cudaEventDestroy(L->ev_begin);
+  cudaEventDestroy(L->ev_end);
+  delete L;
+  return SAGE_OK;
+}
+
+int sage_segment_checksum(int gpu, uint64_t dptr, uint64_t bytes, uint64_t *checksum) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || !checksum) return fail(SAGE_EINVAL, "segment_checksum: bad argument");
+  if ((dptr & 15) || (bytes & 15)) return fail(SAGE_EINVAL, "segment_checksum: needs 16-byte alignment");
+  cudaSetDevice(gpu);
+  std::lock_guard<std::mutex> lk(G->load_mu);
+  SAGE_CUDA(cudaMemsetAsync(G->d_verify, 0, 8, G->aux));
+  uint64_t nvec = bytes / 16;
+  if (nvec) {
+    int blocks = (int)std::min<uint64_t>((nvec + 1023) / 1024, (uint64_t)G->sm_count * 8);
+    checksum_kernel<<<std::max(1, blocks), 256, 0, G->aux>>>(reinterpret_cast<const uint4 *>(dptr), nvec,
+                                                             G->d_verify);
+    SAGE_CUDA(cudaGetLastError());
+  }
+  unsigned long long v = 0;
+  SAGE_CUDA(cudaMemcpyAsync(&v, G->d_verify, 8, cudaMemcpyDeviceToHost, G->aux));
+  SAGE_CUDA(cudaStreamSynchronize(G->aux));
+  *checksum = v;
+  return SAGE_OK;
+}
+
+// Test-only: run the chunk planner and the land semantics on the host, exactly
+// as the kernel consumes them (slot conventions included), without a GPU.
+int sage_debug_emulate_land(sage_handle h, const void *packed, uint64_t packed_bytes, void *seg_out,
+                            uint64_t chunk_bytes, uint64_t *checksum) {
+  Layout *L0 = layout_get(h);
+  if (!L0 || !seg_out || !checksum) return fail(SAGE_EINVAL, "emulate: bad argument");
+  if (packed_bytes != L0->packed) return fail(SAGE_EINVAL, "emulate: packed size mismatch");
+  Plan P;
+  SAGE_TRY(build_plan(*L0, chunk_bytes ? chunk_bytes : L0->chunked.chunk, &P));
+  const uint8_t *pk = static_cast<const uint8_t *>(packed);
+  uint8_t *out = static_cast<uint8_t *>(seg_out);
+  std::vector<uint8_t> written(L0->seg / 16, 0);
+  uint64_t sum = 0;
+  std::vector<uint8_t> slot;
+  for (const ChunkPlan &C : P.chunks) {
+    slot.assign(C.se - C.sb + 32, 0xCD);  // garbage beyond the valid range must never leak
+    memcpy(slot.data(), pk + C.sb, C.se - C.sb);
+    for (uint32_t i = C.item_begin; i < C.item_end; ++i) {
+      const LandItem &I = P.items[i];
+      for (uint32_t loc = 0; loc < I.nvec; ++loc) {
+        long long s = I.src_rel0 + 16ll * loc, dd = I.data0 - 16ll * loc;
+        uint64_t dv = I.dst_vec0 + loc;
+        uint8_t v[16] = {0};
+        for (int b = 0; b < 16 && b < dd; ++b) {
+          long long idx = s + b;
+          if (idx < 0 || (uint64_t)idx >= C.se - C.sb) return fail(SAGE_ESTATE, "emulate: slot overrun");
+          v[b] = slot[idx];
+        }
+        if (dv >= written.size() || written[dv]) return fail(SAGE_ESTATE, "emulate: vector landed twice");
+        written[dv] = 1;
+        memcpy(out + dv * 16, v, 16);
+        for (int w = 0; w < 4; ++w) {
+          uint32_t x;
+          memcpy(&x, v + 4 * w, 4);
+          uint64_t j = dv * 4 + w;
+          uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
+          uint32_t hh = x ^ k;
+          hh ^= hh >> 16; hh *= 0x85EBCA6Bu; hh ^= hh >> 13; hh *= 0xC2B2AE35u; hh ^= hh >> 16;
+          uint32_t g = (hh ^ (hh >> 15)) * 0x2C1B3C6Du;
+          sum += ((uint64_t)g << 32) | hh;
+        }
+      }
+    }
+  }
+  for (size_t v = 0; v < written.size(); ++v)
+    if (!written[v]) return fail(SAGE_ESTATE, "emulate: vector never landed");
+  *checksum = sum;
+  return SAGE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+// pool.cu — per-GPU device state and the VMM segment pool.
+//
+// Replaces MemoryLedger (resources.py:271-337): a capacity-checked ledger with
+// the reference's rounding rule (round_up_umb, resources.py:36-40; 1024 MB for
+// FixedGSL, exact otherwise) and its Denied-with-shortfall refusal
+// (resources.py:244-257, 309-315).  Unlike the model, every non-account-only
+// allocation is real HBM: a cuMemCreate physical allocation mapped with
+// cuMemMap/cuMemSetAccess into a reserved VA range.  Physical handles of freed
+// segments are cached by size so steady-state churn never calls cuMemCreate.
+#include "common.h"
+
+#include <map>
+
+namespace sage {
+
+struct Alloc {
+  int gpu = -1;
+  uint64_t bytes = 0, eff = 0, phys = 0;
+  int cls = 0;
+  bool account_only = false;
+  CUdeviceptr va = 0;
+  CUmemGenericAllocationHandle ph = 0;
+};
+
+struct Pool {
+  std::mutex mu;
+  uint64_t capacity = 0, granularity = 0, usage = 0, by_class[4] = {0, 0, 0, 0};
+  uint64_t physical = 0;   // mapped bytes
+  uint64_t cached = 0;     // bytes held by the free-handle cache
+  uint64_t vmm_gran = 2ull << 20;
+  std::multimap<uint64_t, CUmemGenericAllocationHandle> free_phys;
+};
+
+static std::mutex g_alloc_mu;
+static std::unordered_map<uint64_t, Alloc *> g_allocs;
+static std::atomic<uint64_t> g_alloc_next{1};
+
+static uint64_t round_up(uint64_t v, uint64_t g) { return g ? (v + g - 1) / g * g : v; }
+
+int pool_create(Gpu *G, uint64_t capacity) {
+  auto *P = new Pool();
+  P->capacity = capacity;
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = G->id;
+  size_t gran = 0;
+  SAGE_CU(drv.MemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  if (gran) P->vmm_gran = gran;
+  G->pool = P;
+  return SAGE_OK;
+}
+
+static void release_cache(Pool *P) {
+  for (auto &kv : P->free_phys) drv.MemRelease(kv.second);
+  P->free_phys.clear();
+  P->cached = 0;
+}
+
+void pool_destroy(Gpu *G) {
+  Pool *P = G->pool;
+  if (!P) return;
+  std::vector<uint64_t> mine;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    for (auto &kv : g_allocs)
+      if (kv.second->gpu == G->id) mine.push_back(kv.first);
+  }
+  for (uint64_t id : mine) sage_pool_free(make_handle(Kind::Alloc, id));
+  release_cache(P);
+  delete P;
+  G->pool = nullptr;
+}
+
+static int map_segment(Gpu *G, Pool *P, Alloc *A) {
+  A->phys = round_up(A->bytes, P->vmm_gran);
+  // reuse a cached physical handle of exactly this size
+  {
+    auto it = P->free_phys.find(A->phys);
+    if (it != P->free_phys.end()) {
+      A->ph = it->second;
+      P->free_phys.erase(it);
+      P->cached -= A->phys;
+    }
+  }
+  if (!A->ph) {
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = G->id;
+    CUresult r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
+    if (r == CUDA_ERROR_OUT_OF_MEMORY && P->cached) {
+      release_cache(P);
+      r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
+    }
+    if (r != CUDA_SUCCESS) { A->ph = 0; return cu_fail(r, "cuMemCreate"); }
+  }
+  CUresult r = drv.MemAddressReserve(&A->va, A->phys, P->vmm_gran, 0, 0);
+  if (r != CUDA_SUCCESS) { drv.MemRelease(A->ph); A->ph = 0; return cu_fail(r, "cuMemAddressReserve"); }
+  r = drv.MemMap(A->va, A->phys, 0, A->ph, 0);
+  if (r != CUDA_SUCCESS) {
+    drv.MemAddressFree(A->va, A->phys); drv.MemRelease(A->ph); A->ph = 0; A->va = 0;
+    return cu_fail(r, "cuMemMap");
+  }
+  std::vector<CUmemAccessDesc> acc;
+  int ngpu = (st.flags & SAGE_INIT_PEER_ACCESS) ? st.n_gpus : 1;
+  for (int d = 0; d < ngpu; ++d) {
+    CUmemAccessDesc a{};
+    a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    a.location.id = (ngpu == 1) ? G->id : d;
+    a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    acc.push_back(a);
+  }
+  r = drv.MemSetAccess(A->va, A->phys, acc.data(), acc.size());
+  if (r != CUDA_SUCCESS) {
+    drv.MemUnmap(A->va, A->phys); drv.MemAddressFree(A->va, A->phys); drv.MemRelease(A->ph);
+    A->ph = 0; A->va = 0;
+    return cu_fail(r, "cuMemSetAccess");
+  }
+  P->physical += A->phys;
+  return SAGE_OK;
+}
+
+static void unmap_segment(Pool *P, Alloc *A) {
+  if (!A->va) return;
+  drv.MemUnmap(A->va, A->phys);
+  drv.MemAddressFree(A->va, A->phys);
+  P->physical -= A->phys;
+  // keep the physical pages for reuse while the cache stays within budget
+  if (P->cached + A->phys + P->physical <= P->capacity + (4ull << 30)) {
+    P->free_phys.emplace(A->phys, A->ph);
+    P->cached += A->phys;
+  } else {
+    drv.MemRelease(A->ph);
+  }
+  A->va = 0;
+  A->ph = 0;
+}
+
+// ------------------------------------------------------------- device state -
+int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chunk) {
+  Gpu *G = st.gpus[id].get();
+  G->id = id;
+  SAGE_CUDA(cudaSetDevice(id));
+  SAGE_CUDA(cudaFree(0));  // create/retain the primary context up front (the pre-created ctx)
+  SAGE_CUDA(cudaDeviceGetAttribute(&G->sm_count, cudaDevAttrMultiProcessorCount, id));
+  SAGE_CU(drv.CtxGetCurrent(&G->primary));
+  int lo = 0, hi = 0;
+  SAGE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  SAGE_CUDA(cudaStreamCreateWithPriority(&G->copy, cudaStreamNonBlocking, hi));
+  SAGE_CUDA(cudaStreamCreateWithPriority(&G->land, cudaStreamNonBlocking, hi));
+  SAGE_CUDA(cudaStreamCreateWithFlags(&G->host, cudaStreamNonBlocking));
+  SAGE_CUDA(cudaStreamCreateWithFlags(&G->d2h, cudaStreamNonBlocking));
+  SAGE_CUDA(cudaStreamCreateWithFlags(&G->aux, cudaStreamNonBlocking));
+  const int kSlots = 64;
+  for (int i = 0; i < kSlots; ++i) {
+    cudaStream_t s;
+    SAGE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    G->slots.push_back(s);
+    G->slot_free.push_back(kSlots - 1 - i);
+  }
+  // staging rings: pinned host + device, `ring` slots of (chunk + 64) bytes
+  G->chunk = chunk;
+  G->ring = (uint32_t)std::max<uint64_t>(2, staging_bytes / chunk);
+  const uint64_t slot_bytes = chunk + 256;
+  SAGE_CUDA(cudaHostAlloc((void **)&G->pin, G->ring * slot_bytes, cudaHostAllocPortable));
+  SAGE_CUDA(cudaMalloc((void **)&G->dstage, G->ring * slot_bytes));
+  G->ev_cpu.resize(G->ring);
+  G->ev_h2d.resize(G->ring);
+  G->ev_land.resize(G->ring);
+  for (uint32_t i = 0; i < G->ring; ++i) {
+    SAGE_CUDA(cudaEventCreateWithFlags(&G->ev_cpu[i], cudaEventDisableTiming));
+    SAGE_CUDA(cudaEventCreateWithFlags(&G->ev_h2d[i], cudaEventDisableTiming));
+    SAGE_CUDA(cudaEventCreateWithFlags(&G->ev_land[i], cudaEventDisableTiming));
+  }
+  // checksum accumulators: one per in-flight load
+  G->scratch.n = 4096;
+  SAGE_CUDA(cudaMalloc((void **)&G->scratch.d_acc, G->scratch.n * sizeof(unsigned long long)));
+  SAGE_CUDA(cudaHostAlloc((void **)&G->scratch.h_res, G->scratch.n * sizeof(unsigned long long),
+                          cudaHostAllocPortable));
+  SAGE_CUDA(cudaMalloc((void **)&G->d_verify, 64));
+  // clock anchor
+  SAGE_CUDA(cudaEventCreate(&G->anchor));
+  int64_t h0 = host_now_us();
+  SAGE_CUDA(cudaEventRecord(G->anchor, G->aux));
+  SAGE_CUDA(cudaEventSynchronize(G->anchor));
+  G->anchor_us = (h0 + host_now_us()) / 2;
+  if (pool_bytes == 0) {
+    size_t fr = 0, tot = 0;
+    SAGE_CUDA(cudaMemGetInfo(&fr, &tot));
+    pool_bytes = fr > (4ull << 30) ? fr - (4ull << 30) : fr / 2;
+  }
+  return pool_create(G, pool_bytes);
+}
+
+void gpu_teardown(Gpu *G) {
+  cudaSetDevice(G->id);
+  pool_destroy(G);
+  for (auto s : G->slots) cudaStreamDestroy(s);
+  G->slots.clear();
+  for (cudaStream_t s : {G->copy, G->land, G->host, G->d2h, G->aux})
+    if (s) cudaStreamDestroy(s);
+  for (auto e : G->ev_cpu) cudaEventDestroy(e);
+  for (auto e : G->ev_h2d) cudaEventDestroy(e);
+  for (auto e : G->ev_land) cudaEventDestroy(e);
+  if (G->anchor) cudaEventDestroy(G->anchor);
+  if (G->pin) cudaFreeHost(G->pin);
+  if (G->dstage) cudaFree(G->dstage);
+  if (G->scratch.d_acc) cudaFree(G->scratch.d_acc);
+  if (G->scratch.h_res) cudaFreeHost(G->scratch.h_res);
+  if (G->d_verify) cudaFree(G->d_verify);
+}
+
+}  // namespace sage
+
+using namespace sage;
+
+extern "C" {
+
+int sage_pool_configure(int gpu, uint64_t capacity, uint64_t granularity) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G) return fail(SAGE_ENODEV, "pool_configure: bad gpu");
+  Pool *P = G->pool;
+  std::lock_guard<std::mutex> lk(P->mu);
+  if (capacity && capacity < P->usage) return fail(SAGE_EINVAL, "capacity below current usage");
+  if (capacity) P->capacity = capacity;
+  P->granularity = granularity;
+  return SAGE_OK;
+}
+
+int sage_pool_effective(int gpu, uint64_t bytes, uint64_t *effective) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || !effective) return fail(SAGE_EINVAL, "pool_effective: bad argument");
+  *effective = round_up(bytes, G->pool->granularity);
+  return SAGE_OK;
+}
+
+int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *dptr, uint64_t *shortfall) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G) return fail(SAGE_ENODEV, "pool_alloc: bad gpu");
+  if (!h) return fail(SAGE_EINVAL, "pool_alloc: null handle out");
+  if (bytes == 0) return fail(SAGE_EINVAL, "pool_alloc: allocation size must be > 0");
+  bool acct = (cls & SAGE_ALLOC_ACCOUNT_ONLY) != 0;
+  int c = cls & 0xff;
+  if (c < 0 || c > 3) return fail(SAGE_EINVAL, "pool_alloc: bad class");
+  Pool *P = G->pool;
+  auto *A = new Alloc();
+  A->gpu = gpu;
+  A->bytes = bytes;
+  A->cls = c;
+  A->account_only = acct;
+  {
+    std::lock_guard<std::mutex> lk(P->mu);
+    A->eff = round_up(bytes, P->granularity);
+    if (A->eff > P->capacity - P->usage) {
+      if (shortfall) *shortfall = A->eff - (P->capacity - P->usage);
+      delete A;
+      return fail(SAGE_ENOMEM, "pool budget exceeded");
+    }
+    if (!acct) {
+      cudaSetDevice(gpu);
+      int rc = map_segment(G, P, A);
+      if (rc != SAGE_OK) { delete A; return rc; }
+    }
+    P->usage += A->eff;
+    P->by_class[c] += A->eff;
+  }
+  uint64_t id = g_alloc_next++;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_allocs[id] = A;
+  }
+  *h = make_handle(Kind::Alloc, id);
+  if (dptr) *dptr = (uint64_t)A->va;
+  if (shortfall) *shortfall = 0;
+  return SAGE_OK;
+}
+
+int sage_pool_free(sage_handle h) {
+  if (handle_kind(h) != Kind::Alloc) return fail(SAGE_EINVAL, "not a pool handle");
+  Alloc *A = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_allocs.find(h & ((1ull << 56) - 1));
+    if (it == g_allocs.end()) return fail(SAGE_ESTATE, "double or unknown free");
+    A = it->second;
+    g_allocs.erase(it);
+  }
+  Gpu *G = gpu_get(A->gpu);
+  Pool *P = G->pool;
+  {
+    std::lock_guard<std::mutex> lk(P->mu);
+    if (!A->account_only) {
+      // contract: the caller frees only after the END events of every op that
+      // touched the segment completed (the runtime frees on invocation
+      // completion / decay), so no device-wide drain is needed here
+      cudaSetDevice(A->gpu);
+      unmap_segment(P, A);
+    }
+    P->usage -= A->eff;
+    P->by_class[A->cls] -= A->eff;
+  }
+  delete A;
+  return SAGE_OK;
+}
+
+int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total, uint64_t *physical_total,
+                    uint64_t *capacity) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G) return fail(SAGE_ENODEV, "pool_usage: bad gpu");
+  Pool *P = G->pool;
+  std::lock_guard<std::mutex> lk(P->mu);
+  if (by_class) for (int i = 0; i < 4; ++i) by_class[i] = P->by_class[i];
+  if (ledger_total) *ledger_total = P->usage;
+  if (physical_total) *physical_total = P->physical;
+  if (capacity) *capacity = P->capacity;
+  return SAGE_OK;
+}
+
+int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes) {
+  if (handle_kind(h) != Kind::Alloc) return fail(SAGE_EINVAL, "not a pool handle");
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  auto it = g_allocs.find(h & ((1ull << 56) - 1));
+  if (it == g_allocs.end()) return fail(SAGE_ESTATE, "unknown pool handle");
+  if (dptr) *dptr = (uint64_t)it->second->va;
+  if (bytes) *bytes = it->second->bytes;
+  return SAGE_OK;
+}
+
+}  // extern "C"
