@@ -18,12 +18,15 @@
  *   vectors (SURVEY.md §8c "parity unpinned" rows); this file is the
  *   specification, and tests/golden/ pins it with committed vectors.
  *
- * Checksum (order independent, so any GPU reduction tree is bit exact):
- *   words w_j = little-endian uint32 at byte 4j of the LANDED segment
- *   k_j   = (uint32)j * 0x9E3779B1 ^ (uint32)(j >> 32) * 0x85EBCA77
- *   h_j   = fmix32(w_j ^ k_j)               (murmur3 finaliser)
- *   g_j   = (h_j ^ (h_j >> 15)) * 0x2C1B3C6D
- *   sum   = Σ_j ((uint64)g_j << 32 | h_j)  mod 2^64
+ * Checksum (order independent, so any GPU reduction tree is bit exact),
+ * over the 64-bit little-endian words of the LANDED segment (its size is a
+ * multiple of 16):
+ *   lo_p, hi_p = low / high 32-bit halves of word p
+ *   k_p = (uint32)p * 0x9E3779B1 ^ (uint32)(p >> 32) * 0x85EBCA77
+ *   a_p = lo_p ^ k_p            b_p = hi_p ^ (k_p + 0x7F4A7C15)
+ *   sum = Σ_p  a_p * b_p + (b_p << 32 | a_p)      (64-bit products, mod 2^64)
+ *   One 32x32->64 multiply per 8 bytes keeps the land kernel HBM-bound; the
+ *   linear term keeps every single-word change visible even when a_p*b_p = 0.
  *
  * Land (unpack):  seg[dst_off[i] + b] = packed[src_off[i] + b] for b < len[i];
  *   every other segment byte is zero.
@@ -37,25 +40,20 @@
 #include <string.h>
 #include <pthread.h>
 
-static inline uint32_t fmix32(uint32_t h) {
-  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
-  return h;
+static inline uint64_t pair_term(uint32_t lo, uint32_t hi, uint64_t p) {
+  uint32_t k = (uint32_t)p * 0x9E3779B1u ^ (uint32_t)(p >> 32) * 0x85EBCA77u;
+  uint32_t a = lo ^ k, b = hi ^ (k + 0x7F4A7C15u);
+  return (uint64_t)a * (uint64_t)b + (((uint64_t)b << 32) | a);
 }
 
-static inline uint64_t word_term(uint32_t w, uint64_t j) {
-  uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
-  uint32_t h = fmix32(w ^ k);
-  uint32_t g = (h ^ (h >> 15)) * 0x2C1B3C6Du;
-  return ((uint64_t)g << 32) | h;
-}
-
-/* checksum of `bytes` (multiple of 4) starting at word index word_base */
+/* checksum of `bytes` (multiple of 8) starting at 64-bit word index word_base */
 uint64_t oracle_checksum(const uint8_t *p, uint64_t bytes, uint64_t word_base) {
-  uint64_t s = 0, n = bytes / 4;
-  for (uint64_t j = 0; j < n; ++j) {
-    uint32_t w;
-    memcpy(&w, p + 4 * j, 4);
-    s += word_term(w, word_base + j);
+  uint64_t s = 0, n = bytes / 8;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t lo, hi;
+    memcpy(&lo, p + 8 * i, 4);
+    memcpy(&hi, p + 8 * i + 4, 4);
+    s += pair_term(lo, hi, word_base + i);
   }
   return s;
 }

@@ -8,19 +8,10 @@
 //   SPMV     CSR y = A.x, the matrix RO (Parboil spmv)
 //   SPIN     hold one SM for args[0] µs (calibrated-delay functions)
 #include "common.h"
+#include "checksum.cuh"
 
 namespace sage {
 
-__device__ __forceinline__ uint32_t fmix32b(uint32_t h) {
-  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
-  return h;
-}
-__device__ __forceinline__ unsigned long long wterm(uint32_t w, unsigned long long j) {
-  uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
-  uint32_t h = fmix32b(w ^ k);
-  uint32_t g = (h ^ (h >> 15)) * 0x2C1B3C6Du;
-  return ((unsigned long long)g << 32) | h;
-}
 
 // ---- TOUCH: checksum of RO and input (both 16-B multiples) into out[0..1] --
 __global__ void __launch_bounds__(256) touch_kernel(const uint4 *__restrict__ ro, unsigned long long nro,
@@ -30,12 +21,10 @@ __global__ void __launch_bounds__(256) touch_kernel(const uint4 *__restrict__ ro
   unsigned long long a = 0, b = 0;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nro; i += stride) {
-    uint4 v = __ldg(ro + i);
-    a += wterm(v.x, 4 * i) + wterm(v.y, 4 * i + 1) + wterm(v.z, 4 * i + 2) + wterm(v.w, 4 * i + 3);
+    a += vec_sum(__ldg(ro + i), 2 * i);
   }
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nin; i += stride) {
-    uint4 v = __ldg(in + i);
-    b += wterm(v.x, 4 * i) + wterm(v.y, 4 * i + 1) + wterm(v.z, 4 * i + 2) + wterm(v.w, 4 * i + 3);
+    b += vec_sum(__ldg(in + i), 2 * i);
   }
   for (int o = 16; o; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);

@@ -15,6 +15,7 @@
 //   RETURN    synchronous D2H of the result
 // then the context is destroyed (timed separately as teardown).
 #include "common.h"
+#include "checksum.cuh"
 
 #include <chrono>
 
@@ -101,19 +102,8 @@ static int run_job(Job *J) {
     // verification only (outside every stage): checksum of what was loaded
     if (rc == SAGE_OK && ro_b) {
       std::vector<uint8_t> host(ro_b);
-      if (cudaMemcpy(host.data(), ro, ro_b, cudaMemcpyDeviceToHost) == cudaSuccess) {
-        uint64_t s = 0;
-        for (uint64_t j = 0; j < ro_b / 4; ++j) {
-          uint32_t w;
-          memcpy(&w, host.data() + 4 * j, 4);
-          uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
-          uint32_t h = w ^ k;
-          h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
-          uint32_t g = (h ^ (h >> 15)) * 0x2C1B3C6Du;
-          s += ((uint64_t)g << 32) | h;
-        }
-        J->info.checksum = s;
-      }
+      if (cudaMemcpy(host.data(), ro, ro_b, cudaMemcpyDeviceToHost) == cudaSuccess)
+        J->info.checksum = host_checksum(host.data(), ro_b);
     }
   }
   // teardown (after completion; reported separately)

@@ -21,6 +21,7 @@
 // last data byte).  Per chunk that is one contiguous run of vectors per
 // tensor (an Item); the planner emits Items + a prefix sum of their lengths.
 #include "common.h"
+#include "checksum.cuh"
 
 #include <algorithm>
 
@@ -59,6 +60,7 @@ struct Layout {
   Plan chunked, whole;
 };
 
+static constexpr uint64_t kWholeChunk = 256ull << 20;
 static std::mutex g_lay_mu;
 static std::unordered_map<uint64_t, Layout *> g_layouts;
 static std::atomic<uint64_t> g_lay_next{1};
@@ -180,7 +182,9 @@ static int layout_build(const uint64_t *src_off, const uint64_t *dst_off, const 
   }
   if (n == 0 && seg) return fail(SAGE_EINVAL, "layout: empty layout must have seg_bytes == 0");
   SAGE_TRY(build_plan(*L, chunk, &L->chunked));
-  SAGE_TRY(build_plan(*L, packed ? packed : 1, &L->whole));
+  // HBM-resident / peer sources need no staging: land in 256 MiB virtual
+  // chunks (keeps in-chunk offsets 32-bit) straight from the source
+  SAGE_TRY(build_plan(*L, kWholeChunk, &L->whole));
   return SAGE_OK;
 }
 
@@ -204,167 +208,8 @@ int layouts_destroy_all() {
   return SAGE_OK;
 }
 
-// ------------------------------------------------------------- kernels -----
-__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
-  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
-  return h;
-}
-__device__ __forceinline__ unsigned long long word_term(uint32_t w, unsigned long long j) {
-  uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
-  uint32_t h = fmix32(w ^ k);
-  uint32_t g = (h ^ (h >> 15)) * 0x2C1B3C6Du;
-  return ((unsigned long long)g << 32) | h;
-}
-__device__ __forceinline__ unsigned long long vec_term(uint4 v, unsigned long long j0) {
-  return word_term(v.x, j0) + word_term(v.y, j0 + 1) + word_term(v.z, j0 + 2) + word_term(v.w, j0 + 3);
-}
+#include "land_kernels.cuh"
 
-__device__ __forceinline__ uint32_t sel4(uint32_t ws, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  return ws == 0 ? a : ws == 1 ? b : ws == 2 ? c : d;
-}
-// bytes [sh, sh + 16) of the 32-byte concatenation a|b
-__device__ __forceinline__ uint4 funnel16(uint4 a, uint4 b, uint32_t sh) {
-  uint32_t ws = sh >> 2, bs = (sh & 3u) * 8u;
-  uint32_t r0 = sel4(ws, a.x, a.y, a.z, a.w);
-  uint32_t r1 = sel4(ws, a.y, a.z, a.w, b.x);
-  uint32_t r2 = sel4(ws, a.z, a.w, b.x, b.y);
-  uint32_t r3 = sel4(ws, a.w, b.x, b.y, b.z);
-  uint32_t r4 = sel4(ws, b.x, b.y, b.z, b.w);
-  uint4 o;
-  o.x = __funnelshift_r(r0, r1, bs);
-  o.y = __funnelshift_r(r1, r2, bs);
-  o.z = __funnelshift_r(r2, r3, bs);
-  o.w = __funnelshift_r(r3, r4, bs);
-  return o;
-}
-__device__ __forceinline__ uint32_t keep_bytes(uint32_t w, long long nb) {
-  return nb >= 4 ? w : nb <= 0 ? 0u : (w & ((1u << (8 * (uint32_t)nb)) - 1u));
-}
-
-__device__ __forceinline__ void block_reduce_add(unsigned long long v, unsigned long long *out) {
-  __shared__ unsigned long long red[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    int nw = (blockDim.x + 31) >> 5;
-    v = lane < nw ? red[lane] : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && v) atomicAdd(out, v);
-  }
-}
-
-struct LandArgs {
-  const LandItem *items;
-  const uint32_t *prefix;  // n_items + 1 entries, chunk local
-  uint32_t n_items;
-  uint32_t total_vec;
-  const uint8_t *slot;     // 16-B aligned base holding packed [sb, se)
-  unsigned long long slot_bytes;  // se - sb (valid bytes)
-  uint8_t *dst;            // segment base (16-B aligned)
-  unsigned long long *acc; // checksum accumulator
-};
-
-constexpr int kLandThreads = 256;
-constexpr int kLandU = 4;  // vectors per lane per tile
-
-__global__ void __launch_bounds__(kLandThreads) land_kernel(const __grid_constant__ LandArgs a) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t tile = 32u * kLandU;
-  const uint8_t *slot_end = a.slot + a.slot_bytes;
-  unsigned long long acc = 0;
-  for (uint64_t t0 = (uint64_t)warp * tile; t0 < a.total_vec; t0 += (uint64_t)nwarps * tile) {
-    // warp-uniform binary search: last item with prefix <= t0
-    uint32_t lo = 0, hi = a.n_items;
-    while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(a.prefix + mid) <= t0) lo = mid; else hi = mid;
-    }
-    uint32_t it = lo;
-    uint32_t cur = __ldg(a.prefix + it), nxt = __ldg(a.prefix + it + 1);
-    LandItem I = a.items[it];
-    long long s[kLandU], d[kLandU];
-    unsigned long long dv[kLandU];
-    bool ok[kLandU];
-#pragma unroll
-    for (int u = 0; u < kLandU; ++u) {
-      uint32_t v = (uint32_t)t0 + u * 32u + lane;
-      ok[u] = v < a.total_vec;
-      if (ok[u]) {
-        while (v >= nxt) {  // crosses into the next run (rare: run boundaries)
-          ++it;
-          cur = nxt;
-          nxt = __ldg(a.prefix + it + 1);
-          I = a.items[it];
-        }
-        uint32_t loc = v - cur;
-        s[u] = I.src_rel0 + 16ll * loc;
-        d[u] = I.data0 - 16ll * loc;
-        dv[u] = I.dst_vec0 + loc;
-      } else {
-        s[u] = 0; d[u] = 0; dv[u] = 0;
-      }
-    }
-    uint4 A[kLandU], B[kLandU];
-#pragma unroll
-    for (int u = 0; u < kLandU; ++u) {
-      A[u] = make_uint4(0, 0, 0, 0);
-      B[u] = make_uint4(0, 0, 0, 0);
-      if (ok[u] && d[u] > 0) {
-        const uint8_t *p = a.slot + s[u];
-        const uint4 *q = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
-        A[u] = __ldg(q);
-        if ((reinterpret_cast<uintptr_t>(p) & 15) && reinterpret_cast<const uint8_t *>(q + 1) < slot_end)
-          B[u] = __ldg(q + 1);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kLandU; ++u) {
-      if (!ok[u]) continue;
-      uint4 o = make_uint4(0, 0, 0, 0);
-      if (d[u] > 0) {
-        uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(a.slot + s[u]) & 15);
-        o = sh ? funnel16(A[u], B[u], sh) : A[u];
-        if (d[u] < 16) {
-          o.x = keep_bytes(o.x, d[u]);
-          o.y = keep_bytes(o.y, d[u] - 4);
-          o.z = keep_bytes(o.z, d[u] - 8);
-          o.w = keep_bytes(o.w, d[u] - 12);
-        }
-      }
-      reinterpret_cast<uint4 *>(a.dst)[dv[u]] = o;
-      acc += vec_term(o, dv[u] * 4ull);
-    }
-  }
-  block_reduce_add(acc, a.acc);
-}
-
-// checksum of a landed segment (verify / dedup): read-only pass
-__global__ void __launch_bounds__(256) checksum_kernel(const uint4 *__restrict__ p, unsigned long long nvec,
-                                                       unsigned long long *out) {
-  unsigned long long acc = 0;
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < nvec; i += 4 * stride) {
-    uint4 v0 = __ldg(p + i), v1 = __ldg(p + i + stride), v2 = __ldg(p + i + 2 * stride), v3 = __ldg(p + i + 3 * stride);
-    acc += vec_term(v0, i * 4) + vec_term(v1, (i + stride) * 4) + vec_term(v2, (i + 2 * stride) * 4) +
-           vec_term(v3, (i + 3 * stride) * 4);
-  }
-  for (; i < nvec; i += stride) acc += vec_term(__ldg(p + i), i * 4);
-  block_reduce_add(acc, out);
-}
-
-static int land_grid(Gpu *G, uint32_t total_vec) {
-  uint64_t tiles = (total_vec + 32ull * kLandU - 1) / (32ull * kLandU);
-  uint64_t blocks = (tiles + (kLandThreads / 32) - 1) / (kLandThreads / 32);
-  uint64_t cap = (uint64_t)G->sm_count * 8;
-  return (int)std::max<uint64_t>(1, std::min(blocks, cap));
-}
 
 // --------------------------------------------------------------- loads -----
 struct Load {
@@ -589,8 +434,10 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
     const Plan &P = lay->whole;
     L->chunks = (uint32_t)P.chunks.size();
     if (d->flags & SAGE_LOAD_SRC_PEER) L->link_bytes = d->src_bytes;
-    rc = enqueue_land(G, P, P.chunks[0], d->gpu, static_cast<const uint8_t *>(d->src), dst, acc);
-    if (rc != SAGE_OK) return rc;
+    for (const ChunkPlan &C : P.chunks) {
+      rc = enqueue_land(G, P, C, d->gpu, static_cast<const uint8_t *>(d->src) + C.sb, dst, acc);
+      if (rc != SAGE_OK) return rc;
+    }
   } else {
     const Plan &P = lay->chunked;
     const bool pinned = (d->flags & SAGE_LOAD_SRC_PINNED) != 0;
@@ -741,16 +588,7 @@ int sage_debug_emulate_land(sage_handle h, const void *packed, uint64_t packed_b
         if (dv >= written.size() || written[dv]) return fail(SAGE_ESTATE, "emulate: vector landed twice");
         written[dv] = 1;
         memcpy(out + dv * 16, v, 16);
-        for (int w = 0; w < 4; ++w) {
-          uint32_t x;
-          memcpy(&x, v + 4 * w, 4);
-          uint64_t j = dv * 4 + w;
-          uint32_t k = (uint32_t)j * 0x9E3779B1u ^ (uint32_t)(j >> 32) * 0x85EBCA77u;
-          uint32_t hh = x ^ k;
-          hh ^= hh >> 16; hh *= 0x85EBCA6Bu; hh ^= hh >> 13; hh *= 0xC2B2AE35u; hh ^= hh >> 16;
-          uint32_t g = (hh ^ (hh >> 15)) * 0x2C1B3C6Du;
-          sum += ((uint64_t)g << 32) | hh;
-        }
+        sum += host_checksum(v, 16, dv * 2);
       }
     }
   }

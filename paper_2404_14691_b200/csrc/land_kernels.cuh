@@ -1,0 +1,205 @@
+// land_kernels.cuh — the sm_100a `land` kernel and the checksum kernel.
+// Included by land.cu inside namespace sage (uses LandItem).
+//
+// Roofline: land moves 2 bytes of HBM traffic per landed byte (read the
+// staged packed bytes, write the segment); the checksum adds no traffic.
+// Per 16-byte destination vector the fast path spends ~20 SASS instructions
+// (1-2 LDG.128, 4 SHF funnel shifts when the tensor is not 16-B aligned in
+// the packed stream, 1 STG.128, two 32x32->64 IMAD.WIDE + 4 IADD3 for the
+// checksum), which keeps it under the HBM bound at the 1.3 GHz loaded clock.
+#pragma once
+// (checksum.cuh is included by land.cu at file scope)
+
+template <class T>
+__device__ __forceinline__ T dmin(T a, T b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------ byte funnel ---
+template <int WS>
+__device__ __forceinline__ uint4 funnel_ws(const uint4 &a, const uint4 &b, uint32_t bs) {
+  uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  uint4 o;
+  o.x = __funnelshift_r(w[WS + 0], w[WS + 1], bs);
+  o.y = __funnelshift_r(w[WS + 1], w[WS + 2], bs);
+  o.z = __funnelshift_r(w[WS + 2], w[WS + 3], bs);
+  o.w = __funnelshift_r(w[WS + 3], w[WS + 4], bs);
+  return o;
+}
+__device__ __forceinline__ uint32_t sel4(uint32_t ws, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return ws == 0 ? a : ws == 1 ? b : ws == 2 ? c : d;
+}
+// bytes [sh, sh + 16) of a|b with a per-lane shift (slow path)
+__device__ __forceinline__ uint4 funnel16(const uint4 &a, const uint4 &b, uint32_t sh) {
+  uint32_t ws = sh >> 2, bs = (sh & 3u) * 8u;
+  uint32_t r0 = sel4(ws, a.x, a.y, a.z, a.w);
+  uint32_t r1 = sel4(ws, a.y, a.z, a.w, b.x);
+  uint32_t r2 = sel4(ws, a.z, a.w, b.x, b.y);
+  uint32_t r3 = sel4(ws, a.w, b.x, b.y, b.z);
+  uint32_t r4 = sel4(ws, b.x, b.y, b.z, b.w);
+  uint4 o;
+  o.x = __funnelshift_r(r0, r1, bs);
+  o.y = __funnelshift_r(r1, r2, bs);
+  o.z = __funnelshift_r(r2, r3, bs);
+  o.w = __funnelshift_r(r3, r4, bs);
+  return o;
+}
+__device__ __forceinline__ uint32_t keep_bytes(uint32_t w, long long nb) {
+  return nb >= 4 ? w : nb <= 0 ? 0u : (w & ((1u << (8 * (uint32_t)nb)) - 1u));
+}
+__device__ __forceinline__ uint4 mask_tail(uint4 o, long long d) {
+  o.x = keep_bytes(o.x, d);
+  o.y = keep_bytes(o.y, d - 4);
+  o.z = keep_bytes(o.z, d - 8);
+  o.w = keep_bytes(o.w, d - 12);
+  return o;
+}
+
+struct LandArgs {
+  const LandItem *items;
+  const uint32_t *prefix;  // n_items + 1 entries, chunk local
+  uint32_t n_items;
+  uint32_t total_vec;
+  const uint8_t *slot;     // 16-B aligned base holding packed [sb, se)
+  unsigned long long slot_bytes;
+  uint8_t *dst;            // segment base (16-B aligned)
+  unsigned long long *acc; // checksum accumulator
+};
+
+constexpr int kLandThreads = 256;
+constexpr int kLandU = 4;  // vectors per lane per tile
+
+// fast path body: every vector of the tile lies in one item (warp uniform)
+template <int WS>
+__device__ __forceinline__ unsigned long long land_tile_uniform(const uint4 *__restrict__ qbase, uint32_t nB,
+                                                                uint4 *__restrict__ dbase, unsigned long long pbase,
+                                                                uint32_t loc0, uint32_t lane, uint32_t nvalid,
+                                                                uint32_t nfull, uint32_t ndata, uint32_t bs,
+                                                                long long data0) {
+  unsigned long long acc = 0;
+  uint4 A[kLandU], B[kLandU];
+#pragma unroll
+  for (int u = 0; u < kLandU; ++u) {
+    uint32_t loc = loc0 + u * 32u + lane;
+    A[u] = make_uint4(0, 0, 0, 0);
+    B[u] = make_uint4(0, 0, 0, 0);
+    if (u * 32u + lane < nvalid && loc < ndata) {
+      A[u] = __ldg(qbase + loc);
+      if (WS >= 0 && loc + 1 < nB) B[u] = __ldg(qbase + loc + 1);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kLandU; ++u) {
+    uint32_t loc = loc0 + u * 32u + lane;
+    if (u * 32u + lane >= nvalid) continue;
+    uint4 o;
+    if (WS < 0) o = A[u];
+    else o = funnel_ws<WS < 0 ? 0 : WS>(A[u], B[u], bs);
+    if (loc >= nfull) o = (loc < ndata) ? mask_tail(o, data0 - 16ll * loc) : make_uint4(0, 0, 0, 0);
+    dbase[loc] = o;
+    acc += vec_sum(o, pbase + 2ull * loc);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kLandThreads, 4) land_kernel(const __grid_constant__ LandArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t tile = 32u * kLandU;
+  const uint8_t *slot_end = a.slot + a.slot_bytes;
+  unsigned long long acc = 0;
+  for (uint64_t t0 = (uint64_t)warp * tile; t0 < a.total_vec; t0 += (uint64_t)nwarps * tile) {
+    // warp-uniform binary search: last item with prefix <= t0
+    uint32_t lo = 0, hi = a.n_items;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(a.prefix + mid) <= t0) lo = mid; else hi = mid;
+    }
+    uint32_t it = lo;
+    uint32_t cur = __ldg(a.prefix + it), nxt = __ldg(a.prefix + it + 1);
+    const uint32_t tend = (uint32_t)dmin<uint64_t>(t0 + tile, a.total_vec);
+    if (tend <= nxt) {
+      // ---- fast path: the whole tile is one run of one tensor -------------
+      const LandItem I = a.items[it];
+      const uint32_t loc0 = (uint32_t)t0 - cur;
+      const uint32_t nvalid = tend - (uint32_t)t0;
+      const long long d0 = I.data0;
+      const uint32_t nfull = d0 <= 0 ? 0u : (uint32_t)dmin<long long>(d0 >> 4, 0xFFFFFFFFll);
+      const uint32_t ndata = d0 <= 0 ? 0u : (uint32_t)dmin<long long>((d0 + 15) >> 4, 0xFFFFFFFFll);
+      const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(a.slot + I.src_rel0) & 15);
+      const uint4 *qbase = reinterpret_cast<const uint4 *>(a.slot + I.src_rel0 - sh);
+      const long long span = slot_end - reinterpret_cast<const uint8_t *>(qbase);
+      const uint32_t nB = (uint32_t)dmin<long long>((span + 15) >> 4, 0xFFFFFFFFll);
+      uint4 *dbase = reinterpret_cast<uint4 *>(a.dst) + I.dst_vec0;
+      const unsigned long long pbase = I.dst_vec0 * 2ull;
+      const uint32_t bs = (sh & 3u) * 8u;
+      switch (sh == 0 ? -1 : (int)(sh >> 2)) {
+        case -1: acc += land_tile_uniform<-1>(qbase, nB, dbase, pbase, loc0, lane, nvalid, nfull, ndata, 0, d0); break;
+        case 0: acc += land_tile_uniform<0>(qbase, nB, dbase, pbase, loc0, lane, nvalid, nfull, ndata, bs, d0); break;
+        case 1: acc += land_tile_uniform<1>(qbase, nB, dbase, pbase, loc0, lane, nvalid, nfull, ndata, bs, d0); break;
+        case 2: acc += land_tile_uniform<2>(qbase, nB, dbase, pbase, loc0, lane, nvalid, nfull, ndata, bs, d0); break;
+        default: acc += land_tile_uniform<3>(qbase, nB, dbase, pbase, loc0, lane, nvalid, nfull, ndata, bs, d0); break;
+      }
+      continue;
+    }
+    // ---- slow path: the tile straddles run boundaries (per-lane items) ------
+    LandItem I = a.items[it];
+#pragma unroll 1
+    for (int u = 0; u < kLandU; ++u) {
+      uint32_t v = (uint32_t)t0 + u * 32u + lane;
+      if (v >= a.total_vec) break;
+      while (v >= nxt) {
+        ++it;
+        cur = nxt;
+        nxt = __ldg(a.prefix + it + 1);
+        I = a.items[it];
+      }
+      const uint32_t loc = v - cur;
+      const long long s = I.src_rel0 + 16ll * loc;
+      const long long d = I.data0 - 16ll * loc;
+      const unsigned long long dv = I.dst_vec0 + loc;
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (d > 0) {
+        const uint8_t *p = a.slot + s;
+        const uint4 *q = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
+        const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 15);
+        uint4 A = __ldg(q), B = make_uint4(0, 0, 0, 0);
+        if (sh && reinterpret_cast<const uint8_t *>(q + 1) < slot_end) B = __ldg(q + 1);
+        o = sh ? funnel16(A, B, sh) : A;
+        if (d < 16) o = mask_tail(o, d);
+      }
+      reinterpret_cast<uint4 *>(a.dst)[dv] = o;
+      acc += vec_sum(o, dv * 2ull);
+    }
+  }
+  block_reduce_add(acc, a.acc);
+}
+
+// checksum of a landed segment (verify / dedup): one read-only pass
+__global__ void __launch_bounds__(256) checksum_kernel(const uint4 *__restrict__ p, unsigned long long nvec,
+                                                       unsigned long long *out) {
+  unsigned long long acc = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 v0 = __ldg(p + i), v1 = __ldg(p + i + stride), v2 = __ldg(p + i + 2 * stride), v3 = __ldg(p + i + 3 * stride);
+    acc += vec_sum(v0, 2 * i) + vec_sum(v1, 2 * (i + stride)) + vec_sum(v2, 2 * (i + 2 * stride)) +
+           vec_sum(v3, 2 * (i + 3 * stride));
+  }
+  for (; i < nvec; i += stride) acc += vec_sum(__ldg(p + i), 2 * i);
+  block_reduce_add(acc, out);
+}
+
+static int g_land_occ = 0;  // resident land blocks per SM (occupancy API)
+
+static int land_grid(Gpu *G, uint32_t total_vec) {
+  if (!g_land_occ) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, land_kernel, kLandThreads, 0) != cudaSuccess || occ < 1)
+      occ = 4;
+    g_land_occ = occ;
+  }
+  uint64_t tiles = (total_vec + 32ull * kLandU - 1) / (32ull * kLandU);
+  uint64_t blocks = (tiles + (kLandThreads / 32) - 1) / (kLandThreads / 32);
+  uint64_t cap = (uint64_t)G->sm_count * g_land_occ;
+  return (int)std::max<uint64_t>(1, std::min(blocks, cap));
+}

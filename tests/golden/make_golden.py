@@ -24,15 +24,12 @@ M64 = (1 << 64) - 1
 
 def py_checksum(seg: bytes) -> int:
     s = 0
-    for j in range(len(seg) // 4):
-        (w,) = struct.unpack_from("<I", seg, 4 * j)
-        k = ((j & 0xFFFFFFFF) * 0x9E3779B1 ^ (j >> 32) * 0x85EBCA77) & 0xFFFFFFFF
-        h = w ^ k
-        h ^= h >> 16; h = (h * 0x85EBCA6B) & 0xFFFFFFFF
-        h ^= h >> 13; h = (h * 0xC2B2AE35) & 0xFFFFFFFF
-        h ^= h >> 16
-        g = ((h ^ (h >> 15)) * 0x2C1B3C6D) & 0xFFFFFFFF
-        s = (s + ((g << 32) | h)) & M64
+    for p in range(len(seg) // 8):
+        lo, hi = struct.unpack_from("<II", seg, 8 * p)
+        k = ((p & 0xFFFFFFFF) * 0x9E3779B1 ^ (p >> 32) * 0x85EBCA77) & 0xFFFFFFFF
+        a = lo ^ k
+        b = hi ^ ((k + 0x7F4A7C15) & 0xFFFFFFFF)
+        s = (s + a * b + ((b << 32) | a)) & M64
     return s
 
 
