@@ -77,6 +77,9 @@ int sage_pool_configure(int gpu, uint64_t capacity_bytes, uint64_t granularity_b
 int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *dptr,
                     uint64_t *shortfall);
 int sage_pool_free(sage_handle h);
+/* ledger release now (the reference frees at once, sharing.py:217-229), the
+ * physical pages once `ev` completes (a D2H / kernel may still read them)   */
+int sage_pool_free_after(sage_handle h, sage_handle ev);
 int sage_pool_effective(int gpu, uint64_t bytes, uint64_t *effective);
 int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total,
                     uint64_t *physical_total, uint64_t *capacity);
@@ -162,6 +165,11 @@ typedef struct {
 } sage_load_info;
 int sage_segment_load(const sage_load_desc *d, sage_handle *load, sage_handle *end_ev);
 int sage_load_info_get(sage_handle load, sage_load_info *out);   /* ENOTREADY until done */
+/* CPU_LOAD alone (serial plans): memcpy the DB record into a pinned host
+ * buffer on the GPU's host stream after `wait`; begin/end are host-completed
+ * device-ordered events                                                      */
+int sage_host_load(int gpu, void *pinned_dst, const void *src, uint64_t bytes, const sage_handle *wait,
+                   int n_wait, sage_handle *begin_ev, sage_handle *end_ev);
 int sage_load_release(sage_handle load);
 /* recompute the checksum of a landed segment on the device (verify / dedup) */
 int sage_segment_checksum(int gpu, uint64_t dptr, uint64_t bytes, uint64_t *checksum);

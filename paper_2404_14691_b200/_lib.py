@@ -78,6 +78,7 @@ _SIGS = {
     "sage_pool_configure": (C.c_int, [C.c_int, u64, u64]),
     "sage_pool_alloc": (C.c_int, [C.c_int, u64, C.c_int, C.POINTER(H), C.POINTER(u64), C.POINTER(u64)]),
     "sage_pool_free": (C.c_int, [H]),
+    "sage_pool_free_after": (C.c_int, [H, H]),
     "sage_pool_effective": (C.c_int, [C.c_int, u64, C.POINTER(u64)]),
     "sage_pool_usage": (C.c_int, [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "sage_pool_dptr": (C.c_int, [H, C.POINTER(u64), C.POINTER(u64)]),
@@ -100,6 +101,8 @@ _SIGS = {
     "sage_segment_load": (C.c_int, [C.POINTER(LoadDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_load_info_get": (C.c_int, [H, C.POINTER(LoadInfo)]),
     "sage_load_release": (C.c_int, [H]),
+    "sage_host_load": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, u64, C.POINTER(H), C.c_int, C.POINTER(H),
+                                 C.POINTER(H)]),
     "sage_segment_checksum": (C.c_int, [C.c_int, u64, u64, C.POINTER(u64)]),
     "sage_d2h_cache": (C.c_int, [C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
     "sage_fanout": (C.c_int, [C.c_int, u64, C.c_int, u64, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),

@@ -535,6 +535,31 @@ int sage_load_release(sage_handle h) {
   return SAGE_OK;
 }
 
+namespace {
+struct PlainCopy { void *dst; const void *src; size_t n; };
+void CUDART_CB plain_copy_fn(void *p) {
+  auto *a = static_cast<PlainCopy *>(p);
+  parallel_memcpy(a->dst, a->src, a->n);
+  delete a;
+}
+}  // namespace
+
+int sage_host_load(int gpu, void *dst, const void *src, uint64_t bytes, const sage_handle *wait, int n_wait,
+                   sage_handle *begin_ev, sage_handle *end_ev) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || !begin_ev || !end_ev || (bytes && (!dst || !src))) return fail(SAGE_EINVAL, "host_load: bad argument");
+  cudaSetDevice(gpu);
+  std::lock_guard<std::mutex> lk(G->load_mu);
+  SAGE_TRY(wait_list(G->host, wait, n_wait));
+  Event *b, *e;
+  SAGE_TRY(event_new(gpu, begin_ev, &b));
+  SAGE_TRY(event_record(b, G->host));
+  if (bytes) SAGE_CUDA(cudaLaunchHostFunc(G->host, plain_copy_fn, new PlainCopy{dst, src, (size_t)bytes}));
+  SAGE_TRY(event_new(gpu, end_ev, &e));
+  return event_record(e, G->host);
+}
+
 int sage_segment_checksum(int gpu, uint64_t dptr, uint64_t bytes, uint64_t *checksum) {
   SAGE_TRY(require_up());
   Gpu *G = gpu_get(gpu);

@@ -29,7 +29,27 @@ struct Pool {
   uint64_t cached = 0;     // bytes held by the free-handle cache
   uint64_t vmm_gran = 2ull << 20;
   std::multimap<uint64_t, CUmemGenericAllocationHandle> free_phys;
+  std::vector<std::pair<Alloc *, cudaEvent_t>> zombies;  // ledger-freed, pages pending an event
 };
+
+static void unmap_segment(Pool *P, Alloc *A);
+
+// unmap zombies whose last reader finished (called with P->mu held)
+static void reap(Pool *P, bool all) {
+  auto &Z = P->zombies;
+  for (size_t i = 0; i < Z.size();) {
+    cudaError_t q = all ? cudaEventSynchronize(Z[i].second) : cudaEventQuery(Z[i].second);
+    if (q == cudaSuccess || (q != cudaErrorNotReady)) {
+      unmap_segment(P, Z[i].first);
+      cudaEventDestroy(Z[i].second);
+      delete Z[i].first;
+      Z[i] = Z.back();
+      Z.pop_back();
+    } else {
+      ++i;
+    }
+  }
+}
 
 static std::mutex g_alloc_mu;
 static std::unordered_map<uint64_t, Alloc *> g_allocs;
@@ -67,6 +87,10 @@ void pool_destroy(Gpu *G) {
       if (kv.second->gpu == G->id) mine.push_back(kv.first);
   }
   for (uint64_t id : mine) sage_pool_free(make_handle(Kind::Alloc, id));
+  {
+    std::lock_guard<std::mutex> lk(P->mu);
+    reap(P, true);
+  }
   release_cache(P);
   delete P;
   G->pool = nullptr;
@@ -89,7 +113,8 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = G->id;
     CUresult r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
-    if (r == CUDA_ERROR_OUT_OF_MEMORY && P->cached) {
+    if (r == CUDA_ERROR_OUT_OF_MEMORY && (P->cached || !P->zombies.empty())) {
+      reap(P, true);
       release_cache(P);
       r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
     }
@@ -262,6 +287,7 @@ int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *
     }
     if (!acct) {
       cudaSetDevice(gpu);
+      if (!P->zombies.empty()) reap(P, false);
       int rc = map_segment(G, P, A);
       if (rc != SAGE_OK) { delete A; return rc; }
     }
@@ -302,8 +328,38 @@ int sage_pool_free(sage_handle h) {
     }
     P->usage -= A->eff;
     P->by_class[A->cls] -= A->eff;
+    reap(P, false);
   }
   delete A;
+  return SAGE_OK;
+}
+
+int sage_pool_free_after(sage_handle h, sage_handle evh) {
+  if (handle_kind(h) != Kind::Alloc) return fail(SAGE_EINVAL, "not a pool handle");
+  Event *E = event_get(evh);
+  if (!E || !E->ev || !E->recorded) return fail(SAGE_ESTATE, "free_after: unknown or unrecorded event");
+  Alloc *A = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_allocs.find(h & ((1ull << 56) - 1));
+    if (it == g_allocs.end()) return fail(SAGE_ESTATE, "double or unknown free");
+    A = it->second;
+    g_allocs.erase(it);
+  }
+  Gpu *G = gpu_get(A->gpu);
+  Pool *P = G->pool;
+  std::lock_guard<std::mutex> lk(P->mu);
+  P->usage -= A->eff;
+  P->by_class[A->cls] -= A->eff;
+  if (A->account_only) { delete A; return SAGE_OK; }
+  cudaSetDevice(A->gpu);
+  cudaEvent_t ev;
+  SAGE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  // chain: our private event completes when the caller's event does
+  SAGE_CUDA(cudaStreamWaitEvent(G->aux, E->ev, 0));
+  SAGE_CUDA(cudaEventRecord(ev, G->aux));
+  P->zombies.emplace_back(A, ev);
+  reap(P, false);
   return SAGE_OK;
 }
 
