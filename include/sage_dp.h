@@ -73,6 +73,8 @@ int         sage_set_host_threads(int n);
 #define SAGE_CLASS_INSTANCE_FIXED  3
 #define SAGE_ALLOC_ACCOUNT_ONLY    0x100  /* OR into cls: charge the ledger, map nothing
                                              (FixedGSL instances allocate in their own context) */
+#define SAGE_ALLOC_UNACCOUNTED     0x200  /* OR into cls: map without charging the ledger
+                                             (runtime scratch: staging for oversized inputs) */
 int sage_pool_configure(int gpu, uint64_t capacity_bytes, uint64_t granularity_bytes);
 int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *dptr,
                     uint64_t *shortfall);

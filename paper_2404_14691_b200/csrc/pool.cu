@@ -271,6 +271,7 @@ int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *
   bool acct = (cls & SAGE_ALLOC_ACCOUNT_ONLY) != 0;
   int c = cls & 0xff;
   if (c < 0 || c > 3) return fail(SAGE_EINVAL, "pool_alloc: bad class");
+  if (acct && (cls & SAGE_ALLOC_UNACCOUNTED)) return fail(SAGE_EINVAL, "pool_alloc: account-only and unaccounted");
   Pool *P = G->pool;
   auto *A = new Alloc();
   A->gpu = gpu;
@@ -279,7 +280,8 @@ int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *
   A->account_only = acct;
   {
     std::lock_guard<std::mutex> lk(P->mu);
-    A->eff = round_up(bytes, P->granularity);
+    // unaccounted runtime scratch charges nothing (eff = 0) and skips the budget
+    A->eff = (cls & SAGE_ALLOC_UNACCOUNTED) ? 0 : round_up(bytes, P->granularity);
     if (A->eff > P->capacity - P->usage) {
       if (shortfall) *shortfall = A->eff - (P->capacity - P->usage);
       delete A;

@@ -1,0 +1,552 @@
+"""The real plane: compile a stage plan into device operations.
+
+Reference: PlanExecution (pkg/src/gslsim/functions.py:341-433) walks the
+stage DAG on the event loop, charging loads to fluid channels and fixed
+stages to timers.  Here `DataPlane.start` walks the same DAG ONCE, at
+admission, and enqueues every node as asynchronous device work whose
+dependencies are its predecessors' END events:
+
+  CONTAINER, CPU_CTX  host-side instance state, done synchronously
+  CPU_LOAD            DB record -> pinned staging (memcpy fan-out, host stream);
+                      in Parallel plans it is pipelined chunk by chunk into
+                      GPU_LOAD by one native load (sage_segment_load)
+  GPU_CTX             bind the function context segment on a pooled stream
+                      (the pre-created context: no cuCtxCreate on this path)
+  GPU_LOAD            chunked H2D on the copy engine + `land` (unpack +
+                      checksum) of the read-only segment (from the DB, the
+                      pinned Stage-2 cache, or a peer GPU over NVLink) and of
+                      the invocation input
+  SYNC_WAIT           device-side wait on the leader's END events (Token)
+  COMPUTE             the body kernel on the invocation's stream
+  RETURN              D2H of the result into pinned memory
+
+The host is touched again only when the RETURN END event completes (polled
+by the engine), when stage times are read back and the policy releases.
+FixedGSL instances (fresh_context) run as native serial jobs instead.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from . import device as D
+from .functions import FunctionSpec, PlanMode, Stage, StagePlan, WarmthClass
+from .layout import SegmentLayout
+from .resources import AllocClass, SimulationError
+
+_BODY = {"touch": _lib.BODY_TOUCH, "sgemm": _lib.BODY_SGEMM, "stencil": _lib.BODY_STENCIL,
+         "spmv": _lib.BODY_SPMV, "spin": _lib.BODY_SPIN}
+
+
+def _a256(n: int) -> int:
+    return (n + 255) // 256 * 256
+
+
+def synthetic_bytes(seed: int, nbytes: int) -> np.ndarray:
+    """Deterministic synthetic DB bytes (PCG64 raw draws, little endian)."""
+    words = np.random.PCG64(seed).random_raw((nbytes + 7) // 8).astype(np.uint64)
+    return words.view(np.uint8)[:nbytes].copy()
+
+
+def _name_seed(name: str) -> int:
+    h = 1469598103934665603
+    for ch in name.encode():
+        h = ((h ^ ch) * 1099511628211) & 0xFFFFFFFFFFFF
+    return h
+
+
+@dataclass
+class FunctionData:
+    """What a registered function loads and runs on the real plane.
+
+    layout / db      the read-only segment: packed DB record + landing layout
+                     (layout.seg_bytes must fit the spec's ro allocation)
+    body / args      COMPUTE kernel (csrc/bodies.cu) and its shape arguments
+    input            default per-invocation payload (pageable host bytes)
+    out_bytes        bytes RETURN copies back
+    """
+    layout: SegmentLayout
+    db: np.ndarray
+    body: str = "touch"
+    args: tuple = ()
+    input: Optional[np.ndarray] = None
+    out_bytes: int = 16
+    ro_checksum: Optional[int] = None     # learnt from the first landed copy
+
+    @property
+    def input_bytes(self) -> int:
+        return 0 if self.input is None else int(self.input.nbytes)
+
+
+def synthetic_data(spec: FunctionSpec, tensors: int = 16) -> FunctionData:
+    """Default data of a spec without registered data: a ragged multi-tensor
+    RO record exactly filling spec.ro_bytes when landed, a synthetic input of
+    spec.input_bytes, and the TOUCH body (reads RO + input, returns digests)."""
+    seed = _name_seed(spec.name)
+    ro = spec.ro_bytes // 16 * 16
+    if ro >= 16 * 256 * tensors:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        w = rng.uniform(0.5, 1.5, tensors)
+        sizes = [int(x) // 256 * 256 for x in w / w.sum() * ro]
+        sizes[-1] += ro - sum(sizes)
+        # carve ragged (non-16-aligned) tensor lengths inside 256-B extents
+        lens = [max(1, s - int(rng.integers(0, 200))) for s in sizes]
+        src, dst, d, s0 = [], [], 0, 0
+        for s, n in zip(sizes, lens):
+            src.append(s0)
+            dst.append(d)
+            s0 += n
+            d += s
+        layout = SegmentLayout(tuple(src), tuple(dst), tuple(lens), s0, ro)
+    elif ro > 0:
+        layout = SegmentLayout.identity(ro)
+    else:
+        layout = SegmentLayout((), (), (), 0, 0)
+    db = synthetic_bytes(seed, layout.packed_bytes)
+    inp = synthetic_bytes(seed + 1, spec.input_bytes) if spec.input_bytes else None
+    if spec.body == "spin":
+        return FunctionData(layout, db, "spin", (int(round(spec.compute_ms * 1000)),), inp, 16)
+    return FunctionData(layout, db, "touch", (), inp, 16)
+
+
+class _PinnedPool:
+    """Reuse pinned host buffers by size (cudaHostAlloc costs ms per 100 MiB)."""
+
+    def __init__(self):
+        self.free: dict[int, list] = {}
+
+    def get(self, nbytes: int) -> D.PinnedBuffer:
+        lst = self.free.get(nbytes)
+        if lst:
+            return lst.pop()
+        return D.PinnedBuffer(nbytes)
+
+    def put(self, buf: D.PinnedBuffer) -> None:
+        self.free.setdefault(buf.nbytes, []).append(buf)
+
+    def close(self) -> None:
+        for lst in self.free.values():
+            for b in lst:
+                b.free()
+        self.free.clear()
+
+
+@dataclass
+class _Run:
+    inv: object
+    plan: StagePlan
+    gpu: int
+    slot: Optional[D.Slot] = None
+    events: list = field(default_factory=list)      # every Event to release
+    loads: list = field(default_factory=list)       # (node idx, kind, LoadOp)
+    marks: dict = field(default_factory=dict)       # stage -> (begin src, end src)
+    hooks: dict = field(default_factory=dict)
+    pinned: list = field(default_factory=list)      # pinned buffers to return
+    scratch: list = field(default_factory=list)     # unaccounted device segments
+    result: Optional[D.PinnedBuffer] = None
+    out_bytes: int = 0
+    job: Optional[D.FixedGSLJob] = None
+    end: Optional[D.Event] = None
+    fd: Optional[FunctionData] = None
+    ro_source: str = ""
+    t_enqueue: int = 0
+
+
+class DataPlane:
+    """Device side of one Simulation (runtime.py)."""
+
+    def __init__(self, sim):
+        self.sim = sim
+        self.pinned = _PinnedPool()
+        self.data: dict[str, FunctionData] = {}
+
+    # ---------------------------------------------------------------- data ----
+    def register(self, name: str, data: FunctionData) -> None:
+        spec = self.sim.spec_table[name]
+        if data.layout.seg_bytes > max(spec.ro_bytes, 0) and data.layout.seg_bytes:
+            raise ValueError(f"function {name}: landed segment ({data.layout.seg_bytes} B) exceeds "
+                             f"ro_mem_mb ({spec.ro_bytes} B)")
+        if data.layout.packed_bytes != data.db.nbytes:
+            raise ValueError(f"function {name}: DB record size differs from its layout")
+        self.data[name] = data
+
+    def data_for(self, spec: FunctionSpec) -> FunctionData:
+        fd = self.data.get(spec.name)
+        if fd is None:
+            fd = synthetic_data(spec)
+            self.data[spec.name] = fd
+        return fd
+
+    # -------------------------------------------------------- stage-2 cache ----
+    def cache_segment(self, r) -> Optional[D.Event]:
+        """Stage1 -> Stage2: D2H the landed segment into a pinned host cache."""
+        fd = self.data_for(r.spec)
+        n = fd.layout.seg_bytes
+        if n == 0 or r.gpu_ro is None:
+            return None
+        buf = self.pinned.get(n)
+        ev = D.d2h(r.gpu, r.gpu_ro.dptr, buf, n)
+        r.cpu_ro_cache.segment = buf
+        r.cache_event = ev
+        r.cache_bytes = n
+        return ev
+
+    def drop_cache(self, r) -> None:
+        buf = r.cpu_ro_cache.segment if r.cpu_ro_cache is not None else None
+        if r.cache_event is not None:
+            r.cache_event.sync()
+            r.cache_event.release()
+            r.cache_event = None
+        if isinstance(buf, D.PinnedBuffer):
+            self.pinned.put(buf)
+            r.cpu_ro_cache.segment = None
+
+    def precreate_context(self, gpu: int, alloc) -> Optional[D.Event]:
+        """DGSF: bind a pre-created context segment once, at registration."""
+        slot = D.Slot(gpu)
+        b, e = slot.bind_ctx(alloc.dptr, alloc.requested)
+        e.sync()
+        b.release()
+        e.release()
+        slot.release()
+        return None
+
+    # -------------------------------------------------------------- start -----
+    def start(self, inv, plan: StagePlan, wait_tokens=(), hooks=None, fresh_context: bool = False) -> None:
+        spec = inv.spec
+        fd = self.data_for(spec)
+        run = _Run(inv=inv, plan=plan, gpu=inv.gpu, hooks=dict(hooks or {}), fd=fd)
+        run.t_enqueue = self.sim.engine.tick()
+        inv.run = run
+        if fresh_context:
+            self._start_fixedgsl(run, fd)
+            return
+        try:
+            self._enqueue(run, fd, wait_tokens)
+        except Exception:
+            self._release(run)
+            raise
+        self.sim.engine.watch(run.end, self._on_done, run)
+
+    def _input_dst(self, run: _Run, fd: FunctionData) -> tuple[int, int]:
+        """(input dptr, out dptr) inside the private writable allocation, or an
+        unaccounted scratch segment when writable is too small."""
+        inv = run.inv
+        need = _a256(fd.input_bytes + 16) + _a256(fd.out_bytes)
+        wr = next((a for a in inv.allocations if a.cls is AllocClass.WRITABLE), None)
+        if wr is not None and wr.requested >= need and wr.dptr:
+            base = wr.dptr
+        else:
+            seg = D.pool_alloc(run.gpu, need, _lib.CLASS_WRITABLE, unaccounted=True)
+            run.scratch.append(seg)
+            base = seg.dptr
+        return base, base + _a256(fd.input_bytes + 16)
+
+    def _ro_dst(self, run: _Run) -> int:
+        inv = run.inv
+        grant = getattr(inv, "grant", None)
+        if grant is not None and grant.resident.gpu_ro is not None:
+            return grant.resident.gpu_ro.dptr          # the shared segment (leader or follower)
+        for a in inv.allocations:                      # private RO (SAGE-NR, DGSF)
+            if a.cls is AllocClass.READ_ONLY:
+                return a.dptr
+        raise SimulationError(f"{inv}: no read-only segment to land into")
+
+    def _ctx_dst(self, run: _Run) -> tuple[int, int]:
+        inv = run.inv
+        grant = getattr(inv, "grant", None)
+        if grant is not None and grant.leader_ctx:
+            a = grant.resident.gpu_ctx
+            return a.dptr, a.requested
+        for a in inv.allocations:
+            if a.cls is AllocClass.CONTEXT:
+                return a.dptr, a.requested
+        slot = getattr(inv, "ctx_slot", None)
+        if slot is not None and slot.alloc is not None:
+            return slot.alloc.dptr, slot.alloc.requested
+        return 0, 0
+
+    def _peer_source(self, run: _Run):
+        """A resident, landed copy of this function's RO on another GPU."""
+        sim = self.sim
+        if sim.gpu_count < 2 or not sim.policy_cfg.fanout or sim.sharing is None:
+            return None
+        name = run.inv.spec.name
+        best = None
+        for (n, g), r in sim.sharing.residents.items():
+            if n == name and g != run.gpu and r.gpu_ro is not None and r.ro_token is not None:
+                if best is None or r.ro_token.ready:
+                    best = r
+        return best
+
+    def _enqueue(self, run: _Run, fd: FunctionData, wait_tokens) -> None:
+        inv, plan, gpu = run.inv, run.plan, run.gpu
+        nodes = plan.nodes
+        ends: list[list] = [[] for _ in nodes]
+        run.slot = D.Slot(gpu)
+        ev = run.events
+        in_dst, out_dst = self._input_dst(run, fd)
+        grant = getattr(inv, "grant", None)
+        resident = grant.resident if grant is not None else None
+        serial = plan.mode is PlanMode.SERIAL
+        i_cpu = plan.node_index(Stage.CPU_LOAD)
+        i_gpu = plan.node_index(Stage.GPU_LOAD)
+        staged_ro = staged_in = None   # serial: pinned copies made by CPU_LOAD
+        for i, node in enumerate(nodes):
+            deps = [e for p in node.preds for e in ends[p]]
+            st = node.stage
+            if st in (Stage.CONTAINER, Stage.CPU_CTX):
+                t = self.sim.engine.tick()
+                run.marks[st] = (t, t)           # host-side, synchronous
+            elif st is Stage.CPU_LOAD:
+                if not serial:
+                    continue                     # fused into the GPU_LOAD pipeline
+                ops = []
+                if node.ro and fd.layout.packed_bytes:
+                    staged_ro = self.pinned.get(fd.layout.packed_bytes)
+                    run.pinned.append(staged_ro)
+                    b, e, _ = D.host_load(gpu, staged_ro, fd.db, deps)
+                    ops += [b, e]
+                    ends[i].append(e)
+                if fd.input_bytes:
+                    staged_in = self.pinned.get(fd.input_bytes)
+                    run.pinned.append(staged_in)
+                    b, e, _ = D.host_load(gpu, staged_in, self._payload(inv, fd), deps)
+                    ops += [b, e]
+                    ends[i].append(e)
+                ev.extend(ops)
+                run.marks[st] = (ops[0], ops[-1]) if ops else (self.sim.engine.tick(),) * 2
+            elif st is Stage.GPU_CTX:
+                dptr, nb = self._ctx_dst(run)
+                b, e = run.slot.bind_ctx(dptr, nb, deps)
+                ev += [b, e]
+                ends[i].append(e)
+                run.marks[st] = (b, e)
+                tok = run.hooks.get(Stage.GPU_CTX)
+                if tok is not None:
+                    tok.attach(e)
+            elif st is Stage.GPU_LOAD:
+                cpu_deps = [e for p in nodes[i_cpu].preds for e in ends[p]] if (i_cpu is not None and not serial) else []
+                wait = deps + cpu_deps
+                ro_end = None
+                if node.ro and fd.layout.seg_bytes:
+                    ro_end = self._load_ro(run, fd, resident, wait, staged_ro)
+                    ends[i].append(ro_end)
+                if fd.input_bytes:
+                    src = staged_in if staged_in is not None else self._payload(inv, fd)
+                    op = D.load(gpu, in_dst, src, None, pinned=staged_in is not None, wait=wait)
+                    run.loads.append(("input", op))
+                    ends[i].append(op.end)
+                if not ends[i]:
+                    e = run.slot.record()
+                    ev.append(e)
+                    ends[i].append(e)
+                tok = run.hooks.get(Stage.GPU_LOAD)
+                if tok is not None:
+                    tok.attach(ro_end if ro_end is not None else ends[i][0])
+            elif st is Stage.SYNC_WAIT:
+                tok_evs = [t.event for t in wait_tokens if not t.ready and t.event is not None]
+                b = run.slot.record()
+                run.slot.wait(deps + tok_evs)
+                e = run.slot.record()
+                ev += [b, e]
+                ends[i].append(e)
+                run.marks[st] = (b, e)
+            elif st is Stage.COMPUTE:
+                run.slot.wait(deps)
+                body = self._body(run, fd, resident, in_dst, out_dst)
+                b, e = run.slot.launch(body)
+                ev += [b, e]
+                ends[i].append(e)
+                run.marks[st] = (b, e)
+            elif st is Stage.RETURN:
+                run.slot.wait(deps)
+                run.out_bytes = fd.out_bytes
+                run.result = self.pinned.get(max(16, fd.out_bytes))
+                b, e = run.slot.ret(out_dst, run.result.ptr, fd.out_bytes)
+                ev += [b, e]
+                ends[i].append(e)
+                run.marks[st] = (b, e)
+                run.end = e
+        if run.end is None:
+            raise SimulationError("plan has no RETURN node")
+
+    def _payload(self, inv, fd: FunctionData):
+        p = getattr(inv, "payload", None)
+        if p is None:
+            return fd.input
+        if p.nbytes != fd.input_bytes:
+            raise ValueError(f"{inv}: payload of {p.nbytes} B, function expects {fd.input_bytes} B")
+        return p
+
+    def _load_ro(self, run: _Run, fd: FunctionData, resident, wait, staged_ro) -> D.Event:
+        gpu = run.gpu
+        dst = self._ro_dst(run)
+        plan = run.plan
+        i_cpu = plan.node_index(Stage.CPU_LOAD)
+        host_ro = i_cpu is not None and plan.nodes[i_cpu].ro
+        if staged_ro is not None:                                   # serial: from pinned staging
+            op = D.load(gpu, dst, staged_ro, fd.layout, wait=wait)
+            run.ro_source = "pcie"
+        elif not host_ro and resident is not None and resident.cpu_ro_cache is not None \
+                and isinstance(resident.cpu_ro_cache.segment, D.PinnedBuffer):
+            # Stage2 / Stage3 rejoin: re-land the cached (already unpacked) segment
+            w = list(wait) + ([resident.cache_event] if resident.cache_event is not None else [])
+            op = D.load(gpu, dst, resident.cpu_ro_cache.segment, None, wait=w)
+            run.ro_source = "cache"
+        else:
+            peer = self._peer_source(run) if host_ro else None
+            if peer is not None:
+                # PCIe once per box: land from the resident peer copy over NVLink
+                w = list(wait) + ([peer.ro_token.event] if (not peer.ro_token.ready and peer.ro_token.event) else [])
+                op = D.load(gpu, dst, None, None, device_src=peer.gpu_ro.dptr,
+                            device_src_bytes=fd.layout.seg_bytes, peer_gpu=peer.gpu, wait=w)
+                run.ro_source = "nvlink"
+            else:
+                op = D.load(gpu, dst, fd.db, fd.layout, wait=wait)
+                run.ro_source = "pcie"
+        run.loads.append(("ro", op))
+        return op.end
+
+    def _body(self, run: _Run, fd: FunctionData, resident, in_dst: int, out_dst: int):
+        inv = run.inv
+        ro = 0
+        if fd.layout.seg_bytes:
+            try:
+                ro = self._ro_dst(run)
+            except SimulationError:
+                ro = 0
+        in_bytes = (fd.input_bytes + 15) // 16 * 16
+        return D.body_desc(_BODY[fd.body], ro=ro, ro_bytes=fd.layout.seg_bytes, inp=in_dst, inp_bytes=in_bytes,
+                           out=out_dst, out_bytes=max(16, fd.out_bytes), args=fd.args)
+
+    # ----------------------------------------------------------- FixedGSL -----
+    def _start_fixedgsl(self, run: _Run, fd: FunctionData) -> None:
+        inv = run.inv
+        spec = inv.spec
+        run.result = self.pinned.get(max(16, fd.out_bytes))
+        run.out_bytes = fd.out_bytes
+        alloc = inv.allocations[0].effective if inv.allocations else 0
+        body = D.body_desc(_BODY[fd.body], out_bytes=max(16, fd.out_bytes), args=fd.args)
+        run.job = D.fixedgsl_submit(run.gpu, fd.layout if fd.layout.n else None,
+                                    fd.db if fd.layout.packed_bytes else None, self._payload(inv, fd),
+                                    max(0, alloc - spec.context_bytes), body, run.result, fd.out_bytes)
+        run.end = run.job.end
+        run.ro_source = "pcie"
+        self.sim.engine.watch(run.end, self._on_done, run)
+
+    # ---------------------------------------------------------- completion ----
+    def _t(self, x) -> Optional[int]:
+        if x is None:
+            return None
+        if isinstance(x, int):
+            return x
+        return self.sim.engine.to_engine_time(x.time_us())
+
+    def _on_done(self, run: _Run) -> None:
+        inv = run.inv
+        eng = self.sim.engine
+        try:
+            self._collect(run)
+        finally:
+            for tok in run.hooks.values():
+                tok.set_ready(eng.now)
+            self._release(run)
+        self.sim._on_invocation_done(inv, eng.now)
+
+    def _collect(self, run: _Run) -> None:
+        inv = run.inv
+        if run.job is not None:
+            info = run.job.info()
+            if info is None or info.status != 0:
+                raise SimulationError(f"{inv}: FixedGSL instance failed ({info.status if info else '?'}): "
+                                      f"{_lib.last_error()}")
+            for k, stage in enumerate([Stage.CONTAINER, Stage.CPU_CTX, Stage.CPU_LOAD, Stage.GPU_CTX,
+                                       Stage.GPU_LOAD, Stage.SYNC_WAIT, Stage.COMPUTE, Stage.RETURN]):
+                b, e = info.t[2 * k], info.t[2 * k + 1]
+                if b >= 0:
+                    inv.stages[stage] = [self.sim.engine.to_engine_time(b), self.sim.engine.to_engine_time(e)]
+            inv.ro_checksum = info.checksum
+            inv.teardown_us = info.teardown_us
+            inv.measured["pcie_bytes"] = run.fd.layout.packed_bytes + run.fd.input_bytes
+            inv.measured["host_bytes"] = run.fd.layout.packed_bytes
+        else:
+            for st, (b, e) in run.marks.items():
+                inv.stages[st] = [self._t(b), self._t(e)]
+            cpu_b = cpu_e = gpu_b = gpu_e = None
+            hb = lb = 0
+            for kind, op in run.loads:
+                li = op.info()
+                if li is None:
+                    raise SimulationError(f"{inv}: load not complete at RETURN")
+                if li.cpu_begin_us >= 0:
+                    cpu_b = li.cpu_begin_us if cpu_b is None else min(cpu_b, li.cpu_begin_us)
+                    cpu_e = li.cpu_end_us if cpu_e is None else max(cpu_e, li.cpu_end_us)
+                gpu_b = li.gpu_begin_us if gpu_b is None else min(gpu_b, li.gpu_begin_us)
+                gpu_e = li.gpu_end_us if gpu_e is None else max(gpu_e, li.gpu_end_us)
+                hb += li.host_bytes
+                lb += li.link_bytes
+                if kind == "ro":
+                    self._verify_ro(run, li.checksum)
+                else:
+                    inv.input_checksum = li.checksum
+            inv.measured["host_bytes"] = hb
+            inv.measured[run.ro_source + "_bytes" if run.ro_source == "nvlink" else "pcie_bytes"] = lb
+            eng = self.sim.engine
+            if Stage.GPU_LOAD not in run.marks and gpu_b is not None:
+                inv.stages[Stage.GPU_LOAD] = [eng.to_engine_time(gpu_b), eng.to_engine_time(gpu_e)]
+            elif Stage.GPU_LOAD not in run.marks:
+                t = self._t(run.t_enqueue)
+                inv.stages[Stage.GPU_LOAD] = [t, t]
+            if run.plan.node_index(Stage.CPU_LOAD) is not None and Stage.CPU_LOAD not in run.marks:
+                if cpu_b is not None:
+                    inv.stages[Stage.CPU_LOAD] = [eng.to_engine_time(cpu_b), eng.to_engine_time(cpu_e)]
+                else:
+                    t = run.t_enqueue
+                    inv.stages[Stage.CPU_LOAD] = [t, t]
+        inv.ro_source = run.ro_source
+        if run.result is not None and run.out_bytes:
+            inv.result = run.result.view()[:run.out_bytes].copy()
+
+    def _verify_ro(self, run: _Run, checksum: int) -> None:
+        inv = run.inv
+        inv.ro_checksum = checksum
+        fd = run.fd
+        grant = getattr(inv, "grant", None)
+        r = grant.resident if grant is not None else None
+        if fd.ro_checksum is None:
+            fd.ro_checksum = checksum
+        elif fd.ro_checksum != checksum:
+            raise SimulationError(f"{inv}: landed read-only segment checksum {checksum:016x} != "
+                                  f"{fd.ro_checksum:016x} (source {run.ro_source})")
+        if r is not None:
+            r.ro_checksum = checksum
+
+    def _release(self, run: _Run) -> None:
+        for _, op in run.loads:
+            op.release()
+        run.loads.clear()
+        for e in run.events:
+            e.release()
+        run.events.clear()
+        if run.slot is not None:
+            run.slot.release()
+            run.slot = None
+        for b in run.pinned:
+            self.pinned.put(b)
+        run.pinned.clear()
+        if run.result is not None:
+            self.pinned.put(run.result)
+            run.result = None
+        for s in run.scratch:
+            s.free()
+        run.scratch.clear()
+        if run.job is not None:
+            run.job.release()
+            run.job = None
+
+    def close(self) -> None:
+        self.pinned.close()

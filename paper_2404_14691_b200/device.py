@@ -80,10 +80,10 @@ class DeniedAlloc(Exception):
         self.shortfall = shortfall
 
 
-def pool_alloc(gpu: int, nbytes: int, cls: int, account_only: bool = False) -> Segment:
+def pool_alloc(gpu: int, nbytes: int, cls: int, account_only: bool = False, unaccounted: bool = False) -> Segment:
     h, d, sf = H(), C.c_uint64(), C.c_uint64()
-    rc = lib().sage_pool_alloc(gpu, nbytes, cls | (_lib.ALLOC_ACCOUNT_ONLY if account_only else 0),
-                               C.byref(h), C.byref(d), C.byref(sf))
+    flags = (_lib.ALLOC_ACCOUNT_ONLY if account_only else 0) | (0x200 if unaccounted else 0)
+    rc = lib().sage_pool_alloc(gpu, nbytes, cls | flags, C.byref(h), C.byref(d), C.byref(sf))
     if rc == _lib.SAGE_ENOMEM and sf.value:
         raise DeniedAlloc(sf.value)
     check(rc, "sage_pool_alloc")
@@ -198,6 +198,15 @@ def load(gpu: int, dst: int, src, layout=None, *, pinned: bool = False, device_s
     lh, eh = H(), H()
     check(lib().sage_segment_load(C.byref(d), C.byref(lh), C.byref(eh)), "sage_segment_load")
     return LoadOp(lh.value, Event(eh.value), keep)
+
+
+def host_load(gpu: int, dst: "PinnedBuffer", src, wait: Sequence[Event] = ()) -> tuple[Event, Event, object]:
+    """CPU_LOAD alone: memcpy src into pinned dst on the GPU's host stream."""
+    addr, n, keep = _ptr(src)
+    arr, nw = handles([e.h for e in wait])
+    b, e = H(), H()
+    check(lib().sage_host_load(gpu, dst.ptr, addr, n, arr, nw, C.byref(b), C.byref(e)), "sage_host_load")
+    return Event(b.value), Event(e.value), keep
 
 
 def segment_checksum(gpu: int, dptr: int, nbytes: int) -> int:
