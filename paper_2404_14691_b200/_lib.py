@@ -186,4 +186,7 @@ def handles(seq) -> tuple:
 
 
 def host_threads_default() -> int:
-    return max(2, min(8, (os.cpu_count() or 4) // 2))
+    """CPU_LOAD memcpy fan-out: one host thread moves ~3-5 GB/s, PCIe Gen5
+    takes ~55 GB/s, so use most cores (leave a few for the control loop)."""
+    n = os.cpu_count() or 4
+    return max(2, min(16, n - 4))

@@ -67,6 +67,34 @@ struct LandArgs {
 constexpr int kLandThreads = 256;
 constexpr int kLandU = 4;  // vectors per lane per tile
 
+// fastest path: a full tile of whole data vectors (no tail, no padding, no
+// bound checks) -- the common case inside every large tensor
+template <int WS>
+__device__ __forceinline__ unsigned long long land_tile_full(const uint4 *__restrict__ qbase, uint32_t nB,
+                                                             uint4 *__restrict__ dbase, unsigned long long pbase,
+                                                             uint32_t loc0, uint32_t lane, uint32_t bs) {
+  unsigned long long acc = 0;
+  uint4 A[kLandU], B[kLandU];
+#pragma unroll
+  for (int u = 0; u < kLandU; ++u) {
+    const uint32_t loc = loc0 + u * 32u + lane;
+    A[u] = __ldg(qbase + loc);
+    // a whole data vector with a nonzero shift always needs (and may read) the next block
+    if (WS >= 0) B[u] = __ldg(qbase + loc + 1);
+  }
+  (void)nB;
+#pragma unroll
+  for (int u = 0; u < kLandU; ++u) {
+    const uint32_t loc = loc0 + u * 32u + lane;
+    uint4 o;
+    if (WS < 0) o = A[u];
+    else o = funnel_ws<WS < 0 ? 0 : WS>(A[u], B[u], bs);
+    dbase[loc] = o;
+    acc += vec_sum(o, pbase + 2ull * loc);
+  }
+  return acc;
+}
+
 // fast path body: every vector of the tile lies in one item (warp uniform)
 template <int WS>
 __device__ __forceinline__ unsigned long long land_tile_uniform(const uint4 *__restrict__ qbase, uint32_t nB,
@@ -74,6 +102,8 @@ __device__ __forceinline__ unsigned long long land_tile_uniform(const uint4 *__r
                                                                 uint32_t loc0, uint32_t lane, uint32_t nvalid,
                                                                 uint32_t nfull, uint32_t ndata, uint32_t bs,
                                                                 long long data0) {
+  if (nvalid == 32u * kLandU && loc0 + 32u * kLandU <= nfull)
+    return land_tile_full<WS>(qbase, nB, dbase, pbase, loc0, lane, bs);
   unsigned long long acc = 0;
   uint4 A[kLandU], B[kLandU];
 #pragma unroll

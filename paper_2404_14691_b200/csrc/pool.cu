@@ -28,7 +28,7 @@ struct Pool {
   uint64_t physical = 0;   // mapped bytes
   uint64_t cached = 0;     // bytes held by the free-handle cache
   uint64_t vmm_gran = 2ull << 20;
-  std::multimap<uint64_t, CUmemGenericAllocationHandle> free_phys;
+  std::multimap<uint64_t, std::pair<CUdeviceptr, CUmemGenericAllocationHandle>> free_mapped;
   std::vector<std::pair<Alloc *, cudaEvent_t>> zombies;  // ledger-freed, pages pending an event
 };
 
@@ -72,8 +72,12 @@ int pool_create(Gpu *G, uint64_t capacity) {
 }
 
 static void release_cache(Pool *P) {
-  for (auto &kv : P->free_phys) drv.MemRelease(kv.second);
-  P->free_phys.clear();
+  for (auto &kv : P->free_mapped) {
+    drv.MemUnmap(kv.second.first, kv.first);
+    drv.MemAddressFree(kv.second.first, kv.first);
+    drv.MemRelease(kv.second.second);
+  }
+  P->free_mapped.clear();
   P->cached = 0;
 }
 
@@ -98,13 +102,16 @@ void pool_destroy(Gpu *G) {
 
 static int map_segment(Gpu *G, Pool *P, Alloc *A) {
   A->phys = round_up(A->bytes, P->vmm_gran);
-  // reuse a cached physical handle of exactly this size
+  // reuse a cached mapped segment of exactly this size: no driver call
   {
-    auto it = P->free_phys.find(A->phys);
-    if (it != P->free_phys.end()) {
-      A->ph = it->second;
-      P->free_phys.erase(it);
+    auto it = P->free_mapped.find(A->phys);
+    if (it != P->free_mapped.end()) {
+      A->va = it->second.first;
+      A->ph = it->second.second;
+      P->free_mapped.erase(it);
       P->cached -= A->phys;
+      P->physical += A->phys;
+      return SAGE_OK;
     }
   }
   if (!A->ph) {
@@ -148,14 +155,16 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
 
 static void unmap_segment(Pool *P, Alloc *A) {
   if (!A->va) return;
-  drv.MemUnmap(A->va, A->phys);
-  drv.MemAddressFree(A->va, A->phys);
   P->physical -= A->phys;
-  // keep the physical pages for reuse while the cache stays within budget
-  if (P->cached + A->phys + P->physical <= P->capacity + (4ull << 30)) {
-    P->free_phys.emplace(A->phys, A->ph);
+  // keep the segment MAPPED for reuse by the next allocation of this size
+  // (per-invocation writable churn then costs no driver call) while the
+  // cache stays within budget; otherwise unmap and release the pages
+  if (P->cached + A->phys + P->physical <= P->capacity + (4ull << 30) && P->cached + A->phys <= (16ull << 30)) {
+    P->free_mapped.emplace(A->phys, std::make_pair(A->va, A->ph));
     P->cached += A->phys;
   } else {
+    drv.MemUnmap(A->va, A->phys);
+    drv.MemAddressFree(A->va, A->phys);
     drv.MemRelease(A->ph);
   }
   A->va = 0;
