@@ -43,7 +43,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 def build_lib(force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
-    headers = list(CSRC.glob("*.h")) + [ROOT / "include" / "sage_dp.h"]
+    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "sage_dp.h"]
     objs = []
     jobs = []
     for src in SOURCES:
