@@ -1,0 +1,420 @@
+"""Benchmark of the B200 SAGE data plane (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], "cfg 2"): a burst of 64 concurrent
+invocations of the Parboil-style sgemm / stencil / spmv mix on one GPU with
+shared read-only segments (paper_2404_14691_b200/parboil.py).  One STEP = one
+burst submitted at one instant through the public API
+(`Simulation.submit_many`) and drained, starting from COLD (no resident
+segment: each step performs the three leader read-only loads and 64 input
+loads, parallel setup, 64 kernels, 64 result returns).
+
+  value  invocations/s with every DB record and input already resident in
+         HBM (loads land from HBM, no PCIe) -- the device pipeline
+  e2e    invocations/s through the same API with HOST buffers: pageable DB
+         records + request payloads, CPU_LOAD memcpy + H2D + land inside the
+         timed region, results D2H into pinned memory
+Both are whole-job aggregates over all ranks (max-over-ranks device time).
+
+Extra keys: p50/p99 setup latency (compute_begin - arrival), the cfg-1
+SAGE-vs-FixedGSL setup comparison (16 concurrent 100 MiB cold starts,
+`--cfg1`), per-kernel rooflines measured live with CUDA events, and the CPU
+baseline (the oracle's host-only loading path + numpy bodies, bounded sample).
+
+`--impl reference` times the reference's CPU path instead (the oracle port:
+host-only loading + CPU bodies on all host cores) and prints its own line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "invocations/sec (p50/p99 setup latency alongside)"
+UNIT = "invocations/s"
+
+
+def _rank_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        ids = vis.split(",") if vis else [str(i) for i in range(64)]
+        os.environ["CUDA_VISIBLE_DEVICES"] = ids[local]
+    return rank, world, local
+
+
+# --------------------------------------------------------------- clocks -------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int = 0):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- our arm --------
+def burst_names(table, burst: int):
+    names = sorted(table)
+    return [names[k % len(names)] for k in range(burst)]
+
+
+def run_steps(sim, names, steps: int):
+    """`steps` cold bursts; returns the invocations."""
+    out = []
+    for _ in range(steps):
+        if sim.sharing is not None:   # start every burst cold (no resident segment)
+            for r in list(sim.sharing.residents.values()):
+                sim.sharing._evict(r)
+        invs = sim.submit_many(names)
+        sim.drain()
+        bad = [i for i in invs if i.outcome != "completed"]
+        if bad:
+            raise RuntimeError(f"{len(bad)} invocations did not complete: {bad[0].fail_reason}")
+        out += invs
+    return out
+
+
+def timed(sim, names, steps, warmup, dist):
+    from paper_2404_14691_b200 import _lib
+    from paper_2404_14691_b200 import device as D
+    L = _lib.lib()
+    run_steps(sim, names, warmup)
+    _lib.check(L.sage_stats_reset(), "stats_reset")
+    barrier(dist)
+    _lib.check(L.sage_device_sync(0), "device_sync")
+    a = _lib.H()
+    _lib.check(L.sage_mark(0, _lib.C.byref(a)), "mark")
+    invs = run_steps(sim, names, steps)
+    _lib.check(L.sage_device_sync(0), "device_sync")
+    b = _lib.H()
+    _lib.check(L.sage_mark(0, _lib.C.byref(b)), "mark")
+    D.Event(b.value).sync()
+    us = _lib.C.c_double()
+    _lib.check(L.sage_event_elapsed(a.value, b.value, _lib.C.byref(us)), "event_elapsed")
+    D.Event(a.value).release()
+    D.Event(b.value).release()
+    elapsed = max_over_ranks(dist, us.value)
+    return elapsed, invs
+
+
+def kernel_stats():
+    from paper_2404_14691_b200 import _lib
+    L = _lib.lib()
+    out = {}
+    for kind, name in enumerate(["land", "touch", "sgemm", "stencil", "spmv"]):
+        n, t, b = _lib.u64(), _lib.C.c_double(), _lib.u64()
+        _lib.check(L.sage_stats_get(0, kind, _lib.C.byref(n), _lib.C.byref(t), _lib.C.byref(b)), "stats_get")
+        if n.value:
+            out[name] = {"launches": n.value, "total_us": t.value, "work": b.value}
+    return out
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "bf16_tflops": d.get("bf16_tflops", 1590.0),
+                "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+def cfg1_compare(n: int = 16) -> dict:
+    """BASELINE cfg 1: 16 concurrent cold starts of one 100 MiB function,
+    SAGE (parallel setup + sharing) vs FixedGSL (fresh context, serial)."""
+    from paper_2404_14691_b200.parboil import synthetic_function
+    from paper_2404_14691_b200.policies import policy_preset
+    from paper_2404_14691_b200.runtime import ClusterSpec, Simulation, summarize_setup
+    spec, data = synthetic_function("fn100", 100, 10, 1, tensors=64)
+    out = {}
+    for pol, reps in (("SAGE", 6), ("FixedGSL", 1)):
+        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), {spec.name: spec}, seed=1,
+                         function_data={spec.name: data})
+        try:
+            samples = []
+            for rep in range(reps):
+                if sim.sharing is not None:
+                    for r in list(sim.sharing.residents.values()):
+                        sim.sharing._evict(r)
+                invs = sim.submit_many([spec.name] * n)
+                sim.drain()
+                if rep >= (1 if reps > 1 else 0):   # first SAGE burst is warm-up
+                    samples += invs
+            s = summarize_setup(samples)
+            s["bursts"] = reps - (1 if reps > 1 else 0)
+            out[pol] = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in s.items()}
+        finally:
+            sim.close()
+    out["p50_setup_ratio_fixedgsl_over_sage"] = round(out["FixedGSL"]["setup_p50_ms"] / out["SAGE"]["setup_p50_ms"], 1)
+    out["workload"] = f"{n} concurrent cold starts, 100 MiB RO (64 ragged tensors), 10 MiB writable, 1 MiB input"
+    return out
+
+
+def cpu_baseline(budget_s: float = 15.0, max_inv: int = 9) -> dict:
+    """The oracle's host-only path on this box's host cores: per invocation,
+    DB record -> private buffer -> unpack -> checksum, the input copy, and the
+    function body in numpy (BLAS sgemm / vectorised stencil / spmv)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2404_14691_b200.parboil import cfg2_functions
+    table, data = cfg2_functions()
+    names = burst_names(table, max_inv)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    done = 0
+    for name in names:
+        fd = data[name]
+        lay = fd.layout
+        sums = O.hostpath_c(fd.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes, 1, cores)
+        seg, _ = O.land_c(fd.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+        x = fd.input.copy()
+        if fd.body == "sgemm":
+            m, n, k = fd.args
+            O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(k, n))
+        elif fd.body == "stencil":
+            nx, ny, nz, bits = fd.args
+            beta = float(np.int32(bits).view(np.float32))
+            O.stencil_ref(seg.view(np.float32)[:nx * ny * nz].reshape(nz, ny, nx),
+                          x.view(np.float32).reshape(nz, ny, nx), beta)
+        else:
+            rows, nnz, o_rp, o_col, o_val = fd.args
+            O.spmv_ref(seg[o_rp:o_rp + 4 * (rows + 1)].view(np.int32), seg[o_col:o_col + 4 * nnz].view(np.int32),
+                       seg[o_val:o_val + 4 * nnz].view(np.float32), x.view(np.float32))
+        done += 1
+        assert int(sums[0]) != 0
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(done / dt, 3), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{done} invocations of the cfg-2 mix (host-only load+unpack+checksum, numpy body), "
+                      f"{dt:.1f} s"}
+
+
+def our_arm(args, rank, world, dist) -> dict:
+    from paper_2404_14691_b200 import _lib
+    from paper_2404_14691_b200.parboil import cfg2_functions
+    from paper_2404_14691_b200.policies import policy_preset
+    from paper_2404_14691_b200.runtime import ClusterSpec, Simulation, percentile
+
+    table, data = cfg2_functions()
+    names = burst_names(table, args.burst)
+    sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=1, function_data=data)
+    L = _lib.lib()
+    try:
+        _lib.check(L.sage_stats_enable(1), "stats_enable")
+        # ---- e2e: host buffers through the public API -------------------------
+        clocks = ClockSampler(0).start()
+        e2e_us, invs_e2e = timed(sim, names, args.steps, args.warmup, dist)
+        clocks_e2e = clocks.stop()
+        stats_e2e = kernel_stats()
+        per_step = len(names)
+        h2d = sum(i.measured.get("pcie_bytes", 0) for i in invs_e2e) / args.steps
+        d2h = sum(data[n].out_bytes for n in names)
+        setups_e2e = [i.setup_us for i in invs_e2e]
+        # ---- value: HBM-resident sources ----------------------------------------
+        sim.dataplane.stage_sources_in_hbm(0)
+        clocks = ClockSampler(0).start()
+        val_us, invs_val = timed(sim, names, args.steps, args.warmup, dist)
+        clocks_val = clocks.stop()
+        stats_val = kernel_stats()
+        setups_val = [i.setup_us for i in invs_val]
+        gpu_launches = sum(v["launches"] for v in stats_val.values())
+        sim.dataplane.drop_hbm_sources()
+        sim.check_no_leaks()
+    finally:
+        _lib.check(L.sage_stats_enable(0), "stats_enable")
+        sim.close()
+
+    total_inv = per_step * args.steps * world
+    value = total_inv / (val_us / 1e6)
+    e2e = total_inv / (e2e_us / 1e6)
+    peaks = load_peaks()
+    rooflines = {}
+    for name, s in stats_val.items():
+        avg_us = s["total_us"] / s["launches"]
+        per_launch = s["work"] / s["launches"]
+        if name == "sgemm":
+            ach = per_launch / (avg_us * 1e-6) / 1e12
+            rooflines[name] = {"bound": "tensor", "achieved": round(ach, 2), "peak": peaks["bf16_tflops"],
+                               "unit": "TFLOP/s", "frac": round(ach / peaks["bf16_tflops"], 4),
+                               "avg_launch_us": round(avg_us, 2), "launches": s["launches"],
+                               "share_of_kernel_time": None}
+        else:
+            ach = per_launch / (avg_us * 1e-6) / 1e9
+            rooflines[name] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": round(ach / peaks["hbm_gbs"], 4), "avg_launch_us": round(avg_us, 2),
+                               "launches": s["launches"], "alg_bytes_per_launch": int(per_launch)}
+    tot = sum(s["total_us"] for s in stats_val.values()) or 1.0
+    for name, s in stats_val.items():
+        rooflines[name]["share_of_kernel_time"] = round(s["total_us"] / tot, 3)
+    land = rooflines.get("land", {})
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(val_us / 1e3 / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (bodies) / u8 (land)", "data": "synthetic",
+        "config": {"workload": f"cfg2: burst of {per_step} concurrent invocations (sgemm/stencil/spmv uniform "
+                               f"mix, shared RO segments, cold start per burst) per GPU",
+                   "policy": "SAGE", "burst": per_step, "gpus": world,
+                   "l2": "inputs larger than L2 (212 MiB RO + 504 MiB inputs per step)"},
+        "setup_p50_ms": round(percentile(setups_val, 50) / 1e3, 3),
+        "setup_p99_ms": round(percentile(setups_val, 99) / 1e3, 3),
+        "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": round(e2e_us / 1e3 / args.steps, 3),
+                "setup_p50_ms": round(percentile(setups_e2e, 50) / 1e3, 3),
+                "setup_p99_ms": round(percentile(setups_e2e, 99) / 1e3, 3),
+                "h2d_GBps": round(h2d * args.steps / e2e_us / 1e3, 2)},
+        "roofline": {"kernel": "land", "bound": "hbm", "achieved": land.get("achieved"), "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": land.get("frac"), "traffic": None,
+                     "peak_source": peaks["source"], "avg_launch_us": land.get("avg_launch_us")},
+        "rooflines": rooflines,
+        "kernels_e2e": stats_e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clocks_val,
+        "clocks_e2e": clocks_e2e,
+    }
+    return line
+
+
+def reference_arm(args, rank, world) -> dict:
+    """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
+    steps, warmup = args.steps, args.warmup
+    for _ in range(warmup):
+        cpu_baseline(budget_s=2.0, max_inv=1)
+    vals = []
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(steps):
+        b = cpu_baseline(budget_s=8.0, max_inv=3)
+        vals.append(b["value"])
+        done += 3
+    dt = time.perf_counter() - t0
+    v = done / dt
+    cores = os.cpu_count() or 1
+    return {"metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
+            "ms_per_step": round(dt * 1e3 / steps, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 (bodies) / u8 (load)", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "cfg2 mix, host-only loading path + numpy bodies (bounded sample: 3 "
+                                   "invocations per step, one per function)"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{done} invocations over {steps} steps"},
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--burst", type=int, default=64)
+    ap.add_argument("--no-cfg1", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local = _rank_env()
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(reference_arm(args, rank, world)), flush=True)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(0)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    from paper_2404_14691_b200 import _lib
+    _lib.lib()  # fail loudly if the native library is missing
+    line = our_arm(args, rank, world, dist)
+    if rank == 0 and world == 1:
+        if not args.no_cfg1:
+            line["cfg1_sage_vs_fixedgsl"] = cfg1_compare()
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -231,6 +231,26 @@ int sage_fixedgsl_submit(const sage_fixedgsl_desc *d, sage_handle *job, sage_han
 int sage_fixedgsl_info_get(sage_handle job, sage_fixedgsl_info *out);
 int sage_fixedgsl_release(sage_handle job);
 
+/* ---- measurement ------------------------------------------------------------
+ * Live kernel timing for the roofline: when enabled, every land / body launch
+ * is bracketed by CUDA events on the stream it is launched on; stats_get
+ * resolves them and reports launches, summed device time and algorithmic
+ * bytes (land: packed bytes read + segment bytes written).                    */
+#define SAGE_KERNEL_LAND     0
+#define SAGE_KERNEL_TOUCH    1
+#define SAGE_KERNEL_SGEMM    2
+#define SAGE_KERNEL_STENCIL  3
+#define SAGE_KERNEL_SPMV     4
+#define SAGE_KERNEL_KINDS    6
+int sage_stats_enable(int on);
+int sage_stats_reset(void);
+int sage_stats_get(int gpu, int kind, uint64_t *launches, double *total_us, uint64_t *bytes);
+/* drain every stream of a GPU; record a timing marker on its idle aux stream */
+int sage_device_sync(int gpu);
+int sage_mark(int gpu, sage_handle *ev);
+/* elapsed µs between two completed events of the same GPU (device clock) */
+int sage_event_elapsed(sage_handle a, sage_handle b, double *us);
+
 /* ---- test support (never on the product path) ------------------------------
  * Runs the chunk planner and the land byte semantics on the host so the
  * planner can be checked against the oracle without a GPU.                   */

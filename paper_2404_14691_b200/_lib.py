@@ -111,6 +111,12 @@ _SIGS = {
     "sage_fixedgsl_submit": (C.c_int, [C.POINTER(FixedGSLDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_fixedgsl_info_get": (C.c_int, [H, C.POINTER(FixedGSLInfo)]),
     "sage_fixedgsl_release": (C.c_int, [H]),
+    "sage_stats_enable": (C.c_int, [C.c_int]),
+    "sage_stats_reset": (C.c_int, []),
+    "sage_stats_get": (C.c_int, [C.c_int, C.c_int, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(u64)]),
+    "sage_device_sync": (C.c_int, [C.c_int]),
+    "sage_mark": (C.c_int, [C.c_int, C.POINTER(H)]),
+    "sage_event_elapsed": (C.c_int, [H, H, C.POINTER(C.c_double)]),
     "sage_debug_emulate_land": (C.c_int, [H, C.c_void_p, u64, C.c_void_p, u64, C.POINTER(u64)]),
 }
 

@@ -90,7 +90,9 @@ struct Layout;
 
 struct ChunkScratch {  // per-load device accumulator + pinned result
   unsigned long long *d_acc = nullptr;   // ring of accumulators on device
-  unsigned long long *h_res = nullptr;   // pinned mirror
+  unsigned int *d_done = nullptr;        // ring of finished-block counters
+  unsigned long long *h_res = nullptr;   // mapped pinned results (host view)
+  unsigned long long *d_res = nullptr;   // ... device view
   uint32_t n = 0;
   std::atomic<uint64_t> next{0};
 };
@@ -120,6 +122,13 @@ struct Gpu {
   struct Pool *pool = nullptr;
   // misc scratch for checksum verify
   unsigned long long *d_verify = nullptr;
+  // live kernel timing
+  struct StatRec { int kind; cudaEvent_t b, e; uint64_t bytes; };
+  std::mutex stat_mu;
+  std::vector<StatRec> stat_pending;
+  std::vector<cudaEvent_t> stat_free;
+  uint64_t stat_count[8] = {0}, stat_bytes[8] = {0};
+  double stat_us[8] = {0};
 };
 
 struct State {
@@ -153,5 +162,11 @@ int touch_all_kernels();
 
 // layouts (land.cu)
 int layouts_destroy_all();
+
+// live kernel timing (core.cu): bracket a launch on its stream when enabled
+bool stats_on();
+cudaEvent_t stat_begin(Gpu *G, cudaStream_t s);
+void stat_end(Gpu *G, cudaStream_t s, int kind, cudaEvent_t b, uint64_t bytes);
+void stats_clear_gpu(Gpu *G);
 
 }  // namespace sage

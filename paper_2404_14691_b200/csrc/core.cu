@@ -289,6 +289,55 @@ static int slot_lookup(sage_handle h, Gpu **G, cudaStream_t *s) {
 
 int slot_stream(sage_handle h, Gpu **G, cudaStream_t *s) { return slot_lookup(h, G, s); }
 
+// ------------------------------------------------------ live kernel timing --
+static std::atomic<bool> g_stats{false};
+bool stats_on() { return g_stats.load(std::memory_order_relaxed); }
+
+static cudaEvent_t stat_event(Gpu *G) {
+  cudaEvent_t e = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(G->stat_mu);
+    if (!G->stat_free.empty()) { e = G->stat_free.back(); G->stat_free.pop_back(); }
+  }
+  if (!e) cudaEventCreate(&e);
+  return e;
+}
+cudaEvent_t stat_begin(Gpu *G, cudaStream_t s) {
+  if (!stats_on()) return nullptr;
+  cudaEvent_t b = stat_event(G);
+  cudaEventRecord(b, s);
+  return b;
+}
+void stat_end(Gpu *G, cudaStream_t s, int kind, cudaEvent_t b, uint64_t bytes) {
+  if (!b) return;
+  cudaEvent_t e = stat_event(G);
+  cudaEventRecord(e, s);
+  std::lock_guard<std::mutex> lk(G->stat_mu);
+  G->stat_pending.push_back(Gpu::StatRec{kind, b, e, bytes});
+}
+static void stats_resolve(Gpu *G) {
+  std::lock_guard<std::mutex> lk(G->stat_mu);
+  for (auto &r : G->stat_pending) {
+    cudaEventSynchronize(r.e);
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.b, r.e) == cudaSuccess) {
+      G->stat_us[r.kind] += ms * 1000.0;
+      G->stat_count[r.kind] += 1;
+      G->stat_bytes[r.kind] += r.bytes;
+    }
+    G->stat_free.push_back(r.b);
+    G->stat_free.push_back(r.e);
+  }
+  G->stat_pending.clear();
+}
+void stats_clear_gpu(Gpu *G) {
+  stats_resolve(G);
+  std::lock_guard<std::mutex> lk(G->stat_mu);
+  for (int k = 0; k < 8; ++k) { G->stat_count[k] = 0; G->stat_us[k] = 0; G->stat_bytes[k] = 0; }
+  for (auto e : G->stat_free) cudaEventDestroy(e);
+  G->stat_free.clear();
+}
+
 }  // namespace sage
 
 using namespace sage;
@@ -600,6 +649,55 @@ int sage_fanout(int src_gpu, uint64_t src, int dst_gpu, uint64_t dst, uint64_t b
   Event *e;
   SAGE_TRY(event_new(dst_gpu, end_ev, &e));
   return event_record(e, D->copy);
+}
+
+int sage_stats_enable(int on) {
+  g_stats.store(on != 0);
+  return SAGE_OK;
+}
+int sage_stats_reset(void) {
+  SAGE_TRY(require_up());
+  for (auto &G : st.gpus) {
+    cudaSetDevice(G->id);
+    stats_clear_gpu(G.get());
+  }
+  return SAGE_OK;
+}
+int sage_stats_get(int gpu, int kind, uint64_t *launches, double *total_us, uint64_t *bytes) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || kind < 0 || kind >= SAGE_KERNEL_KINDS) return fail(SAGE_EINVAL, "stats_get: bad argument");
+  cudaSetDevice(gpu);
+  stats_resolve(G);
+  std::lock_guard<std::mutex> lk(G->stat_mu);
+  if (launches) *launches = G->stat_count[kind];
+  if (total_us) *total_us = G->stat_us[kind];
+  if (bytes) *bytes = G->stat_bytes[kind];
+  return SAGE_OK;
+}
+int sage_device_sync(int gpu) {
+  SAGE_TRY(require_up());
+  if (!gpu_get(gpu)) return fail(SAGE_ENODEV, "device_sync: bad gpu");
+  SAGE_CUDA(cudaSetDevice(gpu));
+  SAGE_CUDA(cudaDeviceSynchronize());
+  return SAGE_OK;
+}
+int sage_mark(int gpu, sage_handle *ev) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || !ev) return fail(SAGE_EINVAL, "mark: bad argument");
+  cudaSetDevice(gpu);
+  Event *e;
+  SAGE_TRY(event_new(gpu, ev, &e));
+  return event_record(e, G->aux);
+}
+int sage_event_elapsed(sage_handle a, sage_handle b, double *us) {
+  Event *ea = event_get(a), *eb = event_get(b);
+  if (!ea || !eb || !us || !ea->ev || !eb->ev) return fail(SAGE_EINVAL, "event_elapsed: bad events");
+  float ms = 0.f;
+  SAGE_CUDA(cudaEventElapsedTime(&ms, ea->ev, eb->ev));
+  *us = ms * 1000.0;
+  return SAGE_OK;
 }
 
 int sage_host_alloc(uint64_t bytes, sage_handle *h, void **ptr) {

@@ -214,6 +214,7 @@ int layouts_destroy_all() {
 // --------------------------------------------------------------- loads -----
 struct Load {
   int gpu = -1;
+  sage_handle hb = 0, he = 0;                 // pooled begin / end events (internal)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   std::atomic<int64_t> cpu_begin{-1}, cpu_end{-1};
   uint64_t host_bytes = 0, link_bytes = 0, landed = 0;
@@ -273,9 +274,12 @@ static int wait_list(cudaStream_t s, const sage_handle *w, int n) {
 }
 
 static int enqueue_land(Gpu *G, const Plan &P, const ChunkPlan &C, int gpu, const uint8_t *slot,
-                        uint8_t *dst, unsigned long long *acc) {
-  if (C.nvec == 0) return SAGE_OK;
+                        uint8_t *dst, uint32_t acc_idx, bool final_launch) {
+  if (C.nvec == 0 && !final_launch) return SAGE_OK;
   LandArgs a;
+  a.acc = G->scratch.d_acc + acc_idx;
+  a.done = G->scratch.d_done + acc_idx;
+  a.out = final_launch ? G->scratch.d_res + acc_idx : nullptr;
   a.items = P.d_items[gpu] + C.item_begin;
   a.prefix = P.d_prefix[gpu] + C.prefix_begin;
   a.n_items = C.item_end - C.item_begin;
@@ -283,8 +287,10 @@ static int enqueue_land(Gpu *G, const Plan &P, const ChunkPlan &C, int gpu, cons
   a.slot = slot;
   a.slot_bytes = C.se - C.sb;
   a.dst = dst;
-  a.acc = acc;
-  land_kernel<<<land_grid(G, C.nvec), kLandThreads, 0, G->land>>>(a);
+  cudaEvent_t sb = stat_begin(G, G->land);
+  land_kernel<<<C.nvec ? land_grid(G, C.nvec) : 1, kLandThreads, 0, G->land>>>(a);
+  // algorithmic bytes: the packed bytes read + the segment vectors written
+  stat_end(G, G->land, SAGE_KERNEL_LAND, sb, (C.se - C.sb) + 16ull * C.nvec);
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
 }
@@ -407,35 +413,35 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
     if (rc == SAGE_OK) rc = plan_upload(&lay->whole, d->gpu);
     if (rc != SAGE_OK) { delete L; return rc; }
   }
-  cudaError_t ce;
-  if ((ce = cudaEventCreate(&L->ev_begin)) != cudaSuccess || (ce = cudaEventCreate(&L->ev_end)) != cudaSuccess) {
-    delete L;
-    return cuda_fail(ce, "cudaEventCreate");
-  }
-  Event *E;
+  Event *E, *Eb, *Ee;
   {
     int rc = event_new(d->gpu, end_ev, &E);
+    if (rc == SAGE_OK) rc = event_new(d->gpu, &L->hb, &Eb);
+    if (rc == SAGE_OK) rc = event_new(d->gpu, &L->he, &Ee);
     if (rc != SAGE_OK) { delete L; return rc; }
   }
+  L->ev_begin = Eb->ev;
+  L->ev_end = Ee->ev;
   L->landed = lay->seg;
   L->acc_idx = (uint32_t)(G->scratch.next++ % G->scratch.n);
-  unsigned long long *acc = G->scratch.d_acc + L->acc_idx;
+  G->scratch.h_res[L->acc_idx] = 0;   // an empty load publishes nothing
   uint8_t *dst = reinterpret_cast<uint8_t *>(d->dst);
 
   std::lock_guard<std::mutex> lk(G->load_mu);  // ring order == enqueue order
   int rc = SAGE_OK;
   // the land stream owns the accumulator; user waits gate the first copy/land
   if ((rc = wait_list(G->land, d->wait, d->n_wait)) != SAGE_OK) return rc;
-  SAGE_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), G->land));
   if (dev_src) {
-    // HBM-resident (or peer, over NVLink) source: one land over the whole plan
-    SAGE_CUDA(cudaEventRecord(L->ev_begin, G->land));
+    // HBM-resident (or peer, over NVLink) source: land straight from it
+    SAGE_TRY(event_record(Eb, G->land));
     L->has_gpu_begin = true;
     const Plan &P = lay->whole;
     L->chunks = (uint32_t)P.chunks.size();
     if (d->flags & SAGE_LOAD_SRC_PEER) L->link_bytes = d->src_bytes;
-    for (const ChunkPlan &C : P.chunks) {
-      rc = enqueue_land(G, P, C, d->gpu, static_cast<const uint8_t *>(d->src) + C.sb, dst, acc);
+    for (size_t k = 0; k < P.chunks.size(); ++k) {
+      const ChunkPlan &C = P.chunks[k];
+      rc = enqueue_land(G, P, C, d->gpu, static_cast<const uint8_t *>(d->src) + C.sb, dst, L->acc_idx,
+                        k + 1 == P.chunks.size());
       if (rc != SAGE_OK) return rc;
     }
   } else {
@@ -463,22 +469,22 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
         }
         // GPU_LOAD: H2D into the device slot once its last land is done
         SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_land[r], 0));
-        if (!L->has_gpu_begin) { SAGE_CUDA(cudaEventRecord(L->ev_begin, G->copy)); L->has_gpu_begin = true; }
+        if (!L->has_gpu_begin) { SAGE_TRY(event_record(Eb, G->copy)); L->has_gpu_begin = true; }
         SAGE_CUDA(cudaMemcpyAsync(dslot, pinned ? src : pslot, n, cudaMemcpyHostToDevice, G->copy));
         SAGE_CUDA(cudaEventRecord(G->ev_h2d[r], G->copy));
         SAGE_CUDA(cudaStreamWaitEvent(G->land, G->ev_h2d[r], 0));
         L->link_bytes += n;
       } else if (!L->has_gpu_begin) {
-        SAGE_CUDA(cudaEventRecord(L->ev_begin, G->land));
+        SAGE_TRY(event_record(Eb, G->land));
         L->has_gpu_begin = true;
       }
-      if ((rc = enqueue_land(G, P, C, d->gpu, dslot, dst, acc)) != SAGE_OK) return rc;
+      if ((rc = enqueue_land(G, P, C, d->gpu, dslot, dst, L->acc_idx, k + 1 == P.chunks.size())) != SAGE_OK)
+        return rc;
       SAGE_CUDA(cudaEventRecord(G->ev_land[r], G->land));
     }
   }
-  SAGE_CUDA(cudaMemcpyAsync(G->scratch.h_res + L->acc_idx, acc, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            G->land));
-  SAGE_CUDA(cudaEventRecord(L->ev_end, G->land));
+  if (!L->has_gpu_begin) SAGE_TRY(event_record(Eb, G->land));
+  SAGE_TRY(event_record(Ee, G->land));
   if ((rc = event_record(E, G->land)) != SAGE_OK) return rc;
   uint64_t id = g_load_next++;
   {
@@ -529,8 +535,8 @@ int sage_load_release(sage_handle h) {
   }
   cudaSetDevice(L->gpu);
   cudaEventSynchronize(L->ev_end);  // host copies reference L until the end
-  cudaEventDestroy(L->ev_begin);
-  cudaEventDestroy(L->ev_end);
+  sage_event_release(L->hb);
+  sage_event_release(L->he);
   delete L;
   return SAGE_OK;
 }

@@ -61,8 +61,30 @@ struct LandArgs {
   const uint8_t *slot;     // 16-B aligned base holding packed [sb, se)
   unsigned long long slot_bytes;
   uint8_t *dst;            // segment base (16-B aligned)
-  unsigned long long *acc; // checksum accumulator
+  unsigned long long *acc; // checksum accumulator (zero between loads)
+  unsigned int *done;      // blocks finished in the final launch (zero between loads)
+  unsigned long long *out; // final launch only: mapped pinned result (else null)
 };
+
+// The last block of a load's final launch publishes the checksum straight to
+// mapped pinned host memory and re-arms the accumulator: no memset or D2H
+// copy is enqueued per load.
+__device__ __forceinline__ void land_finalize(const LandArgs &a) {
+  if (a.out == nullptr) return;
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long v = atomicExch(a.acc, 0ull);
+    *reinterpret_cast<volatile unsigned long long *>(a.out) = v;
+    *a.done = 0;
+    __threadfence_system();
+  }
+}
 
 constexpr int kLandThreads = 256;
 constexpr int kLandU = 4;  // vectors per lane per tile
@@ -202,6 +224,7 @@ __global__ void __launch_bounds__(kLandThreads, 4) land_kernel(const __grid_cons
     }
   }
   block_reduce_add(acc, a.acc);
+  land_finalize(a);
 }
 
 // checksum of a landed segment (verify / dedup): one read-only pass

@@ -210,8 +210,12 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
   // checksum accumulators: one per in-flight load
   G->scratch.n = 4096;
   SAGE_CUDA(cudaMalloc((void **)&G->scratch.d_acc, G->scratch.n * sizeof(unsigned long long)));
+  SAGE_CUDA(cudaMalloc((void **)&G->scratch.d_done, G->scratch.n * sizeof(unsigned int)));
+  SAGE_CUDA(cudaMemset(G->scratch.d_acc, 0, G->scratch.n * sizeof(unsigned long long)));
+  SAGE_CUDA(cudaMemset(G->scratch.d_done, 0, G->scratch.n * sizeof(unsigned int)));
   SAGE_CUDA(cudaHostAlloc((void **)&G->scratch.h_res, G->scratch.n * sizeof(unsigned long long),
-                          cudaHostAllocPortable));
+                          cudaHostAllocPortable | cudaHostAllocMapped));
+  SAGE_CUDA(cudaHostGetDevicePointer((void **)&G->scratch.d_res, G->scratch.h_res, 0));
   SAGE_CUDA(cudaMalloc((void **)&G->d_verify, 64));
   // clock anchor
   SAGE_CUDA(cudaEventCreate(&G->anchor));
@@ -229,6 +233,7 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
 
 void gpu_teardown(Gpu *G) {
   cudaSetDevice(G->id);
+  stats_clear_gpu(G);
   pool_destroy(G);
   for (auto s : G->slots) cudaStreamDestroy(s);
   G->slots.clear();
@@ -241,6 +246,7 @@ void gpu_teardown(Gpu *G) {
   if (G->pin) cudaFreeHost(G->pin);
   if (G->dstage) cudaFree(G->dstage);
   if (G->scratch.d_acc) cudaFree(G->scratch.d_acc);
+  if (G->scratch.d_done) cudaFree(G->scratch.d_done);
   if (G->scratch.h_res) cudaFreeHost(G->scratch.h_res);
   if (G->d_verify) cudaFree(G->d_verify);
 }

@@ -75,6 +75,9 @@ class FunctionData:
     input: Optional[np.ndarray] = None
     out_bytes: int = 16
     ro_checksum: Optional[int] = None     # learnt from the first landed copy
+    # HBM-resident sources (bench `value` leg: inputs already in HBM, no PCIe)
+    db_dev: Optional[D.Segment] = None
+    input_dev: Optional[D.Segment] = None
 
     @property
     def input_bytes(self) -> int:
@@ -172,6 +175,28 @@ class DataPlane:
         if data.layout.packed_bytes != data.db.nbytes:
             raise ValueError(f"function {name}: DB record size differs from its layout")
         self.data[name] = data
+
+    def stage_sources_in_hbm(self, gpu: int = 0) -> None:
+        """Copy every registered function's DB record and default input into
+        HBM (runtime scratch, outside the ledger): loads then land from HBM
+        with no PCIe leg -- the device-resident `value` measurement."""
+        for name, fd in self.data.items():
+            for attr, host in (("db_dev", fd.db), ("input_dev", fd.input)):
+                if host is None or host.nbytes == 0 or getattr(fd, attr) is not None:
+                    continue
+                seg = D.pool_alloc(gpu, host.nbytes + 64, _lib.CLASS_WRITABLE, unaccounted=True)
+                op = D.load(gpu, seg.dptr, host, None)
+                op.wait()
+                op.release()
+                setattr(fd, attr, seg)
+
+    def drop_hbm_sources(self) -> None:
+        for fd in self.data.values():
+            for attr in ("db_dev", "input_dev"):
+                seg = getattr(fd, attr)
+                if seg is not None:
+                    seg.free()
+                    setattr(fd, attr, None)
 
     def data_for(self, spec: FunctionSpec) -> FunctionData:
         fd = self.data.get(spec.name)
@@ -336,8 +361,12 @@ class DataPlane:
                     ro_end = self._load_ro(run, fd, resident, wait, staged_ro)
                     ends[i].append(ro_end)
                 if fd.input_bytes:
-                    src = staged_in if staged_in is not None else self._payload(inv, fd)
-                    op = D.load(gpu, in_dst, src, None, pinned=staged_in is not None, wait=wait)
+                    if fd.input_dev is not None and getattr(inv, "payload", None) is None:
+                        op = D.load(gpu, in_dst, None, None, device_src=fd.input_dev.dptr,
+                                    device_src_bytes=fd.input_bytes, wait=wait)
+                    else:
+                        src = staged_in if staged_in is not None else self._payload(inv, fd)
+                        op = D.load(gpu, in_dst, src, None, pinned=staged_in is not None, wait=wait)
                     run.loads.append(("input", op))
                     ends[i].append(op.end)
                 if not ends[i]:
@@ -405,6 +434,10 @@ class DataPlane:
                 op = D.load(gpu, dst, None, None, device_src=peer.gpu_ro.dptr,
                             device_src_bytes=fd.layout.seg_bytes, peer_gpu=peer.gpu, wait=w)
                 run.ro_source = "nvlink"
+            elif fd.db_dev is not None:
+                op = D.load(gpu, dst, None, fd.layout, device_src=fd.db_dev.dptr,
+                            device_src_bytes=fd.layout.packed_bytes, wait=wait)
+                run.ro_source = "hbm"
             else:
                 op = D.load(gpu, dst, fd.db, fd.layout, wait=wait)
                 run.ro_source = "pcie"
