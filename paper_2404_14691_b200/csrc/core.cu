@@ -619,7 +619,8 @@ int sage_return(sage_handle slot, uint64_t src, void *host_dst, uint64_t bytes, 
   SAGE_TRY(event_record(b, s));
   if (bytes) {
     if (!host_dst || !src) return fail(SAGE_EINVAL, "return: null buffer");
-    SAGE_CUDA(cudaMemcpyAsync(host_dst, (const void *)src, bytes, cudaMemcpyDeviceToHost, s));
+    // UVA: the destination is pinned host memory (D2H) or an HBM buffer (D2D)
+    SAGE_CUDA(cudaMemcpyAsync(host_dst, (const void *)src, bytes, cudaMemcpyDefault, s));
   }
   SAGE_TRY(event_new(G->id, end_ev, &e));
   return event_record(e, s);

@@ -165,6 +165,7 @@ class DataPlane:
         self.sim = sim
         self.pinned = _PinnedPool()
         self.data: dict[str, FunctionData] = {}
+        self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
 
     # ---------------------------------------------------------------- data ----
     def register(self, name: str, data: FunctionData) -> None:
@@ -394,8 +395,14 @@ class DataPlane:
             elif st is Stage.RETURN:
                 run.slot.wait(deps)
                 run.out_bytes = fd.out_bytes
-                run.result = self.pinned.get(max(16, fd.out_bytes))
-                b, e = run.slot.ret(out_dst, run.result.ptr, fd.out_bytes)
+                if self.results_in_hbm:
+                    # device-resident measurement: results stay in HBM (D2D)
+                    seg = D.pool_alloc(gpu, max(256, fd.out_bytes), _lib.CLASS_WRITABLE, unaccounted=True)
+                    run.scratch.append(seg)
+                    b, e = run.slot.ret(out_dst, seg.dptr, fd.out_bytes)
+                else:
+                    run.result = self.pinned.get(max(16, fd.out_bytes))
+                    b, e = run.slot.ret(out_dst, run.result.ptr, fd.out_bytes)
                 ev += [b, e]
                 ends[i].append(e)
                 run.marks[st] = (b, e)
@@ -484,11 +491,16 @@ class DataPlane:
         eng = self.sim.engine
         try:
             self._collect(run)
+            for tok in run.hooks.values():
+                tok.set_ready(eng.now)
+            # listeners see inv.result as a zero-copy view of the returned bytes
+            self.sim._on_invocation_done(inv, eng.now)
+            if inv.result is not None:
+                inv.result = inv.result.copy() if self.sim.copy_results else None
         finally:
             for tok in run.hooks.values():
                 tok.set_ready(eng.now)
             self._release(run)
-        self.sim._on_invocation_done(inv, eng.now)
 
     def _collect(self, run: _Run) -> None:
         inv = run.inv
@@ -541,8 +553,8 @@ class DataPlane:
                     t = run.t_enqueue
                     inv.stages[Stage.CPU_LOAD] = [t, t]
         inv.ro_source = run.ro_source
-        if run.result is not None and run.out_bytes:
-            inv.result = run.result.view()[:run.out_bytes].copy()
+        if isinstance(run.result, D.PinnedBuffer) and run.out_bytes:
+            inv.result = run.result.view()[:run.out_bytes]
 
     def _verify_ro(self, run: _Run, checksum: int) -> None:
         inv = run.inv

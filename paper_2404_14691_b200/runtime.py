@@ -118,7 +118,7 @@ class Simulation:
 
     def __init__(self, cluster: ClusterSpec, policy_cfg: PolicyConfig, spec_table: dict, source=None, seed: int = 0,
                  duration_us: int = 0, log_events: bool = False, register_functions=None,
-                 function_data: Optional[dict] = None, init_device: bool = True):
+                 function_data: Optional[dict] = None, init_device: bool = True, copy_results: bool = True):
         self.cluster = cluster
         self.policy_cfg = policy_cfg
         self.spec_table = spec_table
@@ -161,6 +161,9 @@ class Simulation:
             names = register_functions if register_functions is not None else sorted(spec_table)
             for name in names:
                 self.policy.register(self.spec_table[name])
+        # copy_results=False: inv.result is only valid inside completion
+        # listeners (zero-copy view of the pinned return buffer)
+        self.copy_results = copy_results
         self.invocations: list[Invocation] = []
         self.completion_listeners = []
         self._ids = itertools.count()
