@@ -78,6 +78,7 @@ static int run_job(Job *J) {
     for (size_t i = 0; rc == SAGE_OK && i < J->len.size(); ++i)
       if (J->len[i] && (e = cudaMemcpy(ro + J->dst_off[i], priv + J->src_off[i], J->len[i], cudaMemcpyHostToDevice)) != cudaSuccess)
         rc = cuda_fail(e, "fixedgsl cudaMemcpy");
+    if (rc == SAGE_OK && in_b && (e = cudaMemset(in, 0, in_b)) != cudaSuccess) rc = cuda_fail(e, "fixedgsl memset");
     if (rc == SAGE_OK && d.input_bytes && (e = cudaMemcpy(in, d.input, d.input_bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
       rc = cuda_fail(e, "fixedgsl input cudaMemcpy");
     stamp(J, GPU_LOAD, true);
@@ -86,7 +87,7 @@ static int run_job(Job *J) {
       stamp(J, COMPUTE, false);
       sage_body_desc b = d.body;
       b.ro = (uint64_t)ro; b.ro_bytes = ro_b;
-      b.input = (uint64_t)in; b.input_bytes = d.input_bytes;
+      b.input = (uint64_t)in; b.input_bytes = (d.input_bytes + 15) & ~15ull;
       b.out = (uint64_t)out; b.out_bytes = d.body.out_bytes;
       rc = launch_body(&b, 0, gpu_get(d.gpu)->sm_count);
       if (rc == SAGE_OK && (e = cudaDeviceSynchronize()) != cudaSuccess) rc = cuda_fail(e, "fixedgsl compute");

@@ -183,15 +183,24 @@ class Engine:
         return self._heap[0][0] if self._heap else None
 
     def step(self) -> int:
-        """Dispatch everything due now plus completed device work; returns count."""
-        self.tick()
+        """Dispatch everything due now plus completed device work; returns count.
+
+        A timer runs with `now` = its scheduled instant (as in the reference),
+        so chained timers (the four decay stages) never accumulate lateness."""
+        wall = max(self.wall_us(), self._now)
         n = 0
-        while True:
-            ev = self._pop_due()
-            if ev is None:
+        while self._heap:
+            t, _, ev = self._heap[0]
+            if ev.cancelled:
+                heapq.heappop(self._heap)
+                continue
+            if t > wall:
                 break
+            heapq.heappop(self._heap)
+            self._now = max(self._now, t)
             self._dispatch(ev)
             n += 1
+        self._now = max(self._now, wall)
         n += self._poll_watches(0)
         return n
 
