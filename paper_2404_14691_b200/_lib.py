@@ -160,12 +160,23 @@ def init(n_gpus: int = 1, pool_bytes: int = 0, staging_bytes: int = 0, chunk_byt
     check(L.sage_set_host_threads(host_threads or host_threads_default()), "sage_set_host_threads")
     check(L.sage_init(n_gpus, pool_bytes, staging_bytes, chunk_bytes, flags), "sage_init")
     _generation += 1
+    global _up
+    _up = True
+
+
+_up = False
+
+
+def is_up() -> bool:
+    return _up
 
 
 def shutdown() -> None:
     global _generation
     check(lib().sage_shutdown(), "sage_shutdown")
     _generation += 1
+    global _up
+    _up = False
 
 
 def exported_symbols() -> list[str]:

@@ -127,7 +127,7 @@ class Simulation:
         self.gpu_count = cluster.gpus
         self.pre_warmed = cluster.pre_warmed_containers
         self._owns_device = False
-        if init_device:
+        if init_device and not _lib.is_up():
             _lib.init(n_gpus=cluster.gpus, pool_bytes=int(cluster.gpu_mem_mb * (1 << 20)) + (8 << 30),
                       staging_bytes=int(cluster.staging_mb * (1 << 20)), chunk_bytes=int(cluster.chunk_mb * (1 << 20)),
                       flags=_lib.SAGE_INIT_PEER_ACCESS if cluster.gpus > 1 else 0,

@@ -40,7 +40,7 @@ def built():
     return True
 
 
-@pytest.fixture(scope="session")
+@pytest.fixture(scope="module")
 def dp(built):
     """Initialised data plane on GPU 0 (session scoped)."""
     from paper_2404_14691_b200 import _lib
