@@ -536,6 +536,7 @@ class DataPlane:
                 lb += li.link_bytes
                 if kind == "ro":
                     self._verify_ro(run, li.checksum)
+                    inv.ro_landed_us = self.sim.engine.to_engine_time(li.gpu_end_us)
                 else:
                     inv.input_checksum = li.checksum
             inv.measured["host_bytes"] = hb

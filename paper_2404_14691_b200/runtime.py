@@ -63,7 +63,7 @@ class Invocation:
     __slots__ = ("id", "spec", "arrival_us", "gpu", "start_us", "completion_us", "warmth", "outcome", "stages",
                  "host_bytes_umb", "pcie_bytes_umb", "allocations", "grant", "ctx_slot", "was_queued",
                  "fail_reason", "private", "run", "payload", "result", "measured", "ro_checksum",
-                 "input_checksum", "ro_source", "teardown_us")
+                 "input_checksum", "ro_source", "teardown_us", "ro_landed_us")
 
     def __init__(self, iid: int, spec: FunctionSpec, arrival_us: int, payload=None):
         self.id = iid
@@ -91,6 +91,7 @@ class Invocation:
         self.input_checksum: Optional[int] = None
         self.ro_source = ""
         self.teardown_us = None
+        self.ro_landed_us: Optional[int] = None   # when this invocation's RO load landed
 
     def mark_queued(self) -> None:
         self.was_queued = True

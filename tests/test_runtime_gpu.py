@@ -56,8 +56,8 @@ def check_against(invs, want):
         assert g.pcie_bytes_umb == w["pcie_bytes_umb"] and g.host_bytes_umb == w["host_bytes_umb"], (g.id, w)
     leaders = {}
     for g in invs:
-        if g.warmth.label() != "Stage1Hot" and g.ro_checksum is not None:
-            leaders[(g.spec.name, g.gpu)] = g.stages[Stage.GPU_LOAD][1]
+        if g.warmth.label() != "Stage1Hot" and g.ro_landed_us is not None:
+            leaders[(g.spec.name, g.gpu)] = g.ro_landed_us
         elif g.warmth.label() == "Stage1Hot" and (g.spec.name, g.gpu) in leaders:
             assert g.stages[Stage.COMPUTE][0] >= leaders[(g.spec.name, g.gpu)], g
 
