@@ -155,7 +155,7 @@ def kernel_stats():
     from paper_2404_14691_b200 import _lib
     L = _lib.lib()
     out = {}
-    for kind, name in enumerate(["land", "touch", "sgemm", "stencil", "spmv"]):
+    for kind, name in enumerate(["land", "touch", "sgemm", "stencil", "spmv", "verify"]):
         n, t, b = _lib.u64(), _lib.C.c_double(), _lib.u64()
         _lib.check(L.sage_stats_get(0, kind, _lib.C.byref(n), _lib.C.byref(t), _lib.C.byref(b)), "stats_get")
         if n.value:

@@ -241,6 +241,7 @@ int sage_fixedgsl_release(sage_handle job);
 #define SAGE_KERNEL_SGEMM    2
 #define SAGE_KERNEL_STENCIL  3
 #define SAGE_KERNEL_SPMV     4
+#define SAGE_KERNEL_VERIFY   5   /* direct-path checksum of DMA'd identity loads */
 #define SAGE_KERNEL_KINDS    6
 int sage_stats_enable(int on);
 int sage_stats_reset(void);

@@ -102,6 +102,7 @@ struct Gpu {
   int sm_count = 0;
   CUcontext primary = nullptr;
   cudaStream_t copy = nullptr, land = nullptr, host = nullptr, d2h = nullptr, aux = nullptr;
+  cudaStream_t direct = nullptr;          // pinned identity loads: DMA + verify, off the ring
   std::vector<cudaStream_t> slots;        // pre-created stream pool (the "context pool")
   std::vector<int> slot_free;             // free slot indices
   std::mutex slot_mu;

@@ -427,6 +427,43 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
   G->scratch.h_res[L->acc_idx] = 0;   // an empty load publishes nothing
   uint8_t *dst = reinterpret_cast<uint8_t *>(d->dst);
 
+  if (!d->layout && !dev_src && (d->flags & SAGE_LOAD_SRC_PINNED) && d->src_bytes &&
+      lay->seg / 16 < 0xFFFFFFFFull) {
+    // direct path: an identity load from pinned memory needs no staging or
+    // unpack -- one DMA straight into dst on its own stream (so it never
+    // queues behind memcpy-gated ring chunks) + a read-only verify pass
+    cudaStream_t s = G->direct;
+    std::lock_guard<std::mutex> lk(G->load_mu);
+    SAGE_TRY(wait_list(s, d->wait, d->n_wait));
+    SAGE_TRY(event_record(Eb, s));
+    L->has_gpu_begin = true;
+    const uint64_t n = d->src_bytes, seg = lay->seg;
+    if (seg > n) SAGE_CUDA(cudaMemsetAsync(dst + n, 0, seg - n, s));
+    SAGE_CUDA(cudaMemcpyAsync(dst, d->src, n, cudaMemcpyHostToDevice, s));
+    L->link_bytes = n;
+    L->chunks = 1;
+    LandArgs a{};
+    a.dst = dst;
+    a.total_vec = (uint32_t)(seg / 16);
+    a.acc = G->scratch.d_acc + L->acc_idx;
+    a.done = G->scratch.d_done + L->acc_idx;
+    a.out = G->scratch.d_res + L->acc_idx;
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((seg / 16 + 1023) / 1024, G->sm_count * 8ull));
+    cudaEvent_t sb = stat_begin(G, s);
+    verify_kernel<<<blocks, 256, 0, s>>>(a);
+    SAGE_CUDA(cudaGetLastError());
+    stat_end(G, s, SAGE_KERNEL_VERIFY, sb, seg);
+    SAGE_TRY(event_record(Ee, s));
+    SAGE_TRY(event_record(E, s));
+    uint64_t id = g_load_next++;
+    {
+      std::lock_guard<std::mutex> lk2(g_load_mu);
+      g_loads[id] = L;
+    }
+    *load_out = make_handle(Kind::Load, id);
+    return SAGE_OK;
+  }
+
   std::lock_guard<std::mutex> lk(G->load_mu);  // ring order == enqueue order
   int rc = SAGE_OK;
   // the land stream owns the accumulator; user waits gate the first copy/land

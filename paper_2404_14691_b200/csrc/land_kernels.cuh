@@ -242,6 +242,24 @@ __global__ void __launch_bounds__(256) checksum_kernel(const uint4 *__restrict__
   block_reduce_add(acc, out);
 }
 
+// direct-path verify: checksum of bytes a DMA already placed (identity loads
+// from pinned memory), published like a land's final launch
+__global__ void __launch_bounds__(256) verify_kernel(const __grid_constant__ LandArgs a) {
+  const uint4 *p = reinterpret_cast<const uint4 *>(a.dst);
+  const unsigned long long nvec = a.total_vec;
+  unsigned long long acc = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 v0 = __ldg(p + i), v1 = __ldg(p + i + stride), v2 = __ldg(p + i + 2 * stride), v3 = __ldg(p + i + 3 * stride);
+    acc += vec_sum(v0, 2 * i) + vec_sum(v1, 2 * (i + stride)) + vec_sum(v2, 2 * (i + 2 * stride)) +
+           vec_sum(v3, 2 * (i + 3 * stride));
+  }
+  for (; i < nvec; i += stride) acc += vec_sum(__ldg(p + i), 2 * i);
+  block_reduce_add(acc, a.acc);
+  land_finalize(a);
+}
+
 static int g_land_occ = 0;  // resident land blocks per SM (occupancy API)
 
 static int land_grid(Gpu *G, uint32_t total_vec) {

@@ -182,6 +182,7 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
   int lo = 0, hi = 0;
   SAGE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   SAGE_CUDA(cudaStreamCreateWithPriority(&G->copy, cudaStreamNonBlocking, hi));
+  SAGE_CUDA(cudaStreamCreateWithPriority(&G->direct, cudaStreamNonBlocking, hi));
   SAGE_CUDA(cudaStreamCreateWithPriority(&G->land, cudaStreamNonBlocking, hi));
   SAGE_CUDA(cudaStreamCreateWithFlags(&G->host, cudaStreamNonBlocking));
   SAGE_CUDA(cudaStreamCreateWithFlags(&G->d2h, cudaStreamNonBlocking));
@@ -237,7 +238,7 @@ void gpu_teardown(Gpu *G) {
   pool_destroy(G);
   for (auto s : G->slots) cudaStreamDestroy(s);
   G->slots.clear();
-  for (cudaStream_t s : {G->copy, G->land, G->host, G->d2h, G->aux})
+  for (cudaStream_t s : {G->copy, G->direct, G->land, G->host, G->d2h, G->aux})
     if (s) cudaStreamDestroy(s);
   for (auto e : G->ev_cpu) cudaEventDestroy(e);
   for (auto e : G->ev_h2d) cudaEventDestroy(e);

@@ -115,3 +115,29 @@ def test_pool_denied_and_usage(dp):
     assert D.pool_usage(0)["ledger"] == u0["ledger"]
     with pytest.raises(D._lib.SageError):
         D._lib.check(D.lib().sage_pool_free(s.h or 0x0300000000000001), "double free")
+
+
+def test_direct_path_identity_pinned(dp):
+    """Identity loads from pinned memory take the direct DMA + verify path;
+    bytes and checksum equal the oracle's (incl. zero padding to 16)."""
+    for n in (1, 15, 16, 4097, 3 << 20, (9 << 20) + 5):
+        db = O.db_bytes(n, n)
+        pb = D.PinnedBuffer(n)
+        pb.view()[:] = db
+        seg_bytes = (n + 15) // 16 * 16
+        seg = D.pool_alloc(0, seg_bytes, D._lib.CLASS_WRITABLE)
+        # dirty the destination first: the padding must be re-zeroed
+        junk = D.PinnedBuffer(seg_bytes)
+        junk.view()[:] = 0xAB
+        D.load(0, seg.dptr, junk, None).wait()
+        op = D.load(0, seg.dptr, pb, None)
+        res = op.wait()
+        want_seg = np.zeros(seg_bytes, np.uint8)
+        want_seg[:n] = db
+        assert res.checksum == O.checksum_c(want_seg), n
+        assert np.array_equal(D.read_device(0, seg.dptr, seg_bytes), want_seg), n
+        assert res.link_bytes == n and res.host_bytes == 0
+        op.release()
+        seg.free()
+        pb.free()
+        junk.free()
