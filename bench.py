@@ -314,9 +314,15 @@ def our_arm(args, rank, world, dist) -> dict:
             pb = D.PinnedBuffer(data[n].input_bytes)
             pb.view()[:] = data[n].input
             payloads.append(pb)
+        # (a) DB records pageable: every cold load pays the CPU_LOAD memcpy
+        pg_us, invs_pg = timed(sim, names, args.steps, args.warmup, dist, payloads)
+        # (b) the daemon's host store pinned at registration (outside the timed
+        #     region): cold loads DMA straight from it -- the headline e2e
+        sim.dataplane.pin_host_store()
         clocks = ClockSampler(0).start()
         e2e_us, invs_e2e = timed(sim, names, args.steps, args.warmup, dist, payloads)
         clocks_e2e = clocks.stop()
+        sim.dataplane.unpin_host_store()
         for pb in payloads:
             pb.free()
         stats_e2e = kernel_stats()
@@ -384,7 +390,13 @@ def our_arm(args, rank, world, dist) -> dict:
                 "ms_per_step": round(e2e_us / 1e3 / args.steps, 3),
                 "setup_p50_ms": round(percentile(setups_e2e, 50) / 1e3, 3),
                 "setup_p99_ms": round(percentile(setups_e2e, 99) / 1e3, 3),
-                "h2d_GBps": round(h2d * args.steps / e2e_us / 1e3, 2)},
+                "h2d_GBps": round(h2d * args.steps / e2e_us / 1e3, 2),
+                "inputs": "request payloads in pinned host buffers; DB records in the pinned host store",
+                "pageable_db": {"value": round(total_inv / (pg_us / 1e6), 2), "unit": UNIT,
+                                "ms_per_step": round(pg_us / 1e3 / args.steps, 3),
+                                "setup_p50_ms": round(percentile([i.setup_us for i in invs_pg], 50) / 1e3, 3),
+                                "setup_p99_ms": round(percentile([i.setup_us for i in invs_pg], 99) / 1e3, 3),
+                                "note": "DB records pageable: cold loads include the CPU_LOAD memcpy"}},
         "roofline": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": land["frac"], "traffic": None, "peak_source": peaks["source"],
                      "avg_launch_us": land["avg_launch_us"], "alg_bytes_per_launch": land["alg_bytes_per_launch"],

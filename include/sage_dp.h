@@ -92,6 +92,10 @@ int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes);
 /* ---- pinned host buffers (the Stage-2 CPU read-only cache, sharing.py:226-228) */
 int sage_host_alloc(uint64_t bytes, sage_handle *h, void **ptr);
 int sage_host_free(sage_handle h);
+/* pin an existing host range (the memory daemon's host-side DB store): loads
+ * from it skip the staging memcpy and DMA straight from it                  */
+int sage_host_register(void *ptr, uint64_t bytes);
+int sage_host_unregister(void *ptr);
 
 /* ---- segment layouts ------------------------------------------------------
  * A layout maps a PACKED host stream (tensors back to back at arbitrary byte
@@ -133,6 +137,8 @@ int sage_ctx_bind(sage_handle slot, uint64_t ctx_dptr, uint64_t ctx_bytes,
                   sage_handle *end_ev);
 /* make the slot's stream wait for events (the SYNC_WAIT node)                */
 int sage_stream_wait(sage_handle slot, const sage_handle *evs, int n);
+/* SYNC_WAIT as one call: begin event, device-side wait on evs, end event     */
+int sage_sync_wait(sage_handle slot, const sage_handle *evs, int n, sage_handle *begin_ev, sage_handle *end_ev);
 int sage_slot_record(sage_handle slot, sage_handle *ev);
 
 /* ---- loads ----------------------------------------------------------------
@@ -198,6 +204,11 @@ typedef struct {
   uint64_t ro_bytes, input_bytes, out_bytes;
   int64_t  args[8];   /* body-specific shape parameters                 */
 } sage_body_desc;
+/* the same with the node's predecessors' END events waited on first         */
+int sage_launch_after(sage_handle slot, const sage_handle *wait, int n_wait, const sage_body_desc *b,
+                      sage_handle *begin_ev, sage_handle *end_ev);
+int sage_return_after(sage_handle slot, const sage_handle *wait, int n_wait, uint64_t src_dptr, void *dst,
+                      uint64_t bytes, sage_handle *begin_ev, sage_handle *end_ev);
 int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handle *begin_ev,
                 sage_handle *end_ev);
 /* D2H the result on the slot's stream (the RETURN node)                      */

@@ -84,6 +84,8 @@ _SIGS = {
     "sage_pool_dptr": (C.c_int, [H, C.POINTER(u64), C.POINTER(u64)]),
     "sage_host_alloc": (C.c_int, [u64, C.POINTER(H), C.POINTER(C.c_void_p)]),
     "sage_host_free": (C.c_int, [H]),
+    "sage_host_register": (C.c_int, [C.c_void_p, u64]),
+    "sage_host_unregister": (C.c_int, [C.c_void_p]),
     "sage_layout_create": (C.c_int, [C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.c_uint32, u64, u64,
                                      C.POINTER(H)]),
     "sage_layout_destroy": (C.c_int, [H]),
@@ -107,6 +109,9 @@ _SIGS = {
     "sage_d2h_cache": (C.c_int, [C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
     "sage_fanout": (C.c_int, [C.c_int, u64, C.c_int, u64, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
     "sage_launch": (C.c_int, [H, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
+    "sage_launch_after": (C.c_int, [H, C.POINTER(H), C.c_int, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
+    "sage_return_after": (C.c_int, [H, C.POINTER(H), C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),
+    "sage_sync_wait": (C.c_int, [H, C.POINTER(H), C.c_int, C.POINTER(H), C.POINTER(H)]),
     "sage_return": (C.c_int, [H, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),
     "sage_fixedgsl_submit": (C.c_int, [C.POINTER(FixedGSLDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_fixedgsl_info_get": (C.c_int, [H, C.POINTER(FixedGSLInfo)]),

@@ -227,6 +227,15 @@ int touch_all_kernels() {
 
 using namespace sage;
 
+extern "C" int sage_launch_after(sage_handle slot, const sage_handle *wait, int n_wait, const sage_body_desc *b,
+                                 sage_handle *begin_ev, sage_handle *end_ev) {
+  Gpu *G; cudaStream_t s;
+  SAGE_TRY(slot_stream(slot, &G, &s));
+  cudaSetDevice(G->id);
+  SAGE_TRY(wait_events(s, wait, n_wait));
+  return sage_launch(slot, b, begin_ev, end_ev);
+}
+
 extern "C" int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handle *begin_ev, sage_handle *end_ev) {
   if (!b || !begin_ev || !end_ev) return fail(SAGE_EINVAL, "launch: null argument");
   Gpu *G; cudaStream_t s;

@@ -157,6 +157,7 @@ void pool_destroy(Gpu *g);
 int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chunk);
 void gpu_teardown(Gpu *G);
 int slot_stream(sage_handle h, Gpu **G, cudaStream_t *s);
+int wait_events(cudaStream_t s, const sage_handle *w, int n);
 // bodies (bodies.cu)
 int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count);
 int touch_all_kernels();

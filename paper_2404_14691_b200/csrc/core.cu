@@ -563,7 +563,9 @@ int sage_ctx_release(sage_handle slot) {
   return SAGE_OK;
 }
 
-static int wait_events(cudaStream_t s, const sage_handle *w, int n) {
+}  // extern "C"
+
+int sage::wait_events(cudaStream_t s, const sage_handle *w, int n) {
   for (int i = 0; i < n; ++i) {
     Event *e = event_get(w[i]);
     if (!e) return fail(SAGE_ESTATE, "unknown wait event");
@@ -577,11 +579,35 @@ static int wait_events(cudaStream_t s, const sage_handle *w, int n) {
   return SAGE_OK;
 }
 
+extern "C" {
+
 int sage_stream_wait(sage_handle slot, const sage_handle *evs, int n) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
   cudaSetDevice(G->id);
   return wait_events(s, evs, n);
+}
+
+int sage_sync_wait(sage_handle slot, const sage_handle *evs, int n, sage_handle *begin_ev, sage_handle *end_ev) {
+  Gpu *G; cudaStream_t s;
+  SAGE_TRY(slot_lookup(slot, &G, &s));
+  if (!begin_ev || !end_ev) return fail(SAGE_EINVAL, "sync_wait: null out");
+  cudaSetDevice(G->id);
+  Event *b, *e;
+  SAGE_TRY(event_new(G->id, begin_ev, &b));
+  SAGE_TRY(event_record(b, s));
+  SAGE_TRY(wait_events(s, evs, n));
+  SAGE_TRY(event_new(G->id, end_ev, &e));
+  return event_record(e, s);
+}
+
+int sage_return_after(sage_handle slot, const sage_handle *wait, int n_wait, uint64_t src, void *dst,
+                      uint64_t bytes, sage_handle *begin_ev, sage_handle *end_ev) {
+  Gpu *G; cudaStream_t s;
+  SAGE_TRY(slot_lookup(slot, &G, &s));
+  cudaSetDevice(G->id);
+  SAGE_TRY(wait_events(s, wait, n_wait));
+  return sage_return(slot, src, dst, bytes, begin_ev, end_ev);
 }
 
 int sage_slot_record(sage_handle slot, sage_handle *ev) {
@@ -698,6 +724,18 @@ int sage_event_elapsed(sage_handle a, sage_handle b, double *us) {
   float ms = 0.f;
   SAGE_CUDA(cudaEventElapsedTime(&ms, ea->ev, eb->ev));
   *us = ms * 1000.0;
+  return SAGE_OK;
+}
+
+int sage_host_register(void *ptr, uint64_t bytes) {
+  SAGE_TRY(require_up());
+  if (!ptr || !bytes) return fail(SAGE_EINVAL, "host_register: bad argument");
+  SAGE_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return SAGE_OK;
+}
+int sage_host_unregister(void *ptr) {
+  if (!ptr) return fail(SAGE_EINVAL, "host_unregister: null");
+  SAGE_CUDA(cudaHostUnregister(ptr));
   return SAGE_OK;
 }
 

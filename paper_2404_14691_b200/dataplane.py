@@ -78,6 +78,8 @@ class FunctionData:
     # HBM-resident sources (bench `value` leg: inputs already in HBM, no PCIe)
     db_dev: Optional[D.Segment] = None
     input_dev: Optional[D.Segment] = None
+    # the DB record is pinned (registered host store): cold loads DMA from it
+    db_pinned: bool = False
 
     @property
     def input_bytes(self) -> int:
@@ -166,6 +168,12 @@ class DataPlane:
         self.pinned = _PinnedPool()
         self.data: dict[str, FunctionData] = {}
         self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
+        self._free_slots: dict[int, list] = {}
+
+    def _slot(self, gpu: int) -> D.Slot:
+        """A pooled stream of the pre-created context, kept acquired across invocations."""
+        lst = self._free_slots.get(gpu)
+        return lst.pop() if lst else D.Slot(gpu)
 
     # ---------------------------------------------------------------- data ----
     def register(self, name: str, data: FunctionData) -> None:
@@ -190,6 +198,22 @@ class DataPlane:
                 op.wait()
                 op.release()
                 setattr(fd, attr, seg)
+
+    def pin_host_store(self, names=None) -> None:
+        """Register DB records as pinned host memory (the daemon's host
+        store): cold loads then DMA straight from them, no CPU_LOAD memcpy."""
+        for name in (names if names is not None else list(self.data)):
+            fd = self.data[name]
+            if fd.db_pinned or fd.db.nbytes == 0:
+                continue
+            _lib.check(_lib.lib().sage_host_register(fd.db.ctypes.data, fd.db.nbytes), "sage_host_register")
+            fd.db_pinned = True
+
+    def unpin_host_store(self) -> None:
+        for fd in self.data.values():
+            if fd.db_pinned:
+                _lib.check(_lib.lib().sage_host_unregister(fd.db.ctypes.data), "sage_host_unregister")
+                fd.db_pinned = False
 
     def drop_hbm_sources(self) -> None:
         for fd in self.data.values():
@@ -312,7 +336,7 @@ class DataPlane:
         inv, plan, gpu = run.inv, run.plan, run.gpu
         nodes = plan.nodes
         ends: list[list] = [[] for _ in nodes]
-        run.slot = D.Slot(gpu)
+        run.slot = self._slot(gpu)
         ev = run.events
         in_dst, out_dst = self._input_dst(run, fd)
         grant = getattr(inv, "grant", None)
@@ -379,30 +403,26 @@ class DataPlane:
                     tok.attach(ro_end if ro_end is not None else ends[i][0])
             elif st is Stage.SYNC_WAIT:
                 tok_evs = [t.event for t in wait_tokens if not t.ready and t.event is not None]
-                b = run.slot.record()
-                run.slot.wait(deps + tok_evs)
-                e = run.slot.record()
+                b, e = run.slot.sync_wait(deps + tok_evs)
                 ev += [b, e]
                 ends[i].append(e)
                 run.marks[st] = (b, e)
             elif st is Stage.COMPUTE:
-                run.slot.wait(deps)
                 body = self._body(run, fd, resident, in_dst, out_dst)
-                b, e = run.slot.launch(body)
+                b, e = run.slot.launch_after(deps, body)
                 ev += [b, e]
                 ends[i].append(e)
                 run.marks[st] = (b, e)
             elif st is Stage.RETURN:
-                run.slot.wait(deps)
                 run.out_bytes = fd.out_bytes
                 if self.results_in_hbm:
                     # device-resident measurement: results stay in HBM (D2D)
                     seg = D.pool_alloc(gpu, max(256, fd.out_bytes), _lib.CLASS_WRITABLE, unaccounted=True)
                     run.scratch.append(seg)
-                    b, e = run.slot.ret(out_dst, seg.dptr, fd.out_bytes)
+                    b, e = run.slot.ret_after(deps, out_dst, seg.dptr, fd.out_bytes)
                 else:
                     run.result = self.pinned.get(max(16, fd.out_bytes))
-                    b, e = run.slot.ret(out_dst, run.result.ptr, fd.out_bytes)
+                    b, e = run.slot.ret_after(deps, out_dst, run.result.ptr, fd.out_bytes)
                 ev += [b, e]
                 ends[i].append(e)
                 run.marks[st] = (b, e)
@@ -446,7 +466,7 @@ class DataPlane:
                             device_src_bytes=fd.layout.packed_bytes, wait=wait)
                 run.ro_source = "hbm"
             else:
-                op = D.load(gpu, dst, fd.db, fd.layout, wait=wait)
+                op = D.load(gpu, dst, fd.db, fd.layout, pinned=fd.db_pinned, wait=wait)
                 run.ro_source = "pcie"
         run.loads.append(("ro", op))
         return op.end
@@ -579,7 +599,7 @@ class DataPlane:
             e.release()
         run.events.clear()
         if run.slot is not None:
-            run.slot.release()
+            self._free_slots.setdefault(run.slot.gpu, []).append(run.slot)   # back to the pool
             run.slot = None
         for b in run.pinned:
             self.pinned.put(b)
@@ -595,4 +615,10 @@ class DataPlane:
             run.job = None
 
     def close(self) -> None:
+        self.unpin_host_store()
+        self.drop_hbm_sources()
+        for lst in self._free_slots.values():
+            for s in lst:
+                s.release()
+        self._free_slots.clear()
         self.pinned.close()

@@ -273,6 +273,25 @@ class Slot:
         check(lib().sage_launch(self.h, C.byref(body), C.byref(b), C.byref(e)), "sage_launch")
         return Event(b.value), Event(e.value)
 
+    def sync_wait(self, events: Sequence[Event]) -> tuple[Event, Event]:
+        arr, nw = handles([e.h for e in events])
+        b, e = H(), H()
+        check(lib().sage_sync_wait(self.h, arr, nw, C.byref(b), C.byref(e)), "sage_sync_wait")
+        return Event(b.value), Event(e.value)
+
+    def launch_after(self, wait: Sequence[Event], body: "_lib.BodyDesc") -> tuple[Event, Event]:
+        arr, nw = handles([e.h for e in wait])
+        b, e = H(), H()
+        check(lib().sage_launch_after(self.h, arr, nw, C.byref(body), C.byref(b), C.byref(e)), "sage_launch_after")
+        return Event(b.value), Event(e.value)
+
+    def ret_after(self, wait: Sequence[Event], src: int, dst_ptr: int, nbytes: int) -> tuple[Event, Event]:
+        arr, nw = handles([e.h for e in wait])
+        b, e = H(), H()
+        check(lib().sage_return_after(self.h, arr, nw, src, dst_ptr, nbytes, C.byref(b), C.byref(e)),
+              "sage_return_after")
+        return Event(b.value), Event(e.value)
+
     def ret(self, src: int, host_ptr: int, nbytes: int) -> tuple[Event, Event]:
         b, e = H(), H()
         check(lib().sage_return(self.h, src, host_ptr, nbytes, C.byref(b), C.byref(e)), "sage_return")
