@@ -272,7 +272,7 @@ def cpu_baseline(budget_s: float = 15.0, max_inv: int = 9) -> dict:
         x = fd.input.copy()
         if fd.body == "sgemm":
             m, n, k = fd.args
-            O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(k, n))
+            O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(n, k).T)
         elif fd.body == "stencil":
             nx, ny, nz, bits = fd.args
             beta = float(np.int32(bits).view(np.float32))

@@ -195,6 +195,10 @@ int sage_fanout(int src_gpu, uint64_t src_dptr, int dst_gpu, uint64_t dst_dptr, 
 #define SAGE_BODY_STENCIL  2  /* 7-point 3-D Jacobi, coefficients RO, fp32               */
 #define SAGE_BODY_SPMV     3  /* CSR y = A.x, A = RO, fp32                              */
 #define SAGE_BODY_SPIN     4  /* occupy the SMs for args[0] microseconds                */
+#define SAGE_BODY_SGEMM_F32 5 /* the SGEMM on SIMT fp32 cores (exact-fp32 variant)      */
+/* SGEMM: C[M,N] = A[M,K] . BT[N,K]^T, fp32 in memory, tcgen05 kind::tf32 MMAs
+ * with fp32 accumulation in TMEM; args = {M, N, K}; input = BT (K-contiguous,
+ * Parboil's "matrix2t")                                                       */
 typedef struct {
   int32_t body;
   int32_t pad_;

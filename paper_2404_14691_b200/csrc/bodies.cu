@@ -54,16 +54,18 @@ __global__ void __launch_bounds__(256) sgemm_kernel(const float *__restrict__ A,
   float acc[8][8] = {};
   // loaders: A tile 128x8 (each thread 4 floats), B tile 8x128 (each thread 4 floats)
   const int a_row = tid / 2, a_col = (tid % 2) * 4;
-  const int b_row = tid / 32, b_col = (tid % 32) * 4;
+  // B is given transposed (BT[N,K], K contiguous): loaded like A
+  const int b_row = tid / 2, b_col = (tid % 2) * 4;
   const float *Ap = A + (size_t)(bm + a_row) * K + a_col;
-  const float *Bp = B + (size_t)b_row * N + bn + b_col;
+  const float *Bp = B + (size_t)(bn + b_row) * K + b_col;
   int buf = 0;
   {
     float4 av = *reinterpret_cast<const float4 *>(Ap);
     float4 bv = *reinterpret_cast<const float4 *>(Bp);
     As[0][a_col + 0][a_row] = av.x; As[0][a_col + 1][a_row] = av.y;
     As[0][a_col + 2][a_row] = av.z; As[0][a_col + 3][a_row] = av.w;
-    *reinterpret_cast<float4 *>(&Bs[0][b_row][b_col]) = bv;
+    Bs[0][b_col + 0][b_row] = bv.x; Bs[0][b_col + 1][b_row] = bv.y;
+    Bs[0][b_col + 2][b_row] = bv.z; Bs[0][b_col + 3][b_row] = bv.w;
   }
   __syncthreads();
   for (int k0 = 0; k0 < K; k0 += SG_BK) {
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(const float *__restrict__ A,
     const bool more = k0 + SG_BK < K;
     if (more) {
       av = *reinterpret_cast<const float4 *>(Ap + k0 + SG_BK);
-      bv = *reinterpret_cast<const float4 *>(Bp + (size_t)(k0 + SG_BK) * N);
+      bv = *reinterpret_cast<const float4 *>(Bp + k0 + SG_BK);
     }
 #pragma unroll
     for (int kk = 0; kk < SG_BK; ++kk) {
@@ -91,7 +93,8 @@ __global__ void __launch_bounds__(256) sgemm_kernel(const float *__restrict__ A,
       int nb = buf ^ 1;
       As[nb][a_col + 0][a_row] = av.x; As[nb][a_col + 1][a_row] = av.y;
       As[nb][a_col + 2][a_row] = av.z; As[nb][a_col + 3][a_row] = av.w;
-      *reinterpret_cast<float4 *>(&Bs[nb][b_row][b_col]) = bv;
+      Bs[nb][b_col + 0][b_row] = bv.x; Bs[nb][b_col + 1][b_row] = bv.y;
+      Bs[nb][b_col + 2][b_row] = bv.z; Bs[nb][b_col + 3][b_row] = bv.w;
       __syncthreads();
       buf = nb;
     }
@@ -164,13 +167,17 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
                                           b->input_bytes / 16, (unsigned long long *)b->out);
       break;
     }
-    case SAGE_BODY_SGEMM: {
+    case SAGE_BODY_SGEMM:
+    case SAGE_BODY_SGEMM_F32: {
+      // C[M,N] = A[M,K] . BT[N,K]^T (Parboil passes the second operand transposed)
       int M = (int)b->args[0], N = (int)b->args[1], K = (int)b->args[2];
-      if (M <= 0 || N <= 0 || K <= 0 || M % SG_BM || N % SG_BN || K % SG_BK)
-        return fail(SAGE_EINVAL, "sgemm: M,N multiples of 128 and K of 8 required");
       if ((uint64_t)M * K * 4 > b->ro_bytes || (uint64_t)K * N * 4 > b->input_bytes ||
           (uint64_t)M * N * 4 > b->out_bytes)
         return fail(SAGE_EINVAL, "sgemm: buffers too small");
+      if (b->body == SAGE_BODY_SGEMM)  // tcgen05 kind::tf32 (gemm_tc.cu)
+        return sgemm_tc((const float *)b->ro, (const float *)b->input, (float *)b->out, M, N, K, s);
+      if (M <= 0 || N <= 0 || K <= 0 || M % SG_BM || N % SG_BN || K % SG_BK)
+        return fail(SAGE_EINVAL, "sgemm_f32: M,N multiples of 128 and K of 8 required");
       dim3 grid(N / SG_BN, M / SG_BM);
       sgemm_kernel<<<grid, 256, 0, s>>>((const float *)b->ro, (const float *)b->input, (float *)b->out, M, N, K);
       break;
@@ -220,6 +227,7 @@ int touch_all_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&a, stencil_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, spmv_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, spin_kernel));
+  SAGE_TRY(touch_tc_kernels());
   return SAGE_OK;
 }
 
@@ -253,6 +261,7 @@ extern "C" int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handl
     switch (b->body) {
       case SAGE_BODY_TOUCH: work = b->ro_bytes + b->input_bytes; break;
       case SAGE_BODY_SGEMM:
+      case SAGE_BODY_SGEMM_F32:
         kind = SAGE_KERNEL_SGEMM;
         work = 2ull * (uint64_t)b->args[0] * (uint64_t)b->args[1] * (uint64_t)b->args[2];
         break;

@@ -161,6 +161,9 @@ int wait_events(cudaStream_t s, const sage_handle *w, int n);
 // bodies (bodies.cu)
 int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count);
 int touch_all_kernels();
+// tcgen05 GEMM (gemm_tc.cu)
+int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
+int touch_tc_kernels();
 
 // layouts (land.cu)
 int layouts_destroy_all();

@@ -1,0 +1,259 @@
+// gemm_tc.cu — the sgemm function body on the 5th-gen tensor cores.
+//
+// C[M,N] (fp32, row-major) = A[M,K] . BT[N,K]^T, with A the function's
+// shared read-only weights (landed segment) and BT the invocation input,
+// both fp32 and K-contiguous (Parboil's sgemm also takes the second operand
+// transposed, "matrix2t").  The MMA runs as tcgen05.mma kind::tf32 with the
+// fp32 accumulator in TMEM.
+//
+// Structure (one 128 x BN output tile per CTA, 6 warps):
+//   warp 0      TMA producer: A/BT K-blocks (32 fp32 = one 128-B swizzle
+//               row) into a STAGES-deep smem ring, mbarrier complete_tx
+//   warp 1      TMEM allocator + single-thread MMA issuer: 4 x
+//               tcgen05.mma (K = 8 each) per K-block, tcgen05.commit frees
+//               the smem slot; a final commit signals the epilogue
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
+// Operands use the canonical K-major SWIZZLE_128B layout: 8-row x 128-B
+// core groups 1024 B apart (SBO = 64 x 16 B), start address advanced by
+// 32 B per K = 8 step inside the swizzle atom.
+#include "common.h"
+
+#include <cudaTypedefs.h>
+
+namespace sage {
+
+constexpr int TC_BM = 128;        // UMMA M (rows of A / C per CTA)
+constexpr int TC_BK = 32;         // fp32 elements per K-block = 128 bytes
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 192;
+
+template <int BN>
+struct TcSmem {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
+  static constexpr int B_BYTES = BN * TC_BK * 4;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int TOTAL = TC_STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// canonical K-major SWIZZLE_128B smem descriptor (version 1, SBO = 1024 B)
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);       // start address  [0,14)
+  d |= (uint64_t)1 << 16;                         // LBO (unused for swizzled K-major) [16,30)
+  d |= (uint64_t)(1024 >> 4) << 32;               // SBO: 8-row groups 1024 B apart [32,46)
+  d |= (uint64_t)1 << 46;                         // version = 1 (Blackwell) [46,48)
+  d |= (uint64_t)2 << 61;                         // layout: SWIZZLE_128B [61,64)
+  return d;
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = BN
+template <int BN>
+__device__ __forceinline__ uint32_t tf32_idesc() {
+  return (1u << 4)                 // c_format = F32
+         | (2u << 7)               // a_format = TF32
+         | (2u << 10)              // b_format = TF32
+         | ((uint32_t)(BN >> 3) << 17)
+         | ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
+                      int M, int N, int K) {
+  using S = TcSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *sA = smem;                                  // STAGES x A_BYTES
+  uint8_t *sB = smem + TC_STAGES * S::A_BYTES;         // STAGES x B_BYTES
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * S::STAGE);
+  uint64_t *empty = full + TC_STAGES;
+  uint64_t *tmem_full = empty + TC_STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+  const int kblocks = K / TC_BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < TC_STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(tmem_full, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // TMEM: BN fp32 columns x 128 lanes for the accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer ----
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % TC_STAGES, round = kb / TC_STAGES;
+        mbar_wait(&empty[s], (round & 1) ^ 1);
+        mbar_expect_tx(&full[s], S::STAGE);
+        tma_load_2d(sA + s * S::A_BYTES, &mapA, &full[s], kb * TC_BK, m0);
+        tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], kb * TC_BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer (single thread) ----
+      const uint32_t idesc = tf32_idesc<BN>();
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % TC_STAGES, round = kb / TC_STAGES;
+        mbar_wait(&full[s], round & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = kmajor_sw128_desc(smem_u32(sA + s * S::A_BYTES));
+        const uint64_t db = kmajor_sw128_desc(smem_u32(sB + s * S::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < TC_BK / 8; ++k) {
+          // advance 32 B (8 tf32) along K inside the 128-B swizzle row: +2 in 16-B units
+          const uint64_t a = da + (uint64_t)(2 * k), b = db + (uint64_t)(2 * k);
+          const uint32_t acc = (kb | k) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(a), "l"(b), "r"(idesc), "r"(acc));
+        }
+        // free the smem slot once these MMAs have read it
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[s]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(tmem_full))
+                   : "memory");
+    }
+  } else {
+    // ---- epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) ----
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quad = warp & 3;
+    const int row = m0 + quad * 32 + lane;
+    float *crow = C + (size_t)row * N + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
+        float4 *dst = reinterpret_cast<float4 *>(crow + c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                               __uint_as_float(r[4 * j + 3]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+  }
+}
+
+// ------------------------------------------------------------------ host -----
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int encode_kmajor(CUtensorMap *map, const void *base, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return fail(SAGE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {k * 4};
+  cuuint32_t box[2] = {TC_BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
+  return SAGE_OK;
+}
+
+template <int BN>
+static int launch_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  SAGE_TRY(encode_kmajor(&ma, A, (uint64_t)M, (uint64_t)K, TC_BM));
+  SAGE_TRY(encode_kmajor(&mb, BT, (uint64_t)N, (uint64_t)K, BN));
+  // per context (FixedGSL instances launch from fresh contexts)
+  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TcSmem<BN>::TOTAL));
+  dim3 grid(N / BN, M / TC_BM);
+  sgemm_tf32_kernel<BN><<<grid, TC_THREADS, TcSmem<BN>::TOTAL, s>>>(ma, mb, C, M, N, K);
+  SAGE_CUDA(cudaGetLastError());
+  return SAGE_OK;
+}
+
+// M % 128 == 0, N % 64 == 0, K % 32 == 0, 16-B aligned operands
+int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || K <= 0 || M % TC_BM || N % 64 || K % TC_BK)
+    return fail(SAGE_EINVAL, "sgemm (tcgen05): M % 128, N % 64 and K % 32 must be 0");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(BT) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return fail(SAGE_EINVAL, "sgemm (tcgen05): operands must be 16-byte aligned");
+  // 128 x 64 tiles give 2x the CTAs of 128 x 128 (e.g. 128 for 4096 x 256):
+  // better SM coverage for the skinny per-invocation GEMMs
+  return launch_tc<64>(A, BT, C, M, N, K, s);
+}
+
+int touch_tc_kernels() {
+  cudaFuncAttributes a;
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64>));
+  return SAGE_OK;
+}
+
+}  // namespace sage

@@ -35,16 +35,19 @@ def _writable_mb(*nbytes: int) -> float:
     return _mb(sum((n + 255) // 256 * 256 + 256 for n in nbytes))
 
 
-def sgemm(m: int = 4096, k: int = 4096, n: int = 256, seed: int = 11, name: str = "sgemm"):
+def sgemm(m: int = 4096, k: int = 4096, n: int = 256, seed: int = 11, name: str = "sgemm", body: str = "sgemm"):
+    """C = A . B with the second operand passed transposed (BT [n, k]), as
+    Parboil's sgemm does ("matrix2t"); body "sgemm" runs on tcgen05 (TF32
+    MMAs, fp32 accumulate), "sgemm_f32" on the SIMT fp32 cores."""
     rng = np.random.Generator(np.random.PCG64(seed))
     A = rng.standard_normal((m, k), dtype=np.float32)
-    B = rng.standard_normal((k, n), dtype=np.float32)
+    BT = rng.standard_normal((n, k), dtype=np.float32)
     layout = SegmentLayout.packed([A.nbytes], align=256, names=("A",))
-    data = FunctionData(layout, layout.pack([A]), body="sgemm", args=(m, n, k), input=B.reshape(-1).view(np.uint8),
+    data = FunctionData(layout, layout.pack([A]), body=body, args=(m, n, k), input=BT.reshape(-1).view(np.uint8),
                         out_bytes=m * n * 4)
-    spec = FunctionSpec(name=name, ro_mem_mb=_mb(layout.seg_bytes), writable_mem_mb=_writable_mb(B.nbytes, m * n * 4),
-                        compute_ms=1.0, input_bytes_host_mb=_mb(B.nbytes), input_bytes_pcie_mb=_mb(B.nbytes),
-                        body="sgemm")
+    spec = FunctionSpec(name=name, ro_mem_mb=_mb(layout.seg_bytes), writable_mem_mb=_writable_mb(BT.nbytes, m * n * 4),
+                        compute_ms=1.0, input_bytes_host_mb=_mb(BT.nbytes), input_bytes_pcie_mb=_mb(BT.nbytes),
+                        body=body)
     return spec, data
 
 

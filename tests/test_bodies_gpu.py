@@ -1,0 +1,109 @@
+"""Function bodies called directly through the C-ABI (sage_launch) against
+numpy references: the tcgen05 TF32 GEMM over several shapes, the SIMT fp32
+GEMM at strict fp32 tolerance, stencil and spmv edge shapes."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2404_14691_b200 import _lib
+from paper_2404_14691_b200 import device as D
+
+pytestmark = pytest.mark.gpu
+
+
+def upload(arr):
+    a = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+    seg = D.pool_alloc(0, max(256, a.size + 256), _lib.CLASS_WRITABLE, unaccounted=True)
+    op = D.load(0, seg.dptr, a, None)
+    op.wait()
+    op.release()
+    return seg
+
+
+def run_body(kind, ro, ro_bytes, inp, inp_bytes, out_bytes, args):
+    out = D.pool_alloc(0, max(256, out_bytes), _lib.CLASS_WRITABLE, unaccounted=True)
+    slot = D.Slot(0)
+    b, e = slot.launch(D.body_desc(kind, ro=ro, ro_bytes=ro_bytes, inp=inp, inp_bytes=inp_bytes, out=out.dptr,
+                                   out_bytes=out_bytes, args=args))
+    e.sync()
+    got = D.read_device(0, out.dptr, out_bytes)
+    for ev in (b, e):
+        ev.release()
+    slot.release()
+    out.free()
+    return got
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 64, 32), (256, 128, 256), (512, 256, 4096), (4096, 256, 4096),
+                                   (1024, 192, 96)])
+def test_sgemm_tcgen05_tf32(dp, m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    A = rng.standard_normal((m, k), dtype=np.float32)
+    BT = rng.standard_normal((n, k), dtype=np.float32)
+    sa, sb = upload(A), upload(BT)
+    got = run_body(_lib.BODY_SGEMM, sa.dptr, A.nbytes, sb.dptr, BT.nbytes, m * n * 4, (m, n, k))
+    got = got.view(np.float32).reshape(m, n)
+    want = O.sgemm_ref(A, BT.T)
+    # TF32 MMA inputs (10-bit mantissa), fp32 accumulation: 4-sigma rounding bound
+    np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
+    # and it is really TF32, not garbage that happens to be small
+    assert np.abs(got - want).max() < 0.05 * np.abs(want).max()
+    sa.free()
+    sb.free()
+
+
+def test_sgemm_simt_fp32_strict(dp):
+    m, n, k = 256, 128, 512
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((m, k), dtype=np.float32)
+    BT = rng.standard_normal((n, k), dtype=np.float32)
+    sa, sb = upload(A), upload(BT)
+    got = run_body(5, sa.dptr, A.nbytes, sb.dptr, BT.nbytes, m * n * 4, (m, n, k)).view(np.float32).reshape(m, n)
+    np.testing.assert_allclose(got, O.sgemm_ref(A, BT.T), rtol=1e-3, atol=1e-4)
+    sa.free()
+    sb.free()
+
+
+def test_sgemm_rejects_bad_shapes(dp):
+    sa = upload(np.zeros(4096, np.float32))
+    with pytest.raises(_lib.SageError):
+        run_body(_lib.BODY_SGEMM, sa.dptr, 16384, sa.dptr, 16384, 16384, (100, 64, 32))
+    sa.free()
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 4), (33, 17, 9), (256, 64, 16)])
+def test_stencil(dp, shape):
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx)
+    coef = rng.uniform(0.2, 0.6, (nz, ny, nx)).astype(np.float32)
+    grid = rng.standard_normal((nz, ny, nx), dtype=np.float32)
+    sc, sg = upload(coef), upload(grid)
+    bits = int(np.float32(0.1).view(np.int32))
+    got = run_body(_lib.BODY_STENCIL, sc.dptr, coef.nbytes, sg.dptr, grid.nbytes, grid.nbytes, (nx, ny, nz, bits))
+    np.testing.assert_allclose(got.view(np.float32).reshape(nz, ny, nx), O.stencil_ref(coef, grid, 0.1),
+                               rtol=1e-3, atol=1e-5)
+    sc.free()
+    sg.free()
+
+
+def test_spmv_ragged_rows(dp):
+    rng = np.random.default_rng(9)
+    rows = 5000
+    counts = rng.integers(0, 40, rows)
+    counts[::7] = 0                                     # empty rows
+    rowptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    nnz = int(rowptr[-1])
+    col = rng.integers(0, rows, nnz, dtype=np.int32)
+    val = rng.standard_normal(nnz, dtype=np.float32)
+    x = rng.standard_normal(rows, dtype=np.float32)
+    o_rp, o_col = 0, (rowptr.nbytes + 255) // 256 * 256
+    o_val = o_col + (col.nbytes + 255) // 256 * 256
+    ro = np.zeros(o_val + val.nbytes, np.uint8)
+    ro[o_rp:o_rp + rowptr.nbytes] = rowptr.view(np.uint8)
+    ro[o_col:o_col + col.nbytes] = col.view(np.uint8)
+    ro[o_val:o_val + val.nbytes] = val.view(np.uint8)
+    sr, sx = upload(ro), upload(x)
+    got = run_body(_lib.BODY_SPMV, sr.dptr, ro.size, sx.dptr, x.nbytes, rows * 4, (rows, nnz, o_rp, o_col, o_val))
+    np.testing.assert_allclose(got.view(np.float32), O.spmv_ref(rowptr, col, val, x), rtol=1e-3, atol=1e-4)
+    sr.free()
+    sx.free()

@@ -145,9 +145,10 @@ def test_parboil_bodies_match_oracle(built_lib):
             x = fd.input
             if fd.body == "sgemm":
                 m, n, k = fd.args
-                want = O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(k, n))
+                want = O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(n, k).T)
                 got = inv.result.view(np.float32).reshape(m, n)
-                np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
+                # TF32 MMA inputs (10-bit mantissa): 4-sigma bound of the rounding error
+                np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
             elif fd.body == "stencil":
                 nx, ny, nz, bits = fd.args
                 beta = float(np.int32(bits).view(np.float32))
@@ -192,11 +193,11 @@ def test_full_size_cfg2_burst(built_lib):
             elif fd.body == "sgemm":
                 m, n, k = fd.args
                 A = seg[:m * k * 4].view(np.float32).reshape(m, k)
-                B = fd.input.view(np.float32).reshape(k, n)
+                BT = fd.input.view(np.float32).reshape(n, k)
                 rows = np.arange(0, m, 97)
-                want = (A[rows].astype(np.float64) @ B.astype(np.float64)).astype(np.float32)
+                want = (A[rows].astype(np.float64) @ BT.T.astype(np.float64)).astype(np.float32)
                 got = inv.result.view(np.float32).reshape(m, n)[rows]
-                np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
+                np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
         sim.check_no_leaks()
     finally:
         sim.close()
