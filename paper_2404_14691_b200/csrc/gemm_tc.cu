@@ -97,7 +97,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
-  const int kblocks = K / TC_BK;
+  // split-K: CTA z covers K-blocks [z*kblocks, (z+1)*kblocks) and adds its
+  // partial tile into C (zeroed by the host) with vector reductions
+  const int kblocks = K / TC_BK / gridDim.z;
+  const int kb0 = blockIdx.z * kblocks;
+  const bool split = gridDim.z > 1;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -130,8 +134,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int s = kb % TC_STAGES, round = kb / TC_STAGES;
         mbar_wait(&empty[s], (round & 1) ^ 1);
         mbar_expect_tx(&full[s], S::STAGE);
-        tma_load_2d(sA + s * S::A_BYTES, &mapA, &full[s], kb * TC_BK, m0);
-        tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], kb * TC_BK, n0);
+        tma_load_2d(sA + s * S::A_BYTES, &mapA, &full[s], (kb0 + kb) * TC_BK, m0);
+        tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], (kb0 + kb) * TC_BK, n0);
       }
     }
   } else if (warp == 1) {
@@ -187,10 +191,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (row < M) {
         float4 *dst = reinterpret_cast<float4 *>(crow + c);
+        if (split) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                               __uint_as_float(r[4 * j + 3]));
+          for (int j = 0; j < 8; ++j)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + j), "f"(__uint_as_float(r[4 * j])),
+                         "f"(__uint_as_float(r[4 * j + 1])), "f"(__uint_as_float(r[4 * j + 2])),
+                         "f"(__uint_as_float(r[4 * j + 3]))
+                         : "memory");
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
       }
     }
   }
@@ -233,7 +246,16 @@ static int launch_tc(const float *A, const float *BT, float *C, int M, int N, in
   // per context (FixedGSL instances launch from fresh contexts)
   SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  TcSmem<BN>::TOTAL));
-  dim3 grid(N / BN, M / TC_BM);
+  // split K so the grid covers the SMs: a skinny GEMM (N <= 256) has only
+  // M/128 full-width tiles; splitting K keeps every A element read once
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (N / BN) * (M / TC_BM), kblk = K / TC_BK;
+  int split = 1;
+  while (split * 2 * tiles <= sms && kblk % (split * 2) == 0 && kblk / (split * 2) >= 8) split *= 2;
+  if (split > 1) SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+  dim3 grid(N / BN, M / TC_BM, split);
   sgemm_tf32_kernel<BN><<<grid, TC_THREADS, TcSmem<BN>::TOTAL, s>>>(ma, mb, C, M, N, K);
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
@@ -245,14 +267,18 @@ int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cud
     return fail(SAGE_EINVAL, "sgemm (tcgen05): M % 128, N % 64 and K % 32 must be 0");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(BT) | reinterpret_cast<uintptr_t>(C)) & 15)
     return fail(SAGE_EINVAL, "sgemm (tcgen05): operands must be 16-byte aligned");
-  // 128 x 64 tiles give 2x the CTAs of 128 x 128 (e.g. 128 for 4096 x 256):
-  // better SM coverage for the skinny per-invocation GEMMs
+  // widest N tile that divides N: A (the shared weights, the dominant
+  // operand of these skinny GEMMs) is then streamed through smem once
+  if (N % 256 == 0) return launch_tc<256>(A, BT, C, M, N, K, s);
+  if (N % 128 == 0) return launch_tc<128>(A, BT, C, M, N, K, s);
   return launch_tc<64>(A, BT, C, M, N, K, s);
 }
 
 int touch_tc_kernels() {
   cudaFuncAttributes a;
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256>));
   return SAGE_OK;
 }
 
