@@ -219,6 +219,54 @@ int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handle *begin_ev
 int sage_return(sage_handle slot, uint64_t src_dptr, void *host_dst, uint64_t bytes,
                 sage_handle *begin_ev, sage_handle *end_ev);
 
+/* ---- one invocation in one call (the Parallel-plan fast path) ----------------
+ * Replaces the per-node walk of PlanExecution (functions.py:341-433) for the
+ * Parallel DAG: GPU_CTX bind ‖ (CPU_LOAD -> GPU_LOAD of RO + input) -> SYNC_WAIT
+ * -> COMPUTE -> RETURN, enqueued with device-side dependencies in one call.
+ * Stage times, bytes and checksums come back in one collect call.           */
+#define SAGE_INV_CTX      0x01u   /* bind ctx_dptr (leader / private context)       */
+#define SAGE_INV_RO       0x02u   /* land the read-only segment                     */
+#define SAGE_INV_INPUT    0x04u   /* land the invocation input                      */
+#define SAGE_INV_SYNC     0x08u   /* SYNC_WAIT on `wait` (leader tokens)             */
+#define SAGE_SRC_HOST      0      /* pageable host: staging memcpy (CPU_LOAD) + H2D */
+#define SAGE_SRC_PINNED    1      /* pinned host: H2D only                          */
+#define SAGE_SRC_HBM       2      /* device-resident source: land from HBM          */
+#define SAGE_SRC_PEER      3      /* another GPU's landed segment: land over NVLink */
+typedef struct {
+  int32_t gpu;
+  uint32_t flags;
+  uint64_t ctx_dptr, ctx_bytes;
+  int32_t ro_kind, ro_src_gpu;
+  sage_handle ro_layout;          /* 0 = identity (cache reload / peer copy)        */
+  const void *ro_src;
+  uint64_t ro_src_bytes, ro_dst;
+  sage_handle ro_wait[2];         /* e.g. the Stage-2 cache D2H, a peer's token     */
+  int32_t n_ro_wait;
+  int32_t in_kind;
+  const void *in_src;
+  uint64_t in_bytes, in_dst;
+  sage_handle wait[2];            /* SYNC_WAIT: leader RO / ctx END events          */
+  int32_t n_wait;
+  int32_t pad_;
+  sage_body_desc body;            /* COMPUTE                                        */
+  uint64_t ret_src;               /* RETURN: D2H (or D2D) ret_bytes to ret_dst      */
+  void *ret_dst;
+  uint64_t ret_bytes;
+} sage_invoke_desc;
+typedef struct {
+  int64_t t[16];                  /* begin/end per reference Stage (cf. FixedGSL info) */
+  uint64_t host_bytes, link_bytes;
+  uint64_t ro_checksum, in_checksum;
+  int64_t ro_landed_us;           /* -1 if no RO load                               */
+  int32_t status, pad_;
+} sage_invoke_info;
+/* ro_end / ctx_end (may be null) receive borrowed handles of the RO-landed and
+ * context-bound events, valid until sage_invoke_release                      */
+int sage_invoke(const sage_invoke_desc *d, sage_handle *inv, sage_handle *done_ev, sage_handle *ro_end,
+                sage_handle *ctx_end);
+int sage_invoke_collect(sage_handle inv, sage_invoke_info *out);   /* ENOTREADY until done */
+int sage_invoke_release(sage_handle inv);
+
 /* ---- FixedGSL serial baseline (policies.py:102-126, functions.py:261-267) ---
  * One invocation = fresh cuCtxCreate + cudaMalloc + pageable synchronous
  * per-tensor cudaMemcpy + body + D2H + context teardown, run on a library

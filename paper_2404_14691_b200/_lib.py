@@ -62,6 +62,24 @@ class FixedGSLDesc(C.Structure):
                 ("body", BodyDesc), ("result", C.c_void_p), ("result_bytes", u64)]
 
 
+INV_CTX, INV_RO, INV_INPUT, INV_SYNC = 0x1, 0x2, 0x4, 0x8
+SRC_HOST, SRC_PINNED, SRC_HBM, SRC_PEER = 0, 1, 2, 3
+
+
+class InvokeDesc(C.Structure):
+    _fields_ = [("gpu", C.c_int32), ("flags", C.c_uint32), ("ctx_dptr", u64), ("ctx_bytes", u64),
+                ("ro_kind", C.c_int32), ("ro_src_gpu", C.c_int32), ("ro_layout", H), ("ro_src", C.c_void_p),
+                ("ro_src_bytes", u64), ("ro_dst", u64), ("ro_wait", H * 2), ("n_ro_wait", C.c_int32),
+                ("in_kind", C.c_int32), ("in_src", C.c_void_p), ("in_bytes", u64), ("in_dst", u64),
+                ("wait", H * 2), ("n_wait", C.c_int32), ("pad_", C.c_int32), ("body", BodyDesc),
+                ("ret_src", u64), ("ret_dst", C.c_void_p), ("ret_bytes", u64)]
+
+
+class InvokeInfo(C.Structure):
+    _fields_ = [("t", i64 * 16), ("host_bytes", u64), ("link_bytes", u64), ("ro_checksum", u64),
+                ("in_checksum", u64), ("ro_landed_us", i64), ("status", C.c_int32), ("pad_", C.c_int32)]
+
+
 class FixedGSLInfo(C.Structure):
     _fields_ = [("t", i64 * 16), ("checksum", u64), ("teardown_us", i64), ("status", C.c_int32),
                 ("pad_", C.c_int32)]
@@ -113,6 +131,9 @@ _SIGS = {
     "sage_return_after": (C.c_int, [H, C.POINTER(H), C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),
     "sage_sync_wait": (C.c_int, [H, C.POINTER(H), C.c_int, C.POINTER(H), C.POINTER(H)]),
     "sage_return": (C.c_int, [H, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),
+    "sage_invoke": (C.c_int, [C.POINTER(InvokeDesc), C.POINTER(H), C.POINTER(H), C.POINTER(H), C.POINTER(H)]),
+    "sage_invoke_collect": (C.c_int, [H, C.POINTER(InvokeInfo)]),
+    "sage_invoke_release": (C.c_int, [H]),
     "sage_fixedgsl_submit": (C.c_int, [C.POINTER(FixedGSLDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_fixedgsl_info_get": (C.c_int, [H, C.POINTER(FixedGSLInfo)]),
     "sage_fixedgsl_release": (C.c_int, [H]),

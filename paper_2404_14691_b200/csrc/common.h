@@ -67,7 +67,7 @@ int load_driver();
 int64_t host_now_us();   // CLOCK_MONOTONIC µs since sage_init
 
 // ---------------------------------------------------------------- handles ---
-enum class Kind : uint8_t { Event = 1, Slot, Alloc, Host, Layout, Load, Job };
+enum class Kind : uint8_t { Event = 1, Slot, Alloc, Host, Layout, Load, Job, Inv };
 inline sage_handle make_handle(Kind k, uint64_t id) { return ((uint64_t)k << 56) | id; }
 inline Kind handle_kind(sage_handle h) { return (Kind)(h >> 56); }
 

@@ -158,6 +158,21 @@ class _Run:
     fd: Optional[FunctionData] = None
     ro_source: str = ""
     t_enqueue: int = 0
+    invh: int = 0              # native invocation (sage_invoke fast path)
+    keep: object = None        # host payload kept alive until completion
+
+
+_STAGES = [Stage.CONTAINER, Stage.CPU_CTX, Stage.CPU_LOAD, Stage.GPU_CTX, Stage.GPU_LOAD, Stage.SYNC_WAIT,
+           Stage.COMPUTE, Stage.RETURN]
+
+
+class _Borrowed(D.Event):
+    """An event owned by a native invocation: released with it, never alone."""
+
+    __slots__ = ()
+
+    def release(self) -> None:
+        self.h = 0
 
 
 class DataPlane:
@@ -169,6 +184,7 @@ class DataPlane:
         self.data: dict[str, FunctionData] = {}
         self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
         self._free_slots: dict[int, list] = {}
+        self._fast_cache: dict[int, bool] = {}
 
     def _slot(self, gpu: int) -> D.Slot:
         """A pooled stream of the pre-created context, kept acquired across invocations."""
@@ -275,11 +291,145 @@ class DataPlane:
             self._start_fixedgsl(run, fd)
             return
         try:
-            self._enqueue(run, fd, wait_tokens)
+            if self._fast_ok(plan):
+                self._enqueue_fast(run, fd, wait_tokens)
+            else:
+                self._enqueue(run, fd, wait_tokens)
         except Exception:
             self._release(run)
             raise
         self.sim.engine.watch(run.end, self._on_done, run)
+
+    # ------------------------------------------------- one-call fast path -----
+    def _fast_ok(self, plan: StagePlan) -> bool:
+        """Plans whose DAG is the Parallel shape (also Serial plans without a
+        GPU_CTX node, e.g. DGSF's pre-created contexts): one sage_invoke call."""
+        ok = self._fast_cache.get(id(plan))
+        if ok is None:
+            stages = {n.stage for n in plan.nodes}
+            ok = Stage.CONTAINER not in stages and not (plan.mode is PlanMode.SERIAL and Stage.GPU_CTX in stages)
+            self._fast_cache[id(plan)] = ok
+        return ok
+
+    def _enqueue_fast(self, run: _Run, fd: FunctionData, wait_tokens) -> None:
+        inv, plan, gpu = run.inv, run.plan, run.gpu
+        d = _lib.InvokeDesc()
+        d.gpu = gpu
+        flags = 0
+        stages = [n.stage for n in plan.nodes]
+        if Stage.CPU_CTX in stages:
+            t = self.sim.engine.tick()
+            run.marks[Stage.CPU_CTX] = (t, t)     # host-side, synchronous
+        in_dst, out_dst = self._input_dst(run, fd)
+        grant = getattr(inv, "grant", None)
+        resident = grant.resident if grant is not None else None
+        if Stage.GPU_CTX in stages:
+            flags |= _lib.INV_CTX
+            d.ctx_dptr, d.ctx_bytes = self._ctx_dst(run)
+        gnode = plan.nodes[plan.node_index(Stage.GPU_LOAD)]
+        i_cpu = plan.node_index(Stage.CPU_LOAD)
+        host_ro = i_cpu is not None and plan.nodes[i_cpu].ro
+        if gnode.ro and fd.layout.seg_bytes:
+            flags |= _lib.INV_RO
+            d.ro_dst = self._ro_dst(run)
+            cache = resident.cpu_ro_cache.segment if (resident is not None and resident.cpu_ro_cache is not None) else None
+            peer = self._peer_source(run) if host_ro else None
+            if not host_ro and isinstance(cache, D.PinnedBuffer):
+                # Stage2 / Stage3 rejoin: the pinned cache holds the landed bytes
+                d.ro_kind, d.ro_src, d.ro_src_bytes = _lib.SRC_PINNED, cache.ptr, cache.nbytes
+                if resident.cache_event is not None:
+                    d.ro_wait[0] = resident.cache_event.h
+                    d.n_ro_wait = 1
+                run.ro_source = "cache"
+            elif peer is not None:
+                # PCIe once per box: land the resident peer copy over NVLink
+                d.ro_kind, d.ro_src_gpu = _lib.SRC_PEER, peer.gpu
+                d.ro_src, d.ro_src_bytes = peer.gpu_ro.dptr, fd.layout.seg_bytes
+                if not peer.ro_token.ready and peer.ro_token.event is not None:
+                    d.ro_wait[0] = peer.ro_token.event.h
+                    d.n_ro_wait = 1
+                run.ro_source = "nvlink"
+            elif fd.db_dev is not None:
+                d.ro_kind, d.ro_layout = _lib.SRC_HBM, fd.layout.handle()
+                d.ro_src, d.ro_src_bytes = fd.db_dev.dptr, fd.layout.packed_bytes
+                run.ro_source = "hbm"
+            else:
+                d.ro_kind = _lib.SRC_PINNED if fd.db_pinned else _lib.SRC_HOST
+                d.ro_layout = fd.layout.handle()
+                d.ro_src, d.ro_src_bytes = fd.db.ctypes.data, fd.layout.packed_bytes
+                run.ro_source = "pcie"
+        if fd.input_bytes:
+            flags |= _lib.INV_INPUT
+            d.in_dst, d.in_bytes = in_dst, fd.input_bytes
+            payload = getattr(inv, "payload", None)
+            if payload is None and fd.input_dev is not None:
+                d.in_kind, d.in_src = _lib.SRC_HBM, fd.input_dev.dptr
+            else:
+                p = self._payload(inv, fd)
+                if isinstance(p, D.PinnedBuffer):
+                    d.in_kind, d.in_src = _lib.SRC_PINNED, p.ptr
+                else:
+                    d.in_kind, d.in_src = _lib.SRC_HOST, p.ctypes.data
+                run.keep = p
+        if plan.wait_ro or plan.wait_ctx:
+            flags |= _lib.INV_SYNC
+            evs = [t.event.h for t in wait_tokens if not t.ready and t.event is not None][:2]
+            for k, h in enumerate(evs):
+                d.wait[k] = h
+            d.n_wait = len(evs)
+        d.flags = flags
+        d.body = self._body(run, fd, resident, in_dst, out_dst)
+        run.out_bytes = fd.out_bytes
+        d.ret_src, d.ret_bytes = out_dst, fd.out_bytes
+        if self.results_in_hbm:
+            seg = D.pool_alloc(gpu, max(256, fd.out_bytes), _lib.CLASS_WRITABLE, unaccounted=True)
+            run.scratch.append(seg)
+            d.ret_dst = seg.dptr
+        else:
+            run.result = self.pinned.get(max(16, fd.out_bytes))
+            d.ret_dst = run.result.ptr
+        h, done, ro_end, ctx_end = _lib.H(), _lib.H(), _lib.H(), _lib.H()
+        _lib.check(_lib.lib().sage_invoke(_lib.C.byref(d), _lib.C.byref(h), _lib.C.byref(done), _lib.C.byref(ro_end),
+                                          _lib.C.byref(ctx_end)), "sage_invoke")
+        run.invh = h.value
+        run.end = _Borrowed(done.value)
+        tok = run.hooks.get(Stage.GPU_LOAD)
+        if tok is not None:
+            tok.attach(_Borrowed(ro_end.value or done.value))
+        tok = run.hooks.get(Stage.GPU_CTX)
+        if tok is not None:
+            tok.attach(_Borrowed(ctx_end.value or done.value))
+
+    def _collect_fast(self, run: _Run) -> None:
+        inv = run.inv
+        info = _lib.InvokeInfo()
+        rc = _lib.check(_lib.lib().sage_invoke_collect(run.invh, _lib.C.byref(info)), "sage_invoke_collect")
+        if rc == _lib.SAGE_ENOTREADY:
+            raise SimulationError(f"{inv}: collected before completion")
+        eng = self.sim.engine
+        t = info.t
+        for k, st in enumerate(_STAGES):
+            if st is Stage.CPU_CTX or t[2 * k] < 0:
+                continue
+            if run.plan.node_index(st) is None:
+                continue
+            inv.stages[st] = [eng.to_engine_time(t[2 * k]), eng.to_engine_time(t[2 * k + 1])]
+        for st, (b, e) in run.marks.items():
+            inv.stages[st] = [self._t(b), self._t(e)]
+        inv.measured["host_bytes"] = info.host_bytes
+        if run.ro_source == "nvlink":
+            inv.measured["nvlink_bytes"] = run.fd.layout.seg_bytes
+            inv.measured["pcie_bytes"] = info.link_bytes - run.fd.layout.seg_bytes
+        else:
+            inv.measured["pcie_bytes"] = info.link_bytes
+        if info.ro_landed_us >= 0:
+            self._verify_ro(run, info.ro_checksum)
+            inv.ro_landed_us = eng.to_engine_time(info.ro_landed_us)
+        if run.fd.input_bytes:
+            inv.input_checksum = info.in_checksum
+        inv.ro_source = run.ro_source
+        if isinstance(run.result, D.PinnedBuffer) and run.out_bytes:
+            inv.result = run.result.view()[:run.out_bytes]
 
     def _input_dst(self, run: _Run, fd: FunctionData) -> tuple[int, int]:
         """(input dptr, out dptr) inside the private writable allocation, or an
@@ -524,6 +674,9 @@ class DataPlane:
 
     def _collect(self, run: _Run) -> None:
         inv = run.inv
+        if run.invh:
+            self._collect_fast(run)
+            return
         if run.job is not None:
             info = run.job.info()
             if info is None or info.status != 0:
@@ -592,6 +745,10 @@ class DataPlane:
             r.ro_checksum = checksum
 
     def _release(self, run: _Run) -> None:
+        if run.invh:
+            _lib.check(_lib.lib().sage_invoke_release(run.invh), "sage_invoke_release")
+            run.invh = 0
+            run.keep = None
         for _, op in run.loads:
             op.release()
         run.loads.clear()
