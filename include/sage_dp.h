@@ -49,6 +49,9 @@ typedef uint64_t sage_handle;
  * Replaces Simulation.__init__'s device state (simulation.py:99-159): one
  * pool + staging rings + copy/land/host streams per GPU.                      */
 #define SAGE_INIT_PEER_ACCESS  0x1u   /* map every pool segment for all GPUs (fan-out) */
+#define SAGE_INIT_SHARE_DEVICE 0x2u   /* n_gpus logical planes on fewer physical devices
+                                         (logical g -> device g % visible): exercises the
+                                         multi-GPU control plane + peer lands on one GPU */
 int         sage_init(int n_gpus, uint64_t pool_bytes_per_gpu, uint64_t staging_bytes,
                       uint64_t chunk_bytes, uint32_t flags);
 int         sage_shutdown(void);

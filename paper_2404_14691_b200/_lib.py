@@ -23,6 +23,7 @@ SAGE_ECHECKSUM = -6
 SAGE_ENODEV = -7
 
 SAGE_INIT_PEER_ACCESS = 0x1
+SAGE_INIT_SHARE_DEVICE = 0x2
 CLASS_CONTEXT, CLASS_READ_ONLY, CLASS_WRITABLE, CLASS_INSTANCE_FIXED = 0, 1, 2, 3
 ALLOC_ACCOUNT_ONLY = 0x100
 LOAD_SRC_PINNED, LOAD_SRC_DEVICE, LOAD_SRC_PEER = 0x1, 0x2, 0x4
@@ -195,6 +196,12 @@ _up = False
 
 def is_up() -> bool:
     return _up
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    lib().sage_device_count(C.byref(n))
+    return n.value
 
 
 def shutdown() -> None:

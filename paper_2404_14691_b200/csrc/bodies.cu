@@ -239,7 +239,7 @@ extern "C" int sage_launch_after(sage_handle slot, const sage_handle *wait, int 
                                  sage_handle *begin_ev, sage_handle *end_ev) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_stream(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   SAGE_TRY(wait_events(s, wait, n_wait));
   return sage_launch(slot, b, begin_ev, end_ev);
 }
@@ -248,7 +248,7 @@ extern "C" int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handl
   if (!b || !begin_ev || !end_ev) return fail(SAGE_EINVAL, "launch: null argument");
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_stream(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   Event *eb, *ee;
   SAGE_TRY(event_new(G->id, begin_ev, &eb));
   SAGE_TRY(event_record(eb, s));

@@ -98,7 +98,8 @@ struct ChunkScratch {  // per-load device accumulator + pinned result
 };
 
 struct Gpu {
-  int id = -1;
+  int id = -1;                            // logical GPU (the runtime's index)
+  int dev = -1;                           // physical CUDA device it runs on
   int sm_count = 0;
   CUcontext primary = nullptr;
   cudaStream_t copy = nullptr, land = nullptr, host = nullptr, d2h = nullptr, aux = nullptr;
@@ -139,9 +140,15 @@ struct State {
   uint32_t flags = 0;
   std::vector<std::unique_ptr<Gpu>> gpus;
   int host_threads = 8;
+  int n_devices = 1;                      // physical devices visible at init
 };
 extern State st;
 Gpu *gpu_get(int g);
+// physical device of logical GPU g (identity unless SAGE_INIT_SHARE_DEVICE
+// folds several logical planes onto fewer devices)
+inline int dev_of(int g) {
+  return (g >= 0 && g < (int)st.gpus.size() && st.gpus[g]) ? st.gpus[g]->dev : g;
+}
 int require_up();
 
 // host memcpy fan-out pool (CPU_LOAD)

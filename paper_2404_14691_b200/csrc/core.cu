@@ -103,7 +103,7 @@ int event_new(int gpu, sage_handle *h, Event **out) {
     if (!pool.empty()) { e->ev = pool.back(); pool.pop_back(); }
   }
   if (!e->ev) {
-    cudaSetDevice(gpu);
+    cudaSetDevice(dev_of(gpu));
     cudaError_t err = cudaEventCreate(&e->ev);   // timing enabled: stage times
     if (err != cudaSuccess) { delete e; return cuda_fail(err, "cudaEventCreate"); }
   }
@@ -159,7 +159,7 @@ int event_time_us(Event *e, int64_t *t) {
   std::lock_guard<std::mutex> lk(G->anchor_mu);
   // re-anchor when the anchor is old so float32 ms keeps sub-µs resolution
   if (host_now_us() - G->anchor_us > 2000000) {
-    cudaSetDevice(G->id);
+    cudaSetDevice(G->dev);
     int64_t h0 = host_now_us();
     SAGE_CUDA(cudaEventRecord(G->anchor, G->aux));
     SAGE_CUDA(cudaEventSynchronize(G->anchor));
@@ -377,7 +377,9 @@ int sage_init(int n_gpus, uint64_t pool_bytes_per_gpu, uint64_t staging_bytes, u
   cudaError_t e = cudaGetDeviceCount(&avail);
   if (e != cudaSuccess || avail == 0) return fail(SAGE_ENODEV, "no CUDA device visible");
   if (n_gpus <= 0) n_gpus = avail;
-  if (n_gpus > avail) return fail(SAGE_ENODEV, "requested more GPUs than visible");
+  if (n_gpus > avail && !(flags & SAGE_INIT_SHARE_DEVICE))
+    return fail(SAGE_ENODEV, "requested more GPUs than visible");
+  st.n_devices = avail;
   SAGE_TRY(load_driver());
   g_epoch_ns = mono_ns();
   st.chunk = chunk_bytes;
@@ -401,12 +403,13 @@ int sage_init(int n_gpus, uint64_t pool_bytes_per_gpu, uint64_t staging_bytes, u
   if ((flags & SAGE_INIT_PEER_ACCESS) && n_gpus > 1) {
     for (int a = 0; a < n_gpus; ++a)
       for (int b = 0; b < n_gpus; ++b) {
-        if (a == b) continue;
+        const int da = dev_of(a), db = dev_of(b);
+        if (da == db) continue;   // logical planes sharing a device need no peer access
         int can = 0;
-        cudaDeviceCanAccessPeer(&can, a, b);
+        cudaDeviceCanAccessPeer(&can, da, db);
         if (!can) continue;
-        cudaSetDevice(a);
-        cudaError_t pe = cudaDeviceEnablePeerAccess(b, 0);
+        cudaSetDevice(da);
+        cudaError_t pe = cudaDeviceEnablePeerAccess(db, 0);
         if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) {
           std::string m = std::string("peer access ") + cudaGetErrorString(pe);
           sage_shutdown();
@@ -422,7 +425,7 @@ int sage_init(int n_gpus, uint64_t pool_bytes_per_gpu, uint64_t staging_bytes, u
 int sage_shutdown(void) {
   if (!st.up) return SAGE_OK;
   for (auto &G : st.gpus) {
-    cudaSetDevice(G->id);
+    cudaSetDevice(G->dev);
     cudaDeviceSynchronize();
   }
   pool_threads_stop();
@@ -531,7 +534,7 @@ int sage_ctx_acquire(int gpu, sage_handle *slot) {
     if (!G->slot_free.empty()) { idx = G->slot_free.back(); G->slot_free.pop_back(); }
     else {
       // pool exhausted: grow it (never blocks an admission)
-      cudaSetDevice(gpu);
+      cudaSetDevice(dev_of(gpu));
       cudaStream_t s;
       SAGE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
       G->slots.push_back(s);
@@ -584,7 +587,7 @@ extern "C" {
 int sage_stream_wait(sage_handle slot, const sage_handle *evs, int n) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   return wait_events(s, evs, n);
 }
 
@@ -592,7 +595,7 @@ int sage_sync_wait(sage_handle slot, const sage_handle *evs, int n, sage_handle 
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
   if (!begin_ev || !end_ev) return fail(SAGE_EINVAL, "sync_wait: null out");
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   Event *b, *e;
   SAGE_TRY(event_new(G->id, begin_ev, &b));
   SAGE_TRY(event_record(b, s));
@@ -605,7 +608,7 @@ int sage_return_after(sage_handle slot, const sage_handle *wait, int n_wait, uin
                       uint64_t bytes, sage_handle *begin_ev, sage_handle *end_ev) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   SAGE_TRY(wait_events(s, wait, n_wait));
   return sage_return(slot, src, dst, bytes, begin_ev, end_ev);
 }
@@ -613,7 +616,7 @@ int sage_return_after(sage_handle slot, const sage_handle *wait, int n_wait, uin
 int sage_slot_record(sage_handle slot, sage_handle *ev) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   Event *e;
   SAGE_TRY(event_new(G->id, ev, &e));
   return event_record(e, s);
@@ -623,7 +626,7 @@ int sage_ctx_bind(sage_handle slot, uint64_t ctx_dptr, uint64_t ctx_bytes, const
                   int n_wait, sage_handle *begin_ev, sage_handle *end_ev) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   SAGE_TRY(wait_events(s, wait, n_wait));
   Event *b, *e;
   SAGE_TRY(event_new(G->id, begin_ev, &b));
@@ -639,7 +642,7 @@ int sage_return(sage_handle slot, uint64_t src, void *host_dst, uint64_t bytes, 
                 sage_handle *end_ev) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   Event *b, *e;
   SAGE_TRY(event_new(G->id, begin_ev, &b));
   SAGE_TRY(event_record(b, s));
@@ -657,7 +660,7 @@ int sage_d2h_cache(int gpu, uint64_t src, void *host_dst, uint64_t bytes, const 
   SAGE_TRY(require_up());
   Gpu *G = gpu_get(gpu);
   if (!G || !host_dst || !src) return fail(SAGE_EINVAL, "d2h_cache: bad argument");
-  cudaSetDevice(gpu);
+  cudaSetDevice(dev_of(gpu));
   SAGE_TRY(wait_events(G->d2h, wait, n_wait));
   SAGE_CUDA(cudaMemcpyAsync(host_dst, (const void *)src, bytes, cudaMemcpyDeviceToHost, G->d2h));
   Event *e;
@@ -670,9 +673,9 @@ int sage_fanout(int src_gpu, uint64_t src, int dst_gpu, uint64_t dst, uint64_t b
   SAGE_TRY(require_up());
   Gpu *D = gpu_get(dst_gpu);
   if (!D || !gpu_get(src_gpu)) return fail(SAGE_ENODEV, "fanout: bad gpu");
-  cudaSetDevice(dst_gpu);
+  cudaSetDevice(dev_of(dst_gpu));
   SAGE_TRY(wait_events(D->copy, wait, n_wait));
-  SAGE_CUDA(cudaMemcpyPeerAsync((void *)dst, dst_gpu, (const void *)src, src_gpu, bytes, D->copy));
+  SAGE_CUDA(cudaMemcpyPeerAsync((void *)dst, dev_of(dst_gpu), (const void *)src, dev_of(src_gpu), bytes, D->copy));
   Event *e;
   SAGE_TRY(event_new(dst_gpu, end_ev, &e));
   return event_record(e, D->copy);
@@ -685,7 +688,7 @@ int sage_stats_enable(int on) {
 int sage_stats_reset(void) {
   SAGE_TRY(require_up());
   for (auto &G : st.gpus) {
-    cudaSetDevice(G->id);
+    cudaSetDevice(G->dev);
     stats_clear_gpu(G.get());
   }
   return SAGE_OK;
@@ -694,7 +697,7 @@ int sage_stats_get(int gpu, int kind, uint64_t *launches, double *total_us, uint
   SAGE_TRY(require_up());
   Gpu *G = gpu_get(gpu);
   if (!G || kind < 0 || kind >= SAGE_KERNEL_KINDS) return fail(SAGE_EINVAL, "stats_get: bad argument");
-  cudaSetDevice(gpu);
+  cudaSetDevice(dev_of(gpu));
   stats_resolve(G);
   std::lock_guard<std::mutex> lk(G->stat_mu);
   if (launches) *launches = G->stat_count[kind];
@@ -705,7 +708,7 @@ int sage_stats_get(int gpu, int kind, uint64_t *launches, double *total_us, uint
 int sage_device_sync(int gpu) {
   SAGE_TRY(require_up());
   if (!gpu_get(gpu)) return fail(SAGE_ENODEV, "device_sync: bad gpu");
-  SAGE_CUDA(cudaSetDevice(gpu));
+  SAGE_CUDA(cudaSetDevice(dev_of(gpu)));
   SAGE_CUDA(cudaDeviceSynchronize());
   return SAGE_OK;
 }
@@ -713,7 +716,7 @@ int sage_mark(int gpu, sage_handle *ev) {
   SAGE_TRY(require_up());
   Gpu *G = gpu_get(gpu);
   if (!G || !ev) return fail(SAGE_EINVAL, "mark: bad argument");
-  cudaSetDevice(gpu);
+  cudaSetDevice(dev_of(gpu));
   Event *e;
   SAGE_TRY(event_new(gpu, ev, &e));
   return event_record(e, G->aux);

@@ -59,7 +59,7 @@ static int run_job(Job *J) {
   // GPU_CTX: a fresh context (what a cold container pays)
   stamp(J, GPU_CTX, false);
   CUcontext ctx = nullptr;
-  CUresult r = drv.CtxCreate(&ctx, 0, (CUdevice)d.gpu);
+  CUresult r = drv.CtxCreate(&ctx, 0, (CUdevice)dev_of(d.gpu));
   if (r != CUDA_SUCCESS) { free(priv); return cu_fail(r, "cuCtxCreate"); }
   drv.CtxSetCurrent(ctx);
   int rc = touch_all_kernels();

@@ -108,7 +108,7 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
   if (rc != SAGE_OK) {
     std::string msg = sage_last_error();
     Gpu *G = gpu_get(d->gpu);
-    cudaSetDevice(d->gpu);
+    cudaSetDevice(dev_of(d->gpu));
     cudaDeviceSynchronize();  // error path only: nothing may still reference I
     (void)G;
     inv_free(I);

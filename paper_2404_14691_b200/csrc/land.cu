@@ -145,7 +145,7 @@ static int build_plan(const Layout &L, uint64_t chunk, Plan *P) {
 static int plan_upload(Plan *P, int gpu) {
   if ((int)P->d_items.size() <= gpu) { P->d_items.resize(gpu + 1, nullptr); P->d_prefix.resize(gpu + 1, nullptr); }
   if (P->d_items[gpu]) return SAGE_OK;
-  cudaSetDevice(gpu);
+  cudaSetDevice(dev_of(gpu));
   size_t ni = std::max<size_t>(1, P->items.size()), np = std::max<size_t>(1, P->prefix.size());
   SAGE_CUDA(cudaMalloc((void **)&P->d_items[gpu], ni * sizeof(LandItem)));
   SAGE_CUDA(cudaMalloc((void **)&P->d_prefix[gpu], np * sizeof(uint32_t)));
@@ -157,7 +157,7 @@ static int plan_upload(Plan *P, int gpu) {
 
 static void plan_free(Plan *P) {
   for (size_t g = 0; g < P->d_items.size(); ++g) {
-    if (P->d_items[g]) { cudaSetDevice((int)g); cudaFree(P->d_items[g]); }
+    if (P->d_items[g]) { cudaSetDevice(dev_of((int)g)); cudaFree(P->d_items[g]); }
     if (P->d_prefix[g]) cudaFree(P->d_prefix[g]);
   }
   P->d_items.clear(); P->d_prefix.clear();
@@ -247,7 +247,7 @@ static void CUDART_CB host_copy_fn(void *p) {
 static int raw_event_time(Gpu *G, cudaEvent_t ev, int64_t *t) {
   std::lock_guard<std::mutex> lk(G->anchor_mu);
   if (host_now_us() - G->anchor_us > 2000000) {
-    cudaSetDevice(G->id);
+    cudaSetDevice(G->dev);
     int64_t h0 = host_now_us();
     SAGE_CUDA(cudaEventRecord(G->anchor, G->aux));
     SAGE_CUDA(cudaEventSynchronize(G->anchor));
@@ -394,7 +394,7 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
   if ((d->flags & SAGE_LOAD_SRC_PEER) && !gpu_get(d->src_gpu))
     return fail(SAGE_ENODEV, "segment_load: bad src_gpu");
   if (d->dst & 15) return fail(SAGE_EINVAL, "segment_load: dst must be 16-byte aligned");
-  cudaSetDevice(d->gpu);
+  cudaSetDevice(dev_of(d->gpu));
 
   auto *L = new Load();
   L->gpu = d->gpu;
@@ -541,7 +541,7 @@ int sage_load_info_get(sage_handle h, sage_load_info *out) {
     if (it == g_loads.end()) return fail(SAGE_ESTATE, "unknown load handle");
     L = it->second;
   }
-  cudaSetDevice(L->gpu);
+  cudaSetDevice(dev_of(L->gpu));
   cudaError_t q = cudaEventQuery(L->ev_end);
   if (q == cudaErrorNotReady) return SAGE_ENOTREADY;
   if (q != cudaSuccess) return cuda_fail(q, "load end event");
@@ -570,7 +570,7 @@ int sage_load_release(sage_handle h) {
     L = it->second;
     g_loads.erase(it);
   }
-  cudaSetDevice(L->gpu);
+  cudaSetDevice(dev_of(L->gpu));
   cudaEventSynchronize(L->ev_end);  // host copies reference L until the end
   sage_event_release(L->hb);
   sage_event_release(L->he);
@@ -592,7 +592,7 @@ int sage_host_load(int gpu, void *dst, const void *src, uint64_t bytes, const sa
   SAGE_TRY(require_up());
   Gpu *G = gpu_get(gpu);
   if (!G || !begin_ev || !end_ev || (bytes && (!dst || !src))) return fail(SAGE_EINVAL, "host_load: bad argument");
-  cudaSetDevice(gpu);
+  cudaSetDevice(dev_of(gpu));
   std::lock_guard<std::mutex> lk(G->load_mu);
   SAGE_TRY(wait_list(G->host, wait, n_wait));
   Event *b, *e;
@@ -608,7 +608,7 @@ int sage_segment_checksum(int gpu, uint64_t dptr, uint64_t bytes, uint64_t *chec
   Gpu *G = gpu_get(gpu);
   if (!G || !checksum) return fail(SAGE_EINVAL, "segment_checksum: bad argument");
   if ((dptr & 15) || (bytes & 15)) return fail(SAGE_EINVAL, "segment_checksum: needs 16-byte alignment");
-  cudaSetDevice(gpu);
+  cudaSetDevice(dev_of(gpu));
   std::lock_guard<std::mutex> lk(G->load_mu);
   SAGE_CUDA(cudaMemsetAsync(G->d_verify, 0, 8, G->aux));
   uint64_t nvec = bytes / 16;

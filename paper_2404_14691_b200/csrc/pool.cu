@@ -63,7 +63,7 @@ int pool_create(Gpu *G, uint64_t capacity) {
   CUmemAllocationProp prop{};
   prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  prop.location.id = G->id;
+  prop.location.id = G->dev;
   size_t gran = 0;
   SAGE_CU(drv.MemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
   if (gran) P->vmm_gran = gran;
@@ -118,7 +118,7 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
     CUmemAllocationProp prop{};
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    prop.location.id = G->id;
+    prop.location.id = G->dev;
     CUresult r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
     if (r == CUDA_ERROR_OUT_OF_MEMORY && (P->cached || !P->zombies.empty())) {
       reap(P, true);
@@ -139,7 +139,7 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
   for (int d = 0; d < ngpu; ++d) {
     CUmemAccessDesc a{};
     a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    a.location.id = (ngpu == 1) ? G->id : d;
+    a.location.id = (ngpu == 1) ? G->dev : dev_of(d);
     a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
     acc.push_back(a);
   }
@@ -175,9 +175,10 @@ static void unmap_segment(Pool *P, Alloc *A) {
 int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chunk) {
   Gpu *G = st.gpus[id].get();
   G->id = id;
-  SAGE_CUDA(cudaSetDevice(id));
+  G->dev = id % std::max(1, st.n_devices);
+  SAGE_CUDA(cudaSetDevice(G->dev));
   SAGE_CUDA(cudaFree(0));  // create/retain the primary context up front (the pre-created ctx)
-  SAGE_CUDA(cudaDeviceGetAttribute(&G->sm_count, cudaDevAttrMultiProcessorCount, id));
+  SAGE_CUDA(cudaDeviceGetAttribute(&G->sm_count, cudaDevAttrMultiProcessorCount, G->dev));
   SAGE_CU(drv.CtxGetCurrent(&G->primary));
   int lo = 0, hi = 0;
   SAGE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -233,7 +234,7 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
 }
 
 void gpu_teardown(Gpu *G) {
-  cudaSetDevice(G->id);
+  cudaSetDevice(G->dev);
   stats_clear_gpu(G);
   pool_destroy(G);
   for (auto s : G->slots) cudaStreamDestroy(s);
@@ -304,7 +305,7 @@ int sage_pool_alloc(int gpu, uint64_t bytes, int cls, sage_handle *h, uint64_t *
       return fail(SAGE_ENOMEM, "pool budget exceeded");
     }
     if (!acct) {
-      cudaSetDevice(gpu);
+      cudaSetDevice(dev_of(gpu));
       if (!P->zombies.empty()) reap(P, false);
       int rc = map_segment(G, P, A);
       if (rc != SAGE_OK) { delete A; return rc; }
@@ -341,7 +342,7 @@ int sage_pool_free(sage_handle h) {
       // contract: the caller frees only after the END events of every op that
       // touched the segment completed (the runtime frees on invocation
       // completion / decay), so no device-wide drain is needed here
-      cudaSetDevice(A->gpu);
+      cudaSetDevice(dev_of(A->gpu));
       unmap_segment(P, A);
     }
     P->usage -= A->eff;
@@ -370,7 +371,7 @@ int sage_pool_free_after(sage_handle h, sage_handle evh) {
   P->usage -= A->eff;
   P->by_class[A->cls] -= A->eff;
   if (A->account_only) { delete A; return SAGE_OK; }
-  cudaSetDevice(A->gpu);
+  cudaSetDevice(dev_of(A->gpu));
   cudaEvent_t ev;
   SAGE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   // chain: our private event completes when the caller's event does

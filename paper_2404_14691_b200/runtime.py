@@ -129,10 +129,14 @@ class Simulation:
         self.pre_warmed = cluster.pre_warmed_containers
         self._owns_device = False
         if init_device and not _lib.is_up():
-            _lib.init(n_gpus=cluster.gpus, pool_bytes=int(cluster.gpu_mem_mb * (1 << 20)) + (8 << 30),
-                      staging_bytes=int(cluster.staging_mb * (1 << 20)), chunk_bytes=int(cluster.chunk_mb * (1 << 20)),
-                      flags=_lib.SAGE_INIT_PEER_ACCESS if cluster.gpus > 1 else 0,
-                      host_threads=cluster.host_threads)
+            flags = _lib.SAGE_INIT_PEER_ACCESS if cluster.gpus > 1 else 0
+            if cluster.gpus > _lib.device_count():
+                # more logical GPUs than devices: independent planes share a
+                # device (tests the multi-GPU control plane on one GPU)
+                flags |= _lib.SAGE_INIT_SHARE_DEVICE
+            per_gpu = int(cluster.gpu_mem_mb * (1 << 20)) + (8 << 30)
+            _lib.init(n_gpus=cluster.gpus, pool_bytes=per_gpu, staging_bytes=int(cluster.staging_mb * (1 << 20)),
+                      chunk_bytes=int(cluster.chunk_mb * (1 << 20)), flags=flags, host_threads=cluster.host_threads)
             self._owns_device = True
         self.engine = Engine(log_events=log_events)
         self.dispatcher_rng = rng_stream(seed, DISPATCH_STREAM)
