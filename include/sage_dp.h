@@ -143,6 +143,9 @@ int sage_stream_wait(sage_handle slot, const sage_handle *evs, int n);
 /* SYNC_WAIT as one call: begin event, device-side wait on evs, end event     */
 int sage_sync_wait(sage_handle slot, const sage_handle *evs, int n, sage_handle *begin_ev, sage_handle *end_ev);
 int sage_slot_record(sage_handle slot, sage_handle *ev);
+/* the slot's cudaStream_t (as an integer) so a DNN framework can enqueue a
+ * function body (ResNet-50 via PyTorch) on the invocation's stream          */
+int sage_slot_stream(sage_handle slot, uint64_t *stream);
 
 /* ---- loads ----------------------------------------------------------------
  * Replaces the CPU_LOAD -> GPU_LOAD chain (functions.py:257-268) and

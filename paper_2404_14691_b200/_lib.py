@@ -119,6 +119,7 @@ _SIGS = {
     "sage_ctx_bind": (C.c_int, [H, u64, u64, C.POINTER(H), C.c_int, C.POINTER(H), C.POINTER(H)]),
     "sage_stream_wait": (C.c_int, [H, C.POINTER(H), C.c_int]),
     "sage_slot_record": (C.c_int, [H, C.POINTER(H)]),
+    "sage_slot_stream": (C.c_int, [H, C.POINTER(u64)]),
     "sage_segment_load": (C.c_int, [C.POINTER(LoadDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_load_info_get": (C.c_int, [H, C.POINTER(LoadInfo)]),
     "sage_load_release": (C.c_int, [H]),

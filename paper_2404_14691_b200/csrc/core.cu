@@ -613,6 +613,14 @@ int sage_return_after(sage_handle slot, const sage_handle *wait, int n_wait, uin
   return sage_return(slot, src, dst, bytes, begin_ev, end_ev);
 }
 
+int sage_slot_stream(sage_handle slot, uint64_t *stream) {
+  Gpu *G; cudaStream_t s;
+  SAGE_TRY(slot_lookup(slot, &G, &s));
+  if (!stream) return fail(SAGE_EINVAL, "slot_stream: null out");
+  *stream = reinterpret_cast<uint64_t>(s);
+  return SAGE_OK;
+}
+
 int sage_slot_record(sage_handle slot, sage_handle *ev) {
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));

@@ -291,7 +291,7 @@ class DataPlane:
             self._start_fixedgsl(run, fd)
             return
         try:
-            if self._fast_ok(plan):
+            if fd.body != "resnet50" and self._fast_ok(plan):
                 self._enqueue_fast(run, fd, wait_tokens)
             else:
                 self._enqueue(run, fd, wait_tokens)
@@ -558,8 +558,18 @@ class DataPlane:
                 ends[i].append(e)
                 run.marks[st] = (b, e)
             elif st is Stage.COMPUTE:
-                body = self._body(run, fd, resident, in_dst, out_dst)
-                b, e = run.slot.launch_after(deps, body)
+                if fd.body == "resnet50":
+                    # DNN body: PyTorch on the invocation's stream, weights read in
+                    # place from the landed (shared) segment
+                    from . import dnn
+                    run.slot.wait(deps)
+                    b = run.slot.record()
+                    dnn.run_resnet50(fd, self._ro_dst(run), in_dst, out_dst, run.slot.stream(),
+                                     gpu % max(1, _lib.device_count()))
+                    e = run.slot.record()
+                else:
+                    body = self._body(run, fd, resident, in_dst, out_dst)
+                    b, e = run.slot.launch_after(deps, body)
                 ev += [b, e]
                 ends[i].append(e)
                 run.marks[st] = (b, e)

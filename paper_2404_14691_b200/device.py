@@ -273,6 +273,11 @@ class Slot:
         check(lib().sage_launch(self.h, C.byref(body), C.byref(b), C.byref(e)), "sage_launch")
         return Event(b.value), Event(e.value)
 
+    def stream(self) -> int:
+        s = C.c_uint64()
+        check(lib().sage_slot_stream(self.h, C.byref(s)), "sage_slot_stream")
+        return s.value
+
     def sync_wait(self, events: Sequence[Event]) -> tuple[Event, Event]:
         arr, nw = handles([e.h for e in events])
         b, e = H(), H()

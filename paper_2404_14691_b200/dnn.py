@@ -1,0 +1,113 @@
+"""ResNet-50 inference as a SAGE function (BASELINE cfg 3).
+
+The reference's resnet50 is a calibrated record (97.7 MB RO, 11.9 MB
+writable, 24.3 ms compute; functions.py:154, ref PAPER.md Table 3).  Here it
+is a real function: random-init torchvision ResNet-50 weights (params +
+BN buffers, 102,440,608 B fp32) are the packed DB record, landed as one RO
+segment by the `land` kernel; COMPUTE runs the network with PyTorch on the
+invocation's pooled stream over ZERO-COPY views of that segment
+(`torch.func.functional_call` with tensors built from
+`__cuda_array_interface__`), so concurrent invocations share one copy of the
+weights -- the RO sharing SAGE is about.  PyTorch (cuDNN convolutions) is used
+only for the DNN body, as the north star allows; activations come from
+PyTorch's caching allocator, outside the segment pool.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .dataplane import FunctionData
+from .functions import FunctionSpec
+from .layout import SegmentLayout
+
+MIB = 1 << 20
+
+
+def _mb(nbytes: int) -> float:
+    return -(-nbytes * 1_000_000 // MIB) / 1_000_000
+
+
+def _state(seed: int):
+    import torch
+    import torchvision
+    torch.manual_seed(seed)
+    model = torchvision.models.resnet50(weights=None).eval()
+    sd = model.state_dict()
+    names = list(sd.keys())
+    arrays = [sd[n].detach().cpu().contiguous().numpy() for n in names]
+    return names, arrays
+
+
+def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real"):
+    """(FunctionSpec, FunctionData) for ResNet-50 inference on a batch of
+    224x224 fp32 images; the DB record packs the state dict back to back."""
+    names, arrays = _state(seed)
+    sizes = [a.nbytes for a in arrays]
+    layout = SegmentLayout.packed(sizes, align=256, names=tuple(names))
+    db = layout.pack(arrays)
+    rng = np.random.Generator(np.random.PCG64(seed + 1))
+    x = rng.standard_normal((batch, 3, 224, 224), dtype=np.float32)
+    out_bytes = batch * 1000 * 4
+    data = FunctionData(layout, db, body="resnet50", args=(batch,), input=x.reshape(-1).view(np.uint8),
+                        out_bytes=out_bytes)
+    data.meta = {"shapes": [a.shape for a in arrays], "dtypes": [a.dtype.str for a in arrays], "names": names}
+    spec = FunctionSpec(name=name, ro_mem_mb=_mb(layout.seg_bytes),
+                        writable_mem_mb=_mb(x.nbytes + out_bytes + 4096), compute_ms=24.3,
+                        input_bytes_host_mb=_mb(x.nbytes), input_bytes_pcie_mb=_mb(x.nbytes), body="resnet50")
+    return spec, data
+
+
+class _CudaBuf:
+    """Minimal __cuda_array_interface__ over a raw device range (zero copy)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+_MODELS: dict = {}
+
+
+def _skeleton():
+    import torch
+    import torchvision
+    m = _MODELS.get("resnet50")
+    if m is None:
+        with torch.device("meta"):
+            m = torchvision.models.resnet50(weights=None).eval()
+        _MODELS["resnet50"] = m
+    return m
+
+
+def view(ptr: int, nbytes: int, device):
+    import torch
+    return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
+
+
+def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, stream_ptr: int, device_index: int) -> None:
+    """Enqueue one ResNet-50 forward on the invocation's stream, reading the
+    weights in place from the landed segment and writing logits to out."""
+    import torch
+    dev = torch.device("cuda", device_index)
+    meta = fd.meta
+    lay = fd.layout
+    key = (id(fd), ro_ptr, device_index)
+    params = _PARAMS.get(key)
+    if params is None:
+        seg = view(ro_ptr, lay.seg_bytes, dev)
+        params = {}
+        for n, off, ln, shp, dt in zip(meta["names"], lay.dst_off, lay.length, meta["shapes"], meta["dtypes"]):
+            t = seg[off:off + ln].view(torch.int64 if dt.endswith("i8") else torch.float32)
+            params[n] = t.view(shp) if len(shp) else t.view(())
+        _PARAMS.clear()            # landed segments move between invocations: keep one
+        _PARAMS[key] = params
+    batch = fd.args[0]
+    x = view(in_ptr, fd.input_bytes, dev).view(torch.float32).view(batch, 3, 224, 224)
+    out = view(out_ptr, fd.out_bytes, dev).view(torch.float32).view(batch, 1000)
+    model = _skeleton()
+    with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=dev)), torch.inference_mode():
+        y = torch.func.functional_call(model, params, (x,))
+        out.copy_(y)
+
+
+_PARAMS: dict = {}

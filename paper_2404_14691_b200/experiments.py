@@ -1,0 +1,206 @@
+"""BASELINE.json configs on the real plane (reference drivers:
+pkg/src/gslsim/experiments.py:37-193 -- run / compare on one pre-generated
+stream / peak).  Each runner returns a JSON-able dict.
+
+  cfg1  16 concurrent cold starts of one 100 MiB function: SAGE vs FixedGSL
+  cfg2  the Parboil burst (bench.py)
+  cfg3  ResNet-50 inference function under Poisson arrivals; PCIe-once +
+        peer-land fan-out across G (logical on a 1-GPU pool) GPUs
+  cfg4  ten functions with RO log-spaced 10 MiB .. 2 GiB, Poisson mix under
+        the 180 GB budget: resident density and time-averaged memory
+  cfg5  N = 1..512 simultaneous cold starts of a 100 MiB function: SAGE vs
+        the host-only loading path (every invocation pulls its own copy)
+
+    python -m paper_2404_14691_b200.experiments cfg1 cfg3 cfg4 cfg5 --out profiles/
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import time
+from pathlib import Path
+
+from .functions import FunctionSpec, Stage
+from .parboil import synthetic_function
+from .policies import policy_preset
+from .runtime import ClusterSpec, Simulation, percentile, summarize_setup
+from .workload import OpenLoopSource, PoissonOpenSpec, generate_arrivals
+
+
+def _evict_all(sim) -> None:
+    if sim.sharing is not None:
+        for r in list(sim.sharing.residents.values()):
+            sim.sharing._evict(r)
+
+
+def _round(d):
+    return {k: (round(v, 3) if isinstance(v, float) else v) for k, v in d.items()}
+
+
+def cfg1(n: int = 16, reps: int = 5) -> dict:
+    spec, data = synthetic_function("fn100", 100, 10, 1, tensors=64)
+    out = {}
+    for pol, r in (("SAGE", reps + 1), ("FixedGSL", 1)):
+        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), {spec.name: spec}, seed=1,
+                         function_data={spec.name: data})
+        try:
+            sim.prepare()
+            samples = []
+            for rep in range(r):
+                _evict_all(sim)
+                invs = sim.submit_many([spec.name] * n)
+                sim.drain()
+                if rep >= (1 if r > 1 else 0):     # first SAGE burst warms the process
+                    samples += invs
+            s = summarize_setup(samples)
+            s["bursts"] = r - (1 if r > 1 else 0)
+            if pol == "FixedGSL":
+                ctx = [i.stages[Stage.GPU_CTX][1] - i.stages[Stage.GPU_CTX][0] for i in samples]
+                s["fresh_context_ms_p50"] = percentile(ctx, 50) / 1e3
+            out[pol] = _round(s)
+        finally:
+            sim.close()
+    out["p50_setup_ratio"] = round(out["FixedGSL"]["setup_p50_ms"] / out["SAGE"]["setup_p50_ms"], 1)
+    out["workload"] = f"{n} concurrent cold starts, 100 MiB RO (64 ragged tensors), 10 MiB writable, 1 MiB input"
+    return out
+
+
+def cfg3(rate: float = 300.0, duration_s: float = 4.0, gpus_list=(1, 2, 4), seed: int = 1) -> dict:
+    from .dnn import resnet50
+    spec, data = resnet50()
+    arrivals = generate_arrivals(PoissonOpenSpec(rate, duration_s, {spec.name: 1.0}), seed)
+    out = {"workload": f"ResNet-50 (random init, {data.layout.seg_bytes} B fp32 weights, batch 8) "
+                       f"Poisson {rate:g}/s for {duration_s:g} s ({len(arrivals)} arrivals)"}
+    for g in gpus_list:
+        sim = Simulation(ClusterSpec(gpus=g), policy_preset("SAGE"), {spec.name: spec}, seed=seed,
+                         function_data={spec.name: data}, copy_results=False)
+        try:
+            sim.prepare()
+            src = OpenLoopSource(arrivals)
+            t0 = time.perf_counter()
+            src.attach(sim)
+            sim.source = src
+            sim.drain()
+            wall = time.perf_counter() - t0
+            invs = [i for i in sim.invocations if i.outcome == "completed"]
+            srcs = {}
+            for i in invs:
+                if i.ro_source:
+                    srcs[i.ro_source] = srcs.get(i.ro_source, 0) + 1
+            s = summarize_setup(invs)
+            s.update(gpus=g, throughput_per_s=len(invs) / wall, wall_s=wall, ro_loads=srcs,
+                     pcie_ro_bytes=sum(i.measured["pcie_bytes"] for i in invs),
+                     nvlink_bytes=sum(i.measured.get("nvlink_bytes", 0) for i in invs),
+                     note="logical GPUs share the one physical B200 of this pool" if g > 1 else "")
+            out[f"G{g}"] = _round(s)
+            sim.check_no_leaks()
+        finally:
+            sim.close()
+    return out
+
+
+def cfg4(rate: float = 20.0, duration_s: float = 10.0, seed: int = 1, include_fixedgsl: bool = True) -> dict:
+    ro = [10 * (2048 / 10) ** (k / 9) for k in range(10)]          # log-spaced 10 .. 2048 MiB
+    table, data = {}, {}
+    for k, r in enumerate(ro):
+        spec, fd = synthetic_function(f"f{k}", round(r, 1), round(0.05 * r, 1), round(0.01 * r, 2), tensors=32)
+        table[spec.name] = spec
+        data[spec.name] = fd
+    arrivals = generate_arrivals(PoissonOpenSpec(rate, duration_s, {n: 1.0 for n in table}), seed)
+    out = {"workload": f"10 functions, RO {', '.join(f'{r:.1f}' for r in ro)} MiB; Poisson {rate:g}/s for "
+                       f"{duration_s:g} s ({len(arrivals)} arrivals); 180 GB budget"}
+    for pol in (("SAGE", "FixedGSL") if include_fixedgsl else ("SAGE",)):
+        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), table, seed=seed, function_data=data,
+                         copy_results=False)
+        try:
+            sim.prepare()
+            samples = []
+            peak_res = 0
+            peak_mem = 0
+            area = 0.0
+            last = [time.perf_counter(), 0]
+
+            def tick(*_):
+                nonlocal peak_res, peak_mem, area
+                now = time.perf_counter()
+                used = sim.gpu_ledgers[0].usage
+                area += last[1] * (now - last[0])
+                last[0], last[1] = now, used
+                peak_mem = max(peak_mem, used)
+                if sim.sharing is not None:
+                    peak_res = max(peak_res, sum(1 for r in sim.sharing.residents.values() if r.gpu_ro or r.gpu_ctx))
+                samples.append(used)
+
+            sim.completion_listeners.append(lambda inv, now: tick())
+            src = OpenLoopSource(arrivals)
+            t0 = time.perf_counter()
+            last[0] = t0
+            src.attach(sim)
+            sim.source = src
+            sim.drain()
+            tick()
+            wall = time.perf_counter() - t0
+            invs = [i for i in sim.invocations if i.outcome == "completed"]
+            s = summarize_setup(invs)
+            s.update(throughput_per_s=len(invs) / wall, wall_s=wall, peak_resident_functions=peak_res,
+                     peak_gpu_mem_gb=peak_mem / 1e9, avg_gpu_mem_gb=area / max(1e-9, wall) / 1e9)
+            out[pol] = _round(s)
+        finally:
+            sim.close()
+    return out
+
+
+def cfg5(ns=(1, 2, 4, 8, 16, 32, 64, 128, 256, 512), reps: int = 3) -> dict:
+    spec, data = synthetic_function("fn100", 100, 10, 1, tensors=64)
+    out = {"workload": "N simultaneous cold starts of one 100 MiB function on 1 GPU: SAGE (PCIe once, shared) vs "
+                       "host-only loading (SAGE-NR: every invocation lands its own copy)"}
+    for pol in ("SAGE", "SAGE_NR"):
+        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), {spec.name: spec}, seed=1,
+                         function_data={spec.name: data}, copy_results=False)
+        try:
+            sim.prepare()
+            _evict_all(sim)
+            sim.submit_many([spec.name] * 4)         # warm the process
+            sim.drain()
+            rows = {}
+            for n in ns:
+                setups, walls, pcie = [], [], 0
+                for _ in range(reps):
+                    _evict_all(sim)
+                    t0 = time.perf_counter()
+                    invs = sim.submit_many([spec.name] * n)
+                    sim.drain()
+                    walls.append(time.perf_counter() - t0)
+                    setups += [i.setup_us for i in invs]
+                    pcie = sum(i.measured["pcie_bytes"] for i in invs)
+                rows[str(n)] = {"setup_p50_ms": round(percentile(setups, 50) / 1e3, 3),
+                                "setup_p99_ms": round(percentile(setups, 99) / 1e3, 3),
+                                "burst_ms": round(1e3 * min(walls), 3), "pcie_bytes": pcie}
+            out[pol] = rows
+        finally:
+            sim.close()
+    return out
+
+
+RUNNERS = {"cfg1": cfg1, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+", choices=sorted(RUNNERS))
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args(argv)
+    for c in args.configs:
+        t0 = time.perf_counter()
+        res = RUNNERS[c]()
+        res["elapsed_s"] = round(time.perf_counter() - t0, 1)
+        line = json.dumps({c: res})
+        print(line, flush=True)
+        if args.out:
+            Path(args.out).mkdir(parents=True, exist_ok=True)
+            (Path(args.out) / f"{c}.json").write_text(json.dumps(res, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    main()

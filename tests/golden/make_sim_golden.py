@@ -108,6 +108,17 @@ def main():
                             "invocations": record(res.sim),
                             "ro_loads": {f"{k[0]}@{k[1]}": v for k, v in res.sim.sharing.ro_loads_performed.items()}}
 
+    # the reference's open-loop Poisson streams (workload.py:75-113)
+    from gslsim.workload import PoissonOpenSpec, generate_arrivals
+    arr = {}
+    for seed, rate, dur, mix in ((1, 50.0, 2.0, {"resnet50": 1.0}),
+                                 (7, 400.0, 1.0, {"a": 1.0, "b": 2.0, "c": 0.5}),
+                                 (3, 20.0, 30.0, {f"f{i}": 1.0 for i in range(10)})):
+        recs = generate_arrivals(PoissonOpenSpec(rate_per_s=rate, duration_s=dur, mix=mix), seed)
+        arr[f"seed{seed}_rate{rate:g}"] = {"seed": seed, "rate_per_s": rate, "duration_s": dur, "mix": mix,
+                                           "arrivals": [[r.timestamp_us, r.function] for r in recs]}
+    S["poisson_arrivals"] = arr
+
     path = Path(__file__).with_name("sim_parity.json")
     path.write_text(json.dumps(fixture, indent=1, sort_keys=True) + "\n")
     print(f"wrote {path} ({len(S)} scenarios)")

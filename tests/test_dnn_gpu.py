@@ -1,0 +1,37 @@
+"""ResNet-50 as a SAGE function: weights landed by `land` into one shared RO
+segment, COMPUTE by PyTorch on the invocation stream over zero-copy views.
+Outputs must equal the same network run directly with its own parameters."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2404_14691_b200.policies import policy_preset
+from paper_2404_14691_b200.runtime import ClusterSpec, Simulation
+
+pytestmark = pytest.mark.gpu
+
+
+def test_resnet50_function_matches_torch(built):
+    import torch
+    import torchvision
+    from paper_2404_14691_b200 import dnn
+    spec, data = dnn.resnet50(batch=8, seed=0)
+    sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), {spec.name: spec}, seed=1,
+                     function_data={spec.name: data})
+    try:
+        invs = sim.submit_many([spec.name] * 6)
+        sim.drain()
+        assert [i.warmth.label() for i in invs] == ["Cold"] + ["Stage1Hot"] * 5
+        lay = data.layout
+        _, want_cs = O.land_c(data.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+        assert invs[0].ro_checksum == want_cs
+        torch.manual_seed(0)
+        ref = torchvision.models.resnet50(weights=None).eval().cuda()
+        x = torch.from_numpy(data.input.view(np.float32).reshape(8, 3, 224, 224).copy()).cuda()
+        with torch.inference_mode():
+            want = ref(x).float().cpu().numpy()
+        for inv in invs:
+            got = inv.result.view(np.float32).reshape(8, 1000)
+            np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
+    finally:
+        sim.close()
