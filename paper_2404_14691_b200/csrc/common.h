@@ -116,7 +116,9 @@ struct Gpu {
   uint64_t chunk_seq = 0;                 // global chunk sequence (ring position)
   std::mutex load_mu;                     // serialises load enqueue (ring order)
   ChunkScratch scratch;
-  // clock anchor
+  // clock anchor (see clock_anchor_refresh)
+  cudaStream_t clock = nullptr;           // dedicated top-priority stream, never loaded
+  cudaEvent_t anchor_trial = nullptr;
   cudaEvent_t anchor = nullptr;
   int64_t anchor_us = 0;
   std::mutex anchor_mu;
@@ -150,6 +152,9 @@ inline int dev_of(int g) {
   return (g >= 0 && g < (int)st.gpus.size() && st.gpus[g]) ? st.gpus[g]->dev : g;
 }
 int require_up();
+
+// device->host clock anchor (core.cu); call with G->anchor_mu held
+void clock_anchor_refresh(Gpu *G, bool force = false);
 
 // host memcpy fan-out pool (CPU_LOAD)
 void parallel_memcpy(void *dst, const void *src, size_t bytes);

@@ -246,13 +246,7 @@ static void CUDART_CB host_copy_fn(void *p) {
 
 static int raw_event_time(Gpu *G, cudaEvent_t ev, int64_t *t) {
   std::lock_guard<std::mutex> lk(G->anchor_mu);
-  if (host_now_us() - G->anchor_us > 2000000) {
-    cudaSetDevice(G->dev);
-    int64_t h0 = host_now_us();
-    SAGE_CUDA(cudaEventRecord(G->anchor, G->aux));
-    SAGE_CUDA(cudaEventSynchronize(G->anchor));
-    G->anchor_us = (h0 + host_now_us()) / 2;
-  }
+  clock_anchor_refresh(G);
   float ms = 0.f;
   SAGE_CUDA(cudaEventElapsedTime(&ms, G->anchor, ev));
   *t = G->anchor_us + (int64_t)llround((double)ms * 1000.0);

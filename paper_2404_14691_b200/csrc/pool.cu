@@ -219,12 +219,14 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
                           cudaHostAllocPortable | cudaHostAllocMapped));
   SAGE_CUDA(cudaHostGetDevicePointer((void **)&G->scratch.d_res, G->scratch.h_res, 0));
   SAGE_CUDA(cudaMalloc((void **)&G->d_verify, 64));
-  // clock anchor
+  // clock anchor on its own top-priority stream (nothing else is queued there)
+  SAGE_CUDA(cudaStreamCreateWithPriority(&G->clock, cudaStreamNonBlocking, hi));
   SAGE_CUDA(cudaEventCreate(&G->anchor));
-  int64_t h0 = host_now_us();
-  SAGE_CUDA(cudaEventRecord(G->anchor, G->aux));
-  SAGE_CUDA(cudaEventSynchronize(G->anchor));
-  G->anchor_us = (h0 + host_now_us()) / 2;
+  SAGE_CUDA(cudaEventCreate(&G->anchor_trial));
+  {
+    std::lock_guard<std::mutex> lk(G->anchor_mu);
+    clock_anchor_refresh(G, true);
+  }
   if (pool_bytes == 0) {
     size_t fr = 0, tot = 0;
     SAGE_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -245,6 +247,8 @@ void gpu_teardown(Gpu *G) {
   for (auto e : G->ev_h2d) cudaEventDestroy(e);
   for (auto e : G->ev_land) cudaEventDestroy(e);
   if (G->anchor) cudaEventDestroy(G->anchor);
+  if (G->anchor_trial) cudaEventDestroy(G->anchor_trial);
+  if (G->clock) cudaStreamDestroy(G->clock);
   if (G->pin) cudaFreeHost(G->pin);
   if (G->dstage) cudaFree(G->dstage);
   if (G->scratch.d_acc) cudaFree(G->scratch.d_acc);
