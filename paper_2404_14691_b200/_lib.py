@@ -10,11 +10,6 @@ import os
 import threading
 from pathlib import Path
 
-# The plane runs ~8 long-lived streams plus a slot pool; give the device more
-# hardware queues than the default 8 before any CUDA context exists (a user
-# setting wins; sage_init repeats this for pure C callers).
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libsagedp.so"
 

@@ -384,10 +384,6 @@ int sage_set_host_threads(int n) {
 int sage_init(int n_gpus, uint64_t pool_bytes_per_gpu, uint64_t staging_bytes, uint64_t chunk_bytes,
               uint32_t flags) {
   if (st.up) return fail(SAGE_ESTATE, "sage_init called twice (sage_shutdown first)");
-  // more hardware work queues than the default 8, so the ring / slot / clock
-  // streams do not alias onto one queue (only effective before the process
-  // creates its primary context; a user setting wins)
-  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
   if (chunk_bytes == 0) chunk_bytes = 8ull << 20;
   if (chunk_bytes % 256 || chunk_bytes < (64u << 10))
     return fail(SAGE_EINVAL, "chunk_bytes must be a multiple of 256 and >= 64 KiB");
