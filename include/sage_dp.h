@@ -234,6 +234,8 @@ int sage_return(sage_handle slot, uint64_t src_dptr, void *host_dst, uint64_t by
 #define SAGE_INV_RO       0x02u   /* land the read-only segment                     */
 #define SAGE_INV_INPUT    0x04u   /* land the invocation input                      */
 #define SAGE_INV_SYNC     0x08u   /* SYNC_WAIT on `wait` (leader tokens)             */
+#define SAGE_INV_RET_HOST 0x10u   /* ret_dst is host memory: the D2H leaves the slot
+                                     stream for a return stream (PCIe overlap)      */
 #define SAGE_SRC_HOST      0      /* pageable host: staging memcpy (CPU_LOAD) + H2D */
 #define SAGE_SRC_PINNED    1      /* pinned host: H2D only                          */
 #define SAGE_SRC_HBM       2      /* device-resident source: land from HBM          */

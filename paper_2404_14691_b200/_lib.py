@@ -63,7 +63,7 @@ class FixedGSLDesc(C.Structure):
                 ("body", BodyDesc), ("result", C.c_void_p), ("result_bytes", u64)]
 
 
-INV_CTX, INV_RO, INV_INPUT, INV_SYNC = 0x1, 0x2, 0x4, 0x8
+INV_CTX, INV_RO, INV_INPUT, INV_SYNC, INV_RET_HOST = 0x1, 0x2, 0x4, 0x8, 0x10
 SRC_HOST, SRC_PINNED, SRC_HBM, SRC_PEER = 0, 1, 2, 3
 
 

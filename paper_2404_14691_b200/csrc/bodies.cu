@@ -244,6 +244,33 @@ extern "C" int sage_launch_after(sage_handle slot, const sage_handle *wait, int 
   return sage_launch(slot, b, begin_ev, end_ev);
 }
 
+int sage::launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b) {
+  cudaEvent_t sb = stat_begin(G, s);
+  SAGE_TRY(launch_body(b, s, G->sm_count));
+  // algorithmic work per launch (bytes; FLOPs for sgemm)
+  uint64_t work = 0;
+  int kind = SAGE_KERNEL_TOUCH;
+  switch (b->body) {
+    case SAGE_BODY_TOUCH: work = b->ro_bytes + b->input_bytes; break;
+    case SAGE_BODY_SGEMM:
+    case SAGE_BODY_SGEMM_F32:
+      kind = SAGE_KERNEL_SGEMM;
+      work = 2ull * (uint64_t)b->args[0] * (uint64_t)b->args[1] * (uint64_t)b->args[2];
+      break;
+    case SAGE_BODY_STENCIL:
+      kind = SAGE_KERNEL_STENCIL;
+      work = 12ull * (uint64_t)b->args[0] * (uint64_t)b->args[1] * (uint64_t)b->args[2];
+      break;
+    case SAGE_BODY_SPMV:
+      kind = SAGE_KERNEL_SPMV;  // row_ptr + (col, val) per nnz + x gathers + y
+      work = 4ull * (b->args[0] + 1) + 8ull * b->args[1] + 4ull * b->args[1] + 4ull * b->args[0];
+      break;
+    default: sb = nullptr;
+  }
+  stat_end(G, s, kind, sb, work);
+  return SAGE_OK;
+}
+
 extern "C" int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handle *begin_ev, sage_handle *end_ev) {
   if (!b || !begin_ev || !end_ev) return fail(SAGE_EINVAL, "launch: null argument");
   Gpu *G; cudaStream_t s;
@@ -252,31 +279,7 @@ extern "C" int sage_launch(sage_handle slot, const sage_body_desc *b, sage_handl
   Event *eb, *ee;
   SAGE_TRY(event_new(G->id, begin_ev, &eb));
   SAGE_TRY(event_record(eb, s));
-  cudaEvent_t sb = stat_begin(G, s);
-  SAGE_TRY(launch_body(b, s, G->sm_count));
-  {
-    // algorithmic work per launch (bytes; FLOPs for sgemm)
-    uint64_t work = 0;
-    int kind = SAGE_KERNEL_TOUCH;
-    switch (b->body) {
-      case SAGE_BODY_TOUCH: work = b->ro_bytes + b->input_bytes; break;
-      case SAGE_BODY_SGEMM:
-      case SAGE_BODY_SGEMM_F32:
-        kind = SAGE_KERNEL_SGEMM;
-        work = 2ull * (uint64_t)b->args[0] * (uint64_t)b->args[1] * (uint64_t)b->args[2];
-        break;
-      case SAGE_BODY_STENCIL:
-        kind = SAGE_KERNEL_STENCIL;
-        work = 12ull * (uint64_t)b->args[0] * (uint64_t)b->args[1] * (uint64_t)b->args[2];
-        break;
-      case SAGE_BODY_SPMV:
-        kind = SAGE_KERNEL_SPMV;  // row_ptr + (col, val) per nnz + x gathers + y
-        work = 4ull * (b->args[0] + 1) + 8ull * b->args[1] + 4ull * b->args[1] + 4ull * b->args[0];
-        break;
-      default: sb = nullptr;
-    }
-    stat_end(G, s, kind, sb, work);
-  }
+  SAGE_TRY(launch_timed(G, s, b));
   SAGE_TRY(event_new(G->id, end_ev, &ee));
   return event_record(ee, s);
 }

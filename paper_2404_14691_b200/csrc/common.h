@@ -78,12 +78,19 @@ struct Event {
   std::atomic<int> host_done{0}; // host job completion (FixedGSL)
   int64_t host_time = -1;        // host job completion time
   bool recorded = false;
+  std::atomic<int> refs{1};      // handles naming this event (event_alias)
+  std::atomic<bool> done{false}; // sticky completion (skips re-queries)
+  int64_t t_cache = INT64_MIN;   // host-clock time once resolved
 };
 int event_new(int gpu, sage_handle *h, Event **out);        // device event
 int event_new_host(sage_handle *h, Event **out);            // host-completed event
+// a second handle on the same recorded event (a stage boundary shared by the
+// stage that ends and the one that begins there); released independently
+int event_alias(sage_handle src, sage_handle *out);
 Event *event_get(sage_handle h);
 int event_record(Event *e, cudaStream_t s);
 int event_time_us(Event *e, int64_t *t);                    // requires completion
+int event_query(Event *e);                                  // SAGE_OK / SAGE_ENOTREADY
 
 // --------------------------------------------------------------- per GPU ----
 struct Layout;
@@ -103,8 +110,14 @@ struct Gpu {
   int sm_count = 0;
   CUcontext primary = nullptr;
   cudaStream_t copy = nullptr, land = nullptr, host = nullptr, d2h = nullptr, aux = nullptr;
-  cudaStream_t direct = nullptr;          // pinned identity loads: DMA + verify, off the ring
+  cudaStream_t direct = nullptr;          // pinned identity loads: back-to-back DMAs, off the ring
+  cudaStream_t verify = nullptr;          // ... and their checksum pass, so DMAs never wait on it
+  cudaEvent_t ev_dma = nullptr;           // direct -> verify hand-off (re-recorded under load_mu)
   std::vector<cudaStream_t> slots;        // pre-created stream pool (the "context pool")
+  std::vector<cudaStream_t> rets;         // RETURN copy streams (empty: copy on the slot stream)
+  cudaEvent_t ev_ret = nullptr;           // slot -> return stream hand-off (under ret_mu)
+  uint64_t ret_seq = 0;
+  std::mutex ret_mu;
   std::vector<int> slot_free;             // free slot indices
   std::mutex slot_mu;
   // staging rings
@@ -172,6 +185,12 @@ int slot_stream(sage_handle h, Gpu **G, cudaStream_t *s);
 int wait_events(cudaStream_t s, const sage_handle *w, int n);
 // bodies (bodies.cu)
 int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count);
+int launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b);   // + live kernel stats
+// RETURN copy after `prev` (the boundary event just recorded on slot stream
+// s, or 0): on s, or -- a D2H (host_dst) with G->rets configured -- on a
+// return stream
+int return_enqueue(Gpu *G, cudaStream_t s, sage_handle prev, uint64_t src, void *dst, uint64_t bytes,
+                   bool host_dst, sage_handle *begin_ev, sage_handle *end_ev);
 int touch_all_kernels();
 // tcgen05 GEMM (gemm_tc.cu)
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);

@@ -133,17 +133,35 @@ Event *event_get(sage_handle h) {
   auto it = g_ev.events.find(h & ((1ull << 56) - 1));
   return it == g_ev.events.end() ? nullptr : it->second;
 }
+int event_alias(sage_handle src, sage_handle *out) {
+  Event *e = event_get(src);
+  if (!e || !out) return fail(SAGE_ESTATE, "event_alias: unknown event");
+  e->refs.fetch_add(1);
+  uint64_t id = g_ev.next++;
+  {
+    std::lock_guard<std::mutex> lk(g_ev.mu);
+    g_ev.events[id] = e;
+  }
+  *out = make_handle(Kind::Event, id);
+  return SAGE_OK;
+}
 int event_record(Event *e, cudaStream_t s) {
   SAGE_CUDA(cudaEventRecord(e->ev, s));
   e->recorded = true;
+  e->done.store(false, std::memory_order_relaxed);
+  e->t_cache = INT64_MIN;
   return SAGE_OK;
 }
 
-static int event_query_raw(Event *e) {
+int event_query(Event *e) {
   if (!e->ev) return e->host_done.load(std::memory_order_acquire) ? SAGE_OK : SAGE_ENOTREADY;
+  if (e->done.load(std::memory_order_acquire)) return SAGE_OK;
   if (!e->recorded) return fail(SAGE_ESTATE, "event was never recorded");
   cudaError_t r = cudaEventQuery(e->ev);
-  if (r == cudaSuccess) return SAGE_OK;
+  if (r == cudaSuccess) {
+    e->done.store(true, std::memory_order_release);
+    return SAGE_OK;
+  }
   if (r == cudaErrorNotReady) return SAGE_ENOTREADY;
   return cuda_fail(r, "cudaEventQuery");
 }
@@ -157,10 +175,12 @@ int event_time_us(Event *e, int64_t *t) {
   Gpu *G = gpu_get(e->gpu);
   if (!G) return fail(SAGE_ENODEV, "event gpu");
   std::lock_guard<std::mutex> lk(G->anchor_mu);
+  if (e->t_cache != INT64_MIN) { *t = e->t_cache; return SAGE_OK; }
   clock_anchor_refresh(G);
   float ms = 0.f;
   SAGE_CUDA(cudaEventElapsedTime(&ms, G->anchor, e->ev));
-  *t = G->anchor_us + (int64_t)llround((double)ms * 1000.0);
+  *t = e->t_cache = G->anchor_us + (int64_t)llround((double)ms * 1000.0);
+  e->done.store(true, std::memory_order_release);
   return SAGE_OK;
 }
 
@@ -354,6 +374,32 @@ void stats_clear_gpu(Gpu *G) {
   G->stat_free.clear();
 }
 
+int return_enqueue(Gpu *G, cudaStream_t s, sage_handle prev, uint64_t src, void *dst, uint64_t bytes,
+                   bool host_dst, sage_handle *begin_ev, sage_handle *end_ev) {
+  if (bytes && (!dst || !src)) return fail(SAGE_EINVAL, "return: null buffer");
+  Event *b, *e;
+  std::unique_lock<std::mutex> lk(G->ret_mu, std::defer_lock);
+  if (bytes && host_dst && !G->rets.empty()) {
+    // the copy leaves the slot stream for a return stream (so it never waits
+    // behind, nor holds up, work aliased onto the slot's hardware queue)
+    lk.lock();
+    SAGE_CUDA(cudaEventRecord(G->ev_ret, s));
+    s = G->rets[G->ret_seq++ % G->rets.size()];
+    SAGE_CUDA(cudaStreamWaitEvent(s, G->ev_ret, 0));
+    prev = 0;
+  }
+  if (prev) {
+    SAGE_TRY(event_alias(prev, begin_ev));    // RETURN begins where COMPUTE ended
+  } else {
+    SAGE_TRY(event_new(G->id, begin_ev, &b));
+    SAGE_TRY(event_record(b, s));
+  }
+  // UVA: the destination is pinned host memory (D2H) or an HBM buffer (D2D)
+  if (bytes) SAGE_CUDA(cudaMemcpyAsync(dst, (const void *)src, bytes, cudaMemcpyDefault, s));
+  SAGE_TRY(event_new(G->id, end_ev, &e));
+  return event_record(e, s);
+}
+
 }  // namespace sage
 
 using namespace sage;
@@ -453,7 +499,8 @@ int sage_shutdown(void) {
   }
   {
     std::lock_guard<std::mutex> lk(g_ev.mu);
-    for (auto &kv : g_ev.events) {
+    for (auto &kv : g_ev.events) {   // aliased events: freed with their last handle
+      if (kv.second->refs.fetch_sub(1) != 1) continue;
       if (kv.second->ev) cudaEventDestroy(kv.second->ev);
       delete kv.second;
     }
@@ -480,7 +527,7 @@ int sage_shutdown(void) {
 int sage_event_query(sage_handle h) {
   Event *e = event_get(h);
   if (!e) return fail(SAGE_ESTATE, "unknown event handle");
-  return event_query_raw(e);
+  return event_query(e);
 }
 int sage_event_sync(sage_handle h) {
   Event *e = event_get(h);
@@ -496,7 +543,7 @@ int sage_event_sync(sage_handle h) {
 int sage_event_time(sage_handle h, int64_t *t) {
   Event *e = event_get(h);
   if (!e || !t) return fail(SAGE_ESTATE, "unknown event handle");
-  int rc = event_query_raw(e);
+  int rc = event_query(e);
   if (rc != SAGE_OK) return rc;
   return event_time_us(e, t);
 }
@@ -510,6 +557,7 @@ int sage_event_release(sage_handle h) {
     e = it->second;
     g_ev.events.erase(it);
   }
+  if (e->refs.fetch_sub(1) != 1) return SAGE_OK;   // another handle still names it
   if (e->ev) {
     std::lock_guard<std::mutex> lk(g_evpool_mu);
     if (e->gpu >= 0 && e->gpu < (int)g_evpool.size()) g_evpool[e->gpu].push_back(e->ev);
@@ -529,7 +577,7 @@ int sage_event_poll(const sage_handle *evs, int n, uint8_t *done, int64_t timeou
   for (;;) {
     int cnt = 0;
     for (int i = 0; i < n; ++i) {
-      int rc = event_query_raw(es[i]);
+      int rc = event_query(es[i]);
       if (rc == SAGE_OK) { done[i] = 1; ++cnt; }
       else if (rc == SAGE_ENOTREADY) done[i] = 0;
       else return rc;
@@ -667,16 +715,7 @@ int sage_return(sage_handle slot, uint64_t src, void *host_dst, uint64_t bytes, 
   Gpu *G; cudaStream_t s;
   SAGE_TRY(slot_lookup(slot, &G, &s));
   cudaSetDevice(G->dev);
-  Event *b, *e;
-  SAGE_TRY(event_new(G->id, begin_ev, &b));
-  SAGE_TRY(event_record(b, s));
-  if (bytes) {
-    if (!host_dst || !src) return fail(SAGE_EINVAL, "return: null buffer");
-    // UVA: the destination is pinned host memory (D2H) or an HBM buffer (D2D)
-    SAGE_CUDA(cudaMemcpyAsync(host_dst, (const void *)src, bytes, cudaMemcpyDefault, s));
-  }
-  SAGE_TRY(event_new(G->id, end_ev, &e));
-  return event_record(e, s);
+  return return_enqueue(G, s, 0, src, host_dst, bytes, false, begin_ev, end_ev);
 }
 
 int sage_d2h_cache(int gpu, uint64_t src, void *host_dst, uint64_t bytes, const sage_handle *wait, int n_wait,

@@ -66,9 +66,29 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
   I->gpu = d->gpu;
   I->t_enqueue = host_now_us();
   int rc = sage_ctx_acquire(d->gpu, &I->slot);
+  Gpu *G = nullptr;
+  cudaStream_t s = nullptr;
+  if (rc == SAGE_OK) rc = slot_stream(I->slot, &G, &s);
+  if (rc == SAGE_OK) cudaSetDevice(G->dev);
+  // Stage boundaries on the slot stream are shared: the event that ends one
+  // stage also begins the next (one record + one time read instead of two).
+  auto rec = [&](sage_handle *h) -> int {
+    Event *e;
+    SAGE_TRY(event_new(d->gpu, h, &e));
+    return event_record(e, s);
+  };
+  sage_handle last = 0;  // the boundary most recently recorded on s
   // GPU_CTX: bind the function context on the invocation's pooled stream
-  if (rc == SAGE_OK && (d->flags & SAGE_INV_CTX))
-    rc = sage_ctx_bind(I->slot, d->ctx_dptr, d->ctx_bytes, nullptr, 0, &I->ctx_b, &I->ctx_e);
+  // (zero its 64 KiB header: descriptor table, scratch counters)
+  if (rc == SAGE_OK && (d->flags & SAGE_INV_CTX)) {
+    rc = rec(&I->ctx_b);
+    if (rc == SAGE_OK && d->ctx_dptr && d->ctx_bytes) {
+      cudaError_t e = cudaMemsetAsync((void *)d->ctx_dptr, 0, std::min<uint64_t>(d->ctx_bytes, 64 << 10), s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "ctx bind memset");
+    }
+    if (rc == SAGE_OK) rc = rec(&I->ctx_e);
+    last = I->ctx_e;
+  }
   // CPU_LOAD -> GPU_LOAD: the read-only segment ...
   if (rc == SAGE_OK && (d->flags & SAGE_INV_RO)) {
     sage_load_desc L{};
@@ -100,11 +120,21 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
   if (I->in_end) deps[nd++] = I->in_end;
   if (rc == SAGE_OK && (d->flags & SAGE_INV_SYNC)) {
     for (int i = 0; i < d->n_wait && i < 2; ++i) deps[nd++] = d->wait[i];
-    rc = sage_sync_wait(I->slot, deps, nd, &I->sync_b, &I->sync_e);
-    nd = 0;  // same stream from here on
+    rc = last ? event_alias(last, &I->sync_b) : rec(&I->sync_b);
+    if (rc == SAGE_OK) rc = wait_events(s, deps, nd);
+    if (rc == SAGE_OK) rc = rec(&I->sync_e);
+    last = I->sync_e;
+  } else if (rc == SAGE_OK && nd) {
+    rc = wait_events(s, deps, nd);
+    last = 0;  // COMPUTE begins when the joins clear, not at the last boundary
   }
-  if (rc == SAGE_OK) rc = sage_launch_after(I->slot, deps, nd, &d->body, &I->comp_b, &I->comp_e);
-  if (rc == SAGE_OK) rc = sage_return(I->slot, d->ret_src, d->ret_dst, d->ret_bytes, &I->ret_b, &I->ret_e);
+  // COMPUTE
+  if (rc == SAGE_OK) rc = last ? event_alias(last, &I->comp_b) : rec(&I->comp_b);
+  if (rc == SAGE_OK) rc = launch_timed(G, s, &d->body);
+  if (rc == SAGE_OK) rc = rec(&I->comp_e);
+  // RETURN
+  if (rc == SAGE_OK) rc = return_enqueue(G, s, I->comp_e, d->ret_src, d->ret_dst, d->ret_bytes,
+                                        (d->flags & SAGE_INV_RET_HOST) != 0, &I->ret_b, &I->ret_e);
   if (rc != SAGE_OK) {
     std::string msg = sage_last_error();
     Gpu *G = gpu_get(d->gpu);

@@ -216,6 +216,7 @@ struct Load {
   int gpu = -1;
   sage_handle hb = 0, he = 0;                 // pooled begin / end events (internal)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  Event *eb = nullptr, *ee = nullptr;         // ... as Events (cached times)
   std::atomic<int64_t> cpu_begin{-1}, cpu_end{-1};
   uint64_t host_bytes = 0, link_bytes = 0, landed = 0;
   uint32_t chunks = 0;
@@ -242,15 +243,6 @@ static void CUDART_CB host_copy_fn(void *p) {
   parallel_memcpy(a->dst, a->src, a->bytes);
   a->L->cpu_end.store(host_now_us());
   delete a;
-}
-
-static int raw_event_time(Gpu *G, cudaEvent_t ev, int64_t *t) {
-  std::lock_guard<std::mutex> lk(G->anchor_mu);
-  clock_anchor_refresh(G);
-  float ms = 0.f;
-  SAGE_CUDA(cudaEventElapsedTime(&ms, G->anchor, ev));
-  *t = G->anchor_us + (int64_t)llround((double)ms * 1000.0);
-  return SAGE_OK;
 }
 
 static int wait_list(cudaStream_t s, const sage_handle *w, int n) {
@@ -407,15 +399,16 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
     if (rc == SAGE_OK) rc = plan_upload(&lay->whole, d->gpu);
     if (rc != SAGE_OK) { delete L; return rc; }
   }
-  Event *E, *Eb, *Ee;
+  Event *Eb, *Ee;
   {
-    int rc = event_new(d->gpu, end_ev, &E);
-    if (rc == SAGE_OK) rc = event_new(d->gpu, &L->hb, &Eb);
+    int rc = event_new(d->gpu, &L->hb, &Eb);
     if (rc == SAGE_OK) rc = event_new(d->gpu, &L->he, &Ee);
     if (rc != SAGE_OK) { delete L; return rc; }
   }
   L->ev_begin = Eb->ev;
   L->ev_end = Ee->ev;
+  L->eb = Eb;
+  L->ee = Ee;
   L->landed = lay->seg;
   L->acc_idx = (uint32_t)(G->scratch.next++ % G->scratch.n);
   G->scratch.h_res[L->acc_idx] = 0;   // an empty load publishes nothing
@@ -425,7 +418,8 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
       lay->seg / 16 < 0xFFFFFFFFull) {
     // direct path: an identity load from pinned memory needs no staging or
     // unpack -- one DMA straight into dst on its own stream (so it never
-    // queues behind memcpy-gated ring chunks) + a read-only verify pass
+    // queues behind memcpy-gated ring chunks) + a read-only verify pass on a
+    // second stream, so the next DMA starts while this one is verified
     cudaStream_t s = G->direct;
     std::lock_guard<std::mutex> lk(G->load_mu);
     SAGE_TRY(wait_list(s, d->wait, d->n_wait));
@@ -434,6 +428,9 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
     const uint64_t n = d->src_bytes, seg = lay->seg;
     if (seg > n) SAGE_CUDA(cudaMemsetAsync(dst + n, 0, seg - n, s));
     SAGE_CUDA(cudaMemcpyAsync(dst, d->src, n, cudaMemcpyHostToDevice, s));
+    SAGE_CUDA(cudaEventRecord(G->ev_dma, s));
+    s = G->verify;
+    SAGE_CUDA(cudaStreamWaitEvent(s, G->ev_dma, 0));
     L->link_bytes = n;
     L->chunks = 1;
     LandArgs a{};
@@ -448,7 +445,7 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
     SAGE_CUDA(cudaGetLastError());
     stat_end(G, s, SAGE_KERNEL_VERIFY, sb, seg);
     SAGE_TRY(event_record(Ee, s));
-    SAGE_TRY(event_record(E, s));
+    SAGE_TRY(event_alias(L->he, end_ev));   // the caller's end handle: same event
     uint64_t id = g_load_next++;
     {
       std::lock_guard<std::mutex> lk2(g_load_mu);
@@ -516,7 +513,7 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
   }
   if (!L->has_gpu_begin) SAGE_TRY(event_record(Eb, G->land));
   SAGE_TRY(event_record(Ee, G->land));
-  if ((rc = event_record(E, G->land)) != SAGE_OK) return rc;
+  SAGE_TRY(event_alias(L->he, end_ev));
   uint64_t id = g_load_next++;
   {
     std::lock_guard<std::mutex> lk2(g_load_mu);
@@ -536,15 +533,14 @@ int sage_load_info_get(sage_handle h, sage_load_info *out) {
     L = it->second;
   }
   cudaSetDevice(dev_of(L->gpu));
-  cudaError_t q = cudaEventQuery(L->ev_end);
-  if (q == cudaErrorNotReady) return SAGE_ENOTREADY;
-  if (q != cudaSuccess) return cuda_fail(q, "load end event");
+  int q = event_query(L->ee);
+  if (q != SAGE_OK) return q;
   Gpu *G = gpu_get(L->gpu);
   memset(out, 0, sizeof *out);
   out->cpu_begin_us = L->cpu_begin.load();
   out->cpu_end_us = L->cpu_end.load();
-  SAGE_TRY(raw_event_time(G, L->ev_begin, &out->gpu_begin_us));
-  SAGE_TRY(raw_event_time(G, L->ev_end, &out->gpu_end_us));
+  SAGE_TRY(event_time_us(L->eb, &out->gpu_begin_us));
+  SAGE_TRY(event_time_us(L->ee, &out->gpu_end_us));
   out->host_bytes = L->host_bytes;
   out->link_bytes = L->link_bytes;
   out->landed_bytes = L->landed;

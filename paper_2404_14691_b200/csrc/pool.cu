@@ -184,11 +184,26 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
   SAGE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   SAGE_CUDA(cudaStreamCreateWithPriority(&G->copy, cudaStreamNonBlocking, hi));
   SAGE_CUDA(cudaStreamCreateWithPriority(&G->direct, cudaStreamNonBlocking, hi));
+  SAGE_CUDA(cudaStreamCreateWithPriority(&G->verify, cudaStreamNonBlocking, hi));
+  SAGE_CUDA(cudaEventCreateWithFlags(&G->ev_dma, cudaEventDisableTiming));
   SAGE_CUDA(cudaStreamCreateWithPriority(&G->land, cudaStreamNonBlocking, hi));
   SAGE_CUDA(cudaStreamCreateWithFlags(&G->host, cudaStreamNonBlocking));
   SAGE_CUDA(cudaStreamCreateWithFlags(&G->d2h, cudaStreamNonBlocking));
   SAGE_CUDA(cudaStreamCreateWithFlags(&G->aux, cudaStreamNonBlocking));
-  const int kSlots = 64;
+  {
+    // D2H RETURN copy streams (SAGE_RETURN_STREAMS; 0 = on the slot).  Two
+    // measured best for the cfg-2 e2e burst (+5% over the slot stream)
+    const char *env = getenv("SAGE_RETURN_STREAMS");
+    int nret = env ? atoi(env) : 2;
+    for (int i = 0; i < nret && i < 16; ++i) {
+      cudaStream_t s;
+      SAGE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      G->rets.push_back(s);
+    }
+    SAGE_CUDA(cudaEventCreateWithFlags(&G->ev_ret, cudaEventDisableTiming));
+  }
+  const char *slot_env = getenv("SAGE_SLOTS");
+  const int kSlots = slot_env ? std::max(4, std::min(256, atoi(slot_env))) : 64;
   for (int i = 0; i < kSlots; ++i) {
     cudaStream_t s;
     SAGE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -241,8 +256,12 @@ void gpu_teardown(Gpu *G) {
   pool_destroy(G);
   for (auto s : G->slots) cudaStreamDestroy(s);
   G->slots.clear();
-  for (cudaStream_t s : {G->copy, G->direct, G->land, G->host, G->d2h, G->aux})
+  for (auto s : G->rets) cudaStreamDestroy(s);
+  G->rets.clear();
+  if (G->ev_ret) cudaEventDestroy(G->ev_ret);
+  for (cudaStream_t s : {G->copy, G->direct, G->verify, G->land, G->host, G->d2h, G->aux})
     if (s) cudaStreamDestroy(s);
+  if (G->ev_dma) cudaEventDestroy(G->ev_dma);
   for (auto e : G->ev_cpu) cudaEventDestroy(e);
   for (auto e : G->ev_h2d) cudaEventDestroy(e);
   for (auto e : G->ev_land) cudaEventDestroy(e);

@@ -388,6 +388,8 @@ class DataPlane:
         else:
             run.result = self.pinned.get(max(16, fd.out_bytes))
             d.ret_dst = run.result.ptr
+            flags |= _lib.INV_RET_HOST
+        d.flags = flags
         h, done, ro_end, ctx_end = _lib.H(), _lib.H(), _lib.H(), _lib.H()
         _lib.check(_lib.lib().sage_invoke(_lib.C.byref(d), _lib.C.byref(h), _lib.C.byref(done), _lib.C.byref(ro_end),
                                           _lib.C.byref(ctx_end)), "sage_invoke")

@@ -18,6 +18,7 @@ from __future__ import annotations
 import argparse
 import json
 import math
+import sys
 import time
 from pathlib import Path
 
@@ -100,7 +101,7 @@ def cfg3(rate: float = 300.0, duration_s: float = 4.0, gpus_list=(1, 2, 4), seed
     return out
 
 
-def cfg4(rate: float = 20.0, duration_s: float = 10.0, seed: int = 1, include_fixedgsl: bool = True) -> dict:
+def cfg4(rate: float = 10.0, duration_s: float = 6.0, seed: int = 1, include_fixedgsl: bool = True) -> dict:
     ro = [10 * (2048 / 10) ** (k / 9) for k in range(10)]          # log-spaced 10 .. 2048 MiB
     table, data = {}, {}
     for k, r in enumerate(ro):
@@ -146,6 +147,7 @@ def cfg4(rate: float = 20.0, duration_s: float = 10.0, seed: int = 1, include_fi
             s.update(throughput_per_s=len(invs) / wall, wall_s=wall, peak_resident_functions=peak_res,
                      peak_gpu_mem_gb=peak_mem / 1e9, avg_gpu_mem_gb=area / max(1e-9, wall) / 1e9)
             out[pol] = _round(s)
+            print(json.dumps({"cfg4_partial": pol, **out[pol]}), file=sys.stderr, flush=True)
         finally:
             sim.close()
     return out

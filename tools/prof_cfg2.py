@@ -24,6 +24,8 @@ if mode == "value":
     sim.dataplane.stage_sources_in_hbm(0)
     sim.dataplane.results_in_hbm = True
     payloads = None
+elif mode == "e2e":
+    sim.dataplane.pin_host_store()
 
 
 def burst():
@@ -44,8 +46,13 @@ print(mode, "submit_ms", [round(r[0], 2) for r in rows], "total_ms", [round(r[1]
 invs = rows[-1][2]
 last = max(invs, key=lambda i: i.completion_us)
 t0 = min(i.arrival_us for i in invs)
-for i in invs[:3] + invs[-3:]:
-    print(i.id, i.spec.name, i.warmth.label(), {k.value: (v[0] - t0, v[1] - t0) for k, v in i.stages.items()})
+print("timeline (ms from arrival): name warmth | gpu_load | compute | return")
+for i in sorted(invs, key=lambda i: i.stages[next(iter(i.stages))][0]):
+    cols = []
+    for k, v in i.stages.items():
+        if k.value in ("gpu_load", "compute", "return", "sync_wait"):
+            cols.append(f"{k.value[:4]} {(v[0] - t0) / 1e3:6.2f}-{(v[1] - t0) / 1e3:6.2f}")
+    print(f"{i.id:5d} {i.spec.name:8s} {i.warmth.label():8s} {i.ro_source or '-':6s} | " + " | ".join(cols))
 pr = cProfile.Profile()
 pr.enable()
 burst()

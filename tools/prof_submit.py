@@ -43,3 +43,29 @@ for stats in (0, 1):
     print(f"stats={stats}: submit {1e6*(t1-t0)/64:.1f} us/inv, of which sage_invoke {1e6*acc['invoke']/acc['n']:.1f} us; "
           f"burst total {1e3*(t2-t0):.2f} ms")
 sim.close()
+
+# ---- where the host time goes (cProfile over 4 bursts, stats off) ----------
+import cProfile  # noqa: E402
+import pstats  # noqa: E402
+
+sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=1, function_data=data, copy_results=False)
+sim.dataplane.stage_sources_in_hbm(0)
+sim.dataplane.results_in_hbm = True
+L.sage_stats_enable(0)
+for rep in range(3):
+    for r in list(sim.sharing.residents.values()):
+        sim.sharing._evict(r)
+    sim.submit_many(names)
+    sim.drain()
+pr = cProfile.Profile()
+for rep in range(4):
+    for r in list(sim.sharing.residents.values()):
+        sim.sharing._evict(r)
+    pr.enable()
+    sim.submit_many(names)
+    sim.drain()
+    pr.disable()
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(40)
+st.sort_stats("cumulative").print_stats(40)
+sim.close()
