@@ -273,6 +273,13 @@ typedef struct {
 int sage_invoke(const sage_invoke_desc *d, sage_handle *inv, sage_handle *done_ev, sage_handle *ro_end,
                 sage_handle *ctx_end);
 int sage_invoke_collect(sage_handle inv, sage_invoke_info *out);   /* ENOTREADY until done */
+/* Finished invocations in completion order: up to `max` handles into `out`,
+ * waiting up to timeout_us for the first.  Returns the count (>= 0).  The
+ * device signals completion with a host function on the slot stream; the
+ * library's completion thread has already resolved every stage time, so the
+ * following sage_invoke_collect is a copy.  (Replaces polling each
+ * invocation's done event: PlanExecution completion, functions.py:420-433.) */
+int sage_invoke_ready(sage_handle *out, int max, int64_t timeout_us);
 int sage_invoke_release(sage_handle inv);
 
 /* ---- FixedGSL serial baseline (policies.py:102-126, functions.py:261-267) ---

@@ -136,6 +136,7 @@ _SIGS = {
     "sage_invoke": (C.c_int, [C.POINTER(InvokeDesc), C.POINTER(H), C.POINTER(H), C.POINTER(H), C.POINTER(H)]),
     "sage_invoke_collect": (C.c_int, [H, C.POINTER(InvokeInfo)]),
     "sage_invoke_release": (C.c_int, [H]),
+    "sage_invoke_ready": (C.c_int, [C.POINTER(H), C.c_int, i64]),
     "sage_fixedgsl_submit": (C.c_int, [C.POINTER(FixedGSLDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_fixedgsl_info_get": (C.c_int, [H, C.POINTER(FixedGSLInfo)]),
     "sage_fixedgsl_release": (C.c_int, [H]),

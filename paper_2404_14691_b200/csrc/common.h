@@ -196,6 +196,9 @@ int touch_all_kernels();
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
 int touch_tc_kernels();
 
+// invocations (invoke.cu): stop the completion thread, drop live records
+void invoke_shutdown();
+
 // layouts (land.cu)
 int layouts_destroy_all();
 

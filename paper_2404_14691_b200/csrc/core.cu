@@ -490,6 +490,7 @@ int sage_shutdown(void) {
     cudaSetDevice(G->dev);
     cudaDeviceSynchronize();
   }
+  invoke_shutdown();
   pool_threads_stop();
   layouts_destroy_all();
   {

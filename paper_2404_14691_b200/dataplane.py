@@ -175,6 +175,37 @@ class _Borrowed(D.Event):
         self.h = 0
 
 
+class _FastCompletions:
+    """Engine completion source for sage_invoke runs: the library's
+    completion thread queues finished invocations (already resolved), so the
+    loop neither polls per-invocation events nor computes stage times."""
+
+    def __init__(self, dp: "DataPlane", batch: int = 256):
+        self.dp = dp
+        self.runs: dict[int, _Run] = {}
+        self._buf = (_lib.H * batch)()
+        self._n = batch
+
+    def outstanding(self) -> int:
+        return len(self.runs)
+
+    def poll(self, timeout_us: int) -> int:
+        n = _lib.lib().sage_invoke_ready(self._buf, self._n, int(timeout_us))
+        if n < 0:
+            _lib.check(n, "sage_invoke_ready")
+        if n == 0:
+            return 0
+        eng = self.dp.sim.engine
+        eng.tick()
+        fired = 0
+        for k in range(n):
+            run = self.runs.pop(self._buf[k], None)
+            if run is not None:
+                self.dp._on_done(run)
+                fired += 1
+        return fired
+
+
 class DataPlane:
     """Device side of one Simulation (runtime.py)."""
 
@@ -185,6 +216,8 @@ class DataPlane:
         self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
         self._free_slots: dict[int, list] = {}
         self._fast_cache: dict[int, bool] = {}
+        self._fast = _FastCompletions(self)
+        self._fast_source = False
 
     def _slot(self, gpu: int) -> D.Slot:
         """A pooled stream of the pre-created context, kept acquired across invocations."""
@@ -298,7 +331,13 @@ class DataPlane:
         except Exception:
             self._release(run)
             raise
-        self.sim.engine.watch(run.end, self._on_done, run)
+        if run.invh:
+            if not self._fast_source:
+                self.sim.engine.add_source(self._fast)
+                self._fast_source = True
+            self._fast.runs[run.invh] = run
+        else:
+            self.sim.engine.watch(run.end, self._on_done, run)
 
     # ------------------------------------------------- one-call fast path -----
     def _fast_ok(self, plan: StagePlan) -> bool:
@@ -782,6 +821,8 @@ class DataPlane:
         if run.job is not None:
             run.job.release()
             run.job = None
+        if run.inv is not None and run.inv.run is run:
+            run.inv.run = None   # break inv <-> run: finished records free by refcount
 
     def close(self) -> None:
         self.unpin_host_store()

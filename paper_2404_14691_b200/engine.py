@@ -94,6 +94,7 @@ class Engine:
         self._heap: list = []
         self._live = 0
         self._watches: list[_Watch] = []
+        self._sources: list = []   # completion sources: .outstanding() / .poll(timeout_us)
         self._log = [] if log_events else None
 
     # time ---------------------------------------------------------------------
@@ -139,8 +140,25 @@ class Engine:
         """Call callback(payload) from the loop once device_event completes."""
         self._watches.append(_Watch(device_event, callback, payload))
 
+    def add_source(self, source) -> None:
+        """A completion source the loop drains besides watched events: an
+        object with outstanding() -> int and poll(timeout_us) -> callbacks run
+        (the data plane's native completion queue)."""
+        self._sources.append(source)
+
+    def _outstanding(self) -> int:
+        return sum(s.outstanding() for s in self._sources)
+
+    def _poll_sources(self, timeout_us: int) -> int:
+        n = 0
+        for s in self._sources:
+            if s.outstanding():
+                n += s.poll(timeout_us)
+                timeout_us = 0
+        return n
+
     def watching(self) -> int:
-        return len(self._watches)
+        return len(self._watches) + self._outstanding()
 
     def _poll_watches(self, timeout_us: int) -> int:
         if not self._watches:
@@ -202,6 +220,8 @@ class Engine:
             n += 1
         self._now = max(self._now, wall)
         n += self._poll_watches(0)
+        if self._sources:
+            n += self._poll_sources(0)
         return n
 
     def run(self, until: Optional[int] = None, idle: Optional[Callable[[], bool]] = None) -> int:
@@ -217,7 +237,8 @@ class Engine:
             nt = self._next_timer()
             if until is not None and self._now >= until:
                 break
-            if nt is None and not self._watches:
+            outstanding = self._outstanding() if self._sources else 0
+            if nt is None and not self._watches and not outstanding:
                 if until is None:
                     break
                 time.sleep(max(0, until - self.wall_us()) / 1e6)
@@ -228,13 +249,16 @@ class Engine:
                 horizon = min(horizon, until)
             wait = max(0, horizon - self.wall_us())
             if self._watches:
-                dispatched += self._poll_watches(min(wait, 200))
-            elif wait > 0:
+                dispatched += self._poll_watches(0 if outstanding else min(wait, 200))
+            if outstanding:
+                # blocks in the library (GIL released) until a completion
+                dispatched += self._poll_sources(min(wait, 50 if self._watches else 200))
+            elif not self._watches and wait > 0:
                 time.sleep(min(wait, 2000) / 1e6)
         return dispatched
 
     def pending(self) -> int:
-        return self._live + len(self._watches)
+        return self._live + len(self._watches) + self._outstanding()
 
     @property
     def event_log(self) -> list[str]:

@@ -16,6 +16,7 @@ Reported per invocation (reference semantics, metrics.py:184-213):
 """
 from __future__ import annotations
 
+import gc
 import itertools
 from dataclasses import dataclass
 from typing import Optional
@@ -174,6 +175,11 @@ class Simulation:
         self._ids = itertools.count()
         self._in_flight = 0
         self.source = source
+        # a serving process: move everything allocated so far (torch, function
+        # data) out of the cyclic collector's reach so a full collection
+        # during a burst stays short (measured: ~7 ms hiccups otherwise)
+        gc.collect()
+        gc.freeze()
         if source is not None:
             source.attach(self)
 
