@@ -201,9 +201,41 @@ def land_probe(data, iters: int = 20) -> dict:
             raise RuntimeError("land probe: checksums differ between identical lands")
         s = kernel_stats()["land"]
         s["segment"] = f"{name} ({fd.layout.seg_bytes} B, {fd.layout.n} tensors)"
+        s["d2d_GBps"] = d2d_reference(seg.dptr, fd.db_dev.dptr, min(fd.layout.packed_bytes, fd.layout.seg_bytes))
         return s
     finally:
         seg.free()
+
+
+def d2d_reference(dst: int, src: int, nbytes: int, iters: int = 20) -> float:
+    """Copy-engine D2D of the probe's packed bytes (read + write counted), the
+    same-size ceiling next to the 2 GiB copy peak of MEASURED_PEAKS.json."""
+    from paper_2404_14691_b200 import _lib
+    from paper_2404_14691_b200 import device as D
+    L = _lib.lib()
+    evs = []
+    for _ in range(iters + 1):
+        e = _lib.H()
+        _lib.check(L.sage_fanout(0, src, 0, dst, nbytes, None, 0, _lib.C.byref(e)), "fanout")
+        evs.append(e.value)
+    D.Event(evs[-1]).sync()
+    us = _lib.C.c_double()
+    _lib.check(L.sage_event_elapsed(evs[0], evs[-1], _lib.C.byref(us)), "event_elapsed")
+    for e in evs:
+        D.Event(e).release()
+    return round(2 * nbytes * iters / us.value / 1e3, 1)
+
+
+def land_traffic(segment: str):
+    """DRAM bytes per launch of the probe's land from the committed ncu --set
+    full capture (profiles/r1_land_traffic.json), if it is the same segment."""
+    p = ROOT / "profiles" / "r1_land_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    if d.get("segment") != segment:
+        return None
+    return d["dram_bytes_read"] + d["dram_bytes_write"]
 
 
 def barrier(dist):
@@ -420,7 +452,10 @@ def our_arm(args, rank, world, dist) -> dict:
                                 "setup_p99_ms": round(percentile([i.setup_us for i in invs_pg], 99) / 1e3, 3),
                                 "note": "DB records pageable: cold loads include the CPU_LOAD memcpy"}},
         "roofline": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": land["frac"], "traffic": None, "peak_source": peaks["source"],
+                     "unit": "GB/s", "frac": land["frac"], "traffic": land_traffic(probe["segment"]),
+                     "traffic_source": "profiles/r1_land_traffic.json (ncu --set full, one launch)",
+                     "peak_source": peaks["source"], "same_size_d2d_GBps": probe["d2d_GBps"],
+                     "frac_of_same_size_d2d": round(land["achieved"] / probe["d2d_GBps"], 4),
                      "avg_launch_us": land["avg_launch_us"], "alg_bytes_per_launch": land["alg_bytes_per_launch"],
                      "launches": land["launches"], "how": f"{land['launches']} back-to-back HBM-resident lands of "
                                                            f"{land['segment']}, CUDA events on the land stream"},

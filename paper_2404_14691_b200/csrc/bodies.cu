@@ -127,6 +127,72 @@ __global__ void __launch_bounds__(256) stencil_kernel(const float *__restrict__ 
   }
 }
 
+// Vectorised stencil: a warp owns 128 consecutive x (one float4 per lane) of
+// one row y and a slab of kStZ planes.  z neighbours ride a register queue
+// (each input plane is loaded once per slab), x neighbours come from the
+// adjacent lanes by shuffle, y neighbours are L1/L2-hit float4 loads.  Needs
+// nx % 4 == 0 and 16-B aligned arrays; summation order is the scalar
+// kernel's.
+constexpr int kStZ = 8;
+__global__ void __launch_bounds__(256) stencil4_kernel(const float *__restrict__ coef, const float *__restrict__ in,
+                                                       float *__restrict__ out, int nx, int ny, int nz, float beta,
+                                                       int xsegs) {
+  const int lane = threadIdx.x & 31;
+  const long long unit = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long per_z = (long long)xsegs * ny;
+  const int zs = (int)(unit / per_z);
+  const int rem = (int)(unit - (long long)zs * per_z);
+  const int y = rem / xsegs;
+  const int x4 = (rem - y * xsegs) * 128 + lane * 4;
+  const int z0 = zs * kStZ;
+  if (z0 >= nz) return;  // warp uniform
+  const int z1 = min(nz, z0 + kStZ);
+  const bool valid = x4 < nx;
+  const size_t plane = (size_t)nx * ny;
+  const size_t col = (size_t)y * nx + (valid ? x4 : 0);
+  auto ld4 = [&](int z, size_t c) { return __ldg(reinterpret_cast<const float4 *>(in + (size_t)z * plane + c)); };
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 below = (valid && z0 > 0) ? ld4(z0 - 1, col) : zero;
+  float4 cur = valid ? ld4(z0, col) : zero;
+  const bool yin = y > 0 && y < ny - 1;
+  for (int z = z0; z < z1; ++z) {
+    const float4 above = (valid && z + 1 < nz) ? ld4(z + 1, col) : zero;
+    const bool zin = z > 0 && z < nz - 1;
+    float4 n4 = zero, s4 = zero, c4 = zero;
+    if (valid && yin && zin) {
+      n4 = ld4(z, col - nx);
+      s4 = ld4(z, col + nx);
+      c4 = __ldg(reinterpret_cast<const float4 *>(coef + (size_t)z * plane + col));
+    }
+    float left = __shfl_up_sync(0xffffffffu, cur.w, 1);
+    float right = __shfl_down_sync(0xffffffffu, cur.x, 1);
+    const size_t i = (size_t)z * plane + col;
+    if (valid) {
+      if (lane == 0 && x4 > 0) left = __ldg(in + i - 1);
+      if ((lane == 31 || x4 + 4 >= nx) && x4 + 4 < nx) right = __ldg(in + i + 4);
+      float4 o = cur;
+      if (yin && zin) {
+        const float xs[6] = {left, cur.x, cur.y, cur.z, cur.w, right};
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+        const float ns[4] = {n4.x, n4.y, n4.z, n4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+        const float bl[4] = {below.x, below.y, below.z, below.w}, ab[4] = {above.x, above.y, above.z, above.w};
+        float r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int x = x4 + j;
+          if (x == 0 || x == nx - 1) { r[j] = xs[j + 1]; continue; }
+          float s = xs[j] + xs[j + 2] + ns[j] + ss[j] + bl[j] + ab[j];
+          r[j] = fmaf(cc[j], xs[j + 1], beta * s);
+        }
+        o = make_float4(r[0], r[1], r[2], r[3]);
+      }
+      *reinterpret_cast<float4 *>(out + i) = o;
+    }
+    below = cur;
+    cur = above;
+  }
+}
+
 // ---- SPMV: CSR, 4 lanes per row ------------------------------------------------
 __global__ void __launch_bounds__(256) spmv_kernel(const int *__restrict__ rowptr, const int *__restrict__ col,
                                                    const float *__restrict__ val, const float *__restrict__ x,
@@ -137,6 +203,39 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int *__restrict__ rowpt
   if (row < rows) {
     int b = __ldg(rowptr + row), e = __ldg(rowptr + row + 1);
     for (int k = b + sub; k < e; k += 4) s = fmaf(__ldg(val + k), __ldg(x + __ldg(col + k)), s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (row < rows && sub == 0) y[row] = s;
+}
+
+// Vectorised CSR: 4 lanes per row, each lane takes 4 consecutive non-zeros
+// per step with one 16-B load of values and one of columns (a warp moves 512 B
+// of each per instruction).  Head elements before the first 4-aligned index
+// and the tail after the last full quad go scalar.  Needs col / val 16-B
+// aligned.  Per-lane partial sums are combined in the scalar kernel's
+// shuffle order.
+__global__ void __launch_bounds__(256) spmv4_kernel(const int *__restrict__ rowptr, const int *__restrict__ col,
+                                                    const float *__restrict__ val, const float *__restrict__ x,
+                                                    float *__restrict__ y, int rows) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = g >> 2, sub = g & 3;
+  float s = 0.f;
+  if (row < rows) {
+    const int b = __ldg(rowptr + row), e = __ldg(rowptr + row + 1);
+    const int a4 = min(e, (b + 3) & ~3);
+    if (b + sub < a4) s = fmaf(__ldg(val + b + sub), __ldg(x + __ldg(col + b + sub)), s);
+    int k = a4 + 4 * sub;
+    for (; k + 4 <= e; k += 16) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(val + k));
+      const int4 c = __ldg(reinterpret_cast<const int4 *>(col + k));
+      const float x0 = __ldg(x + c.x), x1 = __ldg(x + c.y), x2 = __ldg(x + c.z), x3 = __ldg(x + c.w);
+      s = fmaf(v.x, x0, s);
+      s = fmaf(v.y, x1, s);
+      s = fmaf(v.z, x2, s);
+      s = fmaf(v.w, x3, s);
+    }
+    for (; k < e; ++k) s = fmaf(__ldg(val + k), __ldg(x + __ldg(col + k)), s);
   }
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   s += __shfl_xor_sync(0xffffffffu, s, 2);
@@ -191,6 +290,13 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
       if (nx <= 0 || ny <= 0 || nz <= 0 || cells * 4 > b->ro_bytes || cells * 4 > b->input_bytes ||
           cells * 4 > b->out_bytes)
         return fail(SAGE_EINVAL, "stencil: bad shape or buffers too small");
+      if (nx % 4 == 0 && !((b->ro | b->input | b->out) & 15)) {
+        const int xsegs = (nx + 127) / 128;
+        const long long units = (long long)xsegs * ny * ((nz + kStZ - 1) / kStZ);
+        stencil4_kernel<<<(unsigned)((units + 7) / 8), 256, 0, s>>>((const float *)b->ro, (const float *)b->input,
+                                                                     (float *)b->out, nx, ny, nz, beta, xsegs);
+        break;
+      }
       dim3 grid((nx + 255) / 256, ny);
       stencil_kernel<<<grid, 256, 0, s>>>((const float *)b->ro, (const float *)b->input, (float *)b->out, nx, ny,
                                           nz, beta);
@@ -204,6 +310,12 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
           o_val + 4ull * nnz > b->ro_bytes || 4ull * rows > b->out_bytes)
         return fail(SAGE_EINVAL, "spmv: bad shape or buffers too small");
       int blocks = (int)((4ll * rows + 255) / 256);
+      if (!((b->ro + o_col) & 15) && !((b->ro + o_val) & 15)) {
+        spmv4_kernel<<<blocks, 256, 0, s>>>((const int *)(b->ro + o_rp), (const int *)(b->ro + o_col),
+                                            (const float *)(b->ro + o_val), (const float *)b->input, (float *)b->out,
+                                            rows);
+        break;
+      }
       spmv_kernel<<<blocks, 256, 0, s>>>((const int *)(b->ro + o_rp), (const int *)(b->ro + o_col),
                                          (const float *)(b->ro + o_val), (const float *)b->input, (float *)b->out,
                                          rows);
@@ -226,6 +338,8 @@ int touch_all_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, stencil_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, spmv_kernel));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, stencil4_kernel));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, spmv4_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, spin_kernel));
   SAGE_TRY(touch_tc_kernels());
   return SAGE_OK;

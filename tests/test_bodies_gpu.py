@@ -71,7 +71,9 @@ def test_sgemm_rejects_bad_shapes(dp):
     sa.free()
 
 
-@pytest.mark.parametrize("shape", [(8, 8, 4), (33, 17, 9), (256, 64, 16)])
+# nx % 4 == 0 takes the vectorised slab kernel (partial warps, z not a slab
+# multiple); other nx the scalar kernel
+@pytest.mark.parametrize("shape", [(8, 8, 4), (33, 17, 9), (256, 64, 16), (12, 10, 11), (260, 7, 5), (256, 256, 64)])
 def test_stencil(dp, shape):
     nx, ny, nz = shape
     rng = np.random.default_rng(nx)
@@ -86,7 +88,10 @@ def test_stencil(dp, shape):
     sg.free()
 
 
-def test_spmv_ragged_rows(dp):
+@pytest.mark.parametrize("misalign", [0, 4])
+def test_spmv_ragged_rows(dp, misalign):
+    """misalign 0: 16-B aligned col/val (vectorised kernel, unaligned row
+    starts); 4: col/val at 4-B offsets (scalar kernel)."""
     rng = np.random.default_rng(9)
     rows = 5000
     counts = rng.integers(0, 40, rows)
@@ -96,7 +101,7 @@ def test_spmv_ragged_rows(dp):
     col = rng.integers(0, rows, nnz, dtype=np.int32)
     val = rng.standard_normal(nnz, dtype=np.float32)
     x = rng.standard_normal(rows, dtype=np.float32)
-    o_rp, o_col = 0, (rowptr.nbytes + 255) // 256 * 256
+    o_rp, o_col = 0, (rowptr.nbytes + 255) // 256 * 256 + misalign
     o_val = o_col + (col.nbytes + 255) // 256 * 256
     ro = np.zeros(o_val + val.nbytes, np.uint8)
     ro[o_rp:o_rp + rowptr.nbytes] = rowptr.view(np.uint8)
