@@ -253,6 +253,12 @@ __global__ void spin_kernel(long long us) {
   }
 }
 
+// SAGE_BODY_LEGACY (diagnostics): bit 0 = scalar stencil, bit 1 = scalar spmv
+static int legacy_bodies() {
+  static const int v = [] { const char *e = getenv("SAGE_BODY_LEGACY"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
   switch (b->body) {
     case SAGE_BODY_TOUCH: {
@@ -290,7 +296,7 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
       if (nx <= 0 || ny <= 0 || nz <= 0 || cells * 4 > b->ro_bytes || cells * 4 > b->input_bytes ||
           cells * 4 > b->out_bytes)
         return fail(SAGE_EINVAL, "stencil: bad shape or buffers too small");
-      if (nx % 4 == 0 && !((b->ro | b->input | b->out) & 15)) {
+      if (!(legacy_bodies() & 1) && nx % 4 == 0 && !((b->ro | b->input | b->out) & 15)) {
         const int xsegs = (nx + 127) / 128;
         const long long units = (long long)xsegs * ny * ((nz + kStZ - 1) / kStZ);
         stencil4_kernel<<<(unsigned)((units + 7) / 8), 256, 0, s>>>((const float *)b->ro, (const float *)b->input,
@@ -310,7 +316,7 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
           o_val + 4ull * nnz > b->ro_bytes || 4ull * rows > b->out_bytes)
         return fail(SAGE_EINVAL, "spmv: bad shape or buffers too small");
       int blocks = (int)((4ll * rows + 255) / 256);
-      if (!((b->ro + o_col) & 15) && !((b->ro + o_val) & 15)) {
+      if (!(legacy_bodies() & 2) && !((b->ro + o_col) & 15) && !((b->ro + o_val) & 15)) {
         spmv4_kernel<<<blocks, 256, 0, s>>>((const int *)(b->ro + o_rp), (const int *)(b->ro + o_col),
                                             (const float *)(b->ro + o_val), (const float *)b->input, (float *)b->out,
                                             rows);
