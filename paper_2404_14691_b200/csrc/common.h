@@ -77,7 +77,9 @@ struct Event {
   cudaEvent_t ev = nullptr;      // device event (null for host jobs)
   std::atomic<int> host_done{0}; // host job completion (FixedGSL)
   int64_t host_time = -1;        // host job completion time
-  bool recorded = false;
+  std::atomic<bool> recorded{false};
+  std::atomic<bool> pending{false}; // created for an invocation not yet issued (invoke.cu):
+                                    // queries report "not ready", waits block until recorded
   std::atomic<int> refs{1};      // handles naming this event (event_alias)
   std::atomic<bool> done{false}; // sticky completion (skips re-queries)
   int64_t t_cache = INT64_MIN;   // host-clock time once resolved
@@ -91,6 +93,9 @@ Event *event_get(sage_handle h);
 int event_record(Event *e, cudaStream_t s);
 int event_time_us(Event *e, int64_t *t);                    // requires completion
 int event_query(Event *e);                                  // SAGE_OK / SAGE_ENOTREADY
+// block until a pending event has been recorded by the issuer; ESTATE for an
+// event that was never recorded and is not pending
+int event_await_recorded(Event *e);
 
 // --------------------------------------------------------------- per GPU ----
 struct Layout;
@@ -189,8 +194,10 @@ int launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b);   // + live k
 // RETURN copy after `prev` (the boundary event just recorded on slot stream
 // s, or 0): on s, or -- a D2H (host_dst) with G->rets configured -- on a
 // return stream
+// pre_end (optional): a pre-created event to record as the END (the caller
+// gets an alias of it)
 int return_enqueue(Gpu *G, cudaStream_t s, sage_handle prev, uint64_t src, void *dst, uint64_t bytes,
-                   bool host_dst, sage_handle *begin_ev, sage_handle *end_ev);
+                   bool host_dst, sage_handle *begin_ev, sage_handle *end_ev, sage_handle pre_end = 0);
 int touch_all_kernels();
 // tcgen05 GEMM (gemm_tc.cu)
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
@@ -198,6 +205,12 @@ int touch_tc_kernels();
 
 // invocations (invoke.cu): stop the completion thread, drop live records
 void invoke_shutdown();
+// wait until the invocation issuer has enqueued everything submitted for
+// `gpu` (-1: every GPU)
+void issuer_drain(int gpu);
+
+// sage_segment_load with an optional pre-created END event (land.cu)
+int segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev, sage_handle pre_end);
 
 // layouts (land.cu)
 int layouts_destroy_all();

@@ -147,16 +147,24 @@ int event_alias(sage_handle src, sage_handle *out) {
 }
 int event_record(Event *e, cudaStream_t s) {
   SAGE_CUDA(cudaEventRecord(e->ev, s));
-  e->recorded = true;
   e->done.store(false, std::memory_order_relaxed);
   e->t_cache = INT64_MIN;
+  e->recorded.store(true, std::memory_order_release);
+  return SAGE_OK;
+}
+
+int event_await_recorded(Event *e) {
+  if (e->recorded.load(std::memory_order_acquire)) return SAGE_OK;
+  if (!e->pending.load(std::memory_order_acquire)) return fail(SAGE_ESTATE, "event was never recorded");
+  while (!e->recorded.load(std::memory_order_acquire)) std::this_thread::sleep_for(std::chrono::microseconds(10));
   return SAGE_OK;
 }
 
 int event_query(Event *e) {
   if (!e->ev) return e->host_done.load(std::memory_order_acquire) ? SAGE_OK : SAGE_ENOTREADY;
   if (e->done.load(std::memory_order_acquire)) return SAGE_OK;
-  if (!e->recorded) return fail(SAGE_ESTATE, "event was never recorded");
+  if (!e->recorded.load(std::memory_order_acquire))
+    return e->pending.load(std::memory_order_acquire) ? SAGE_ENOTREADY : fail(SAGE_ESTATE, "event was never recorded");
   cudaError_t r = cudaEventQuery(e->ev);
   if (r == cudaSuccess) {
     e->done.store(true, std::memory_order_release);
@@ -375,7 +383,7 @@ void stats_clear_gpu(Gpu *G) {
 }
 
 int return_enqueue(Gpu *G, cudaStream_t s, sage_handle prev, uint64_t src, void *dst, uint64_t bytes,
-                   bool host_dst, sage_handle *begin_ev, sage_handle *end_ev) {
+                   bool host_dst, sage_handle *begin_ev, sage_handle *end_ev, sage_handle pre_end) {
   if (bytes && (!dst || !src)) return fail(SAGE_EINVAL, "return: null buffer");
   Event *b, *e;
   std::unique_lock<std::mutex> lk(G->ret_mu, std::defer_lock);
@@ -396,7 +404,13 @@ int return_enqueue(Gpu *G, cudaStream_t s, sage_handle prev, uint64_t src, void 
   }
   // UVA: the destination is pinned host memory (D2H) or an HBM buffer (D2D)
   if (bytes) SAGE_CUDA(cudaMemcpyAsync(dst, (const void *)src, bytes, cudaMemcpyDefault, s));
-  SAGE_TRY(event_new(G->id, end_ev, &e));
+  if (pre_end) {
+    e = event_get(pre_end);
+    if (!e) return fail(SAGE_ESTATE, "return: unknown pre-created end event");
+    SAGE_TRY(event_alias(pre_end, end_ev));
+  } else {
+    SAGE_TRY(event_new(G->id, end_ev, &e));
+  }
   return event_record(e, s);
 }
 
@@ -537,7 +551,7 @@ int sage_event_sync(sage_handle h) {
     while (!e->host_done.load(std::memory_order_acquire)) std::this_thread::sleep_for(std::chrono::microseconds(50));
     return SAGE_OK;
   }
-  if (!e->recorded) return fail(SAGE_ESTATE, "event was never recorded");
+  SAGE_TRY(event_await_recorded(e));
   SAGE_CUDA(cudaEventSynchronize(e->ev));
   return SAGE_OK;
 }
@@ -641,7 +655,7 @@ int sage::wait_events(cudaStream_t s, const sage_handle *w, int n) {
       while (!e->host_done.load()) std::this_thread::sleep_for(std::chrono::microseconds(20));
       continue;
     }
-    if (!e->recorded) return fail(SAGE_ESTATE, "wait on an event that was never recorded");
+    SAGE_TRY(event_await_recorded(e));
     SAGE_CUDA(cudaStreamWaitEvent(s, e->ev, 0));
   }
   return SAGE_OK;
@@ -772,6 +786,7 @@ int sage_stats_get(int gpu, int kind, uint64_t *launches, double *total_us, uint
 int sage_device_sync(int gpu) {
   SAGE_TRY(require_up());
   if (!gpu_get(gpu)) return fail(SAGE_ENODEV, "device_sync: bad gpu");
+  issuer_drain(gpu);
   SAGE_CUDA(cudaSetDevice(dev_of(gpu)));
   SAGE_CUDA(cudaDeviceSynchronize());
   return SAGE_OK;

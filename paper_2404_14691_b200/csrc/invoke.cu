@@ -9,6 +9,25 @@
 // land / direct streams, joined by cudaStreamWaitEvent on their END events.
 // One call replaces ~6 ctypes round trips per invocation; one collect call
 // returns every stage time, byte count and checksum at completion.
+//
+// Issue order (the memory daemon's transfer scheduler).  All host->device
+// copies of a GPU execute in the order they were enqueued, whatever stream
+// they are on (one H2D copy-engine queue; tools/probe_ce.py).  Enqueued at
+// admission, a burst's large cold read-only loads therefore hold the PCIe
+// H2D direction for milliseconds while no invocation can compute and the
+// D2H direction idles.  sage_invoke hands the invocation to an issuer
+// thread instead.  The issuer keeps at most `lookahead` bytes of H2D queued
+// per GPU and, whenever there is room, enqueues the ready invocation (every
+// event it waits on already recorded) with the smallest H2D - D2H balance,
+// FIFO among equals, anything older than `max_defer` first.  Followers of a
+// landed segment (balance ~0: their return traffic overlaps the next loads)
+// thus run between the chunks of the next cold load.  The events handed back
+// are created at submit and recorded when the invocation is issued; waits on
+// them block until then.  Off the submitting thread, the ~30 us of CUDA
+// enqueue per invocation also overlaps the caller's admission work.
+//   SAGE_ISSUER=0              enqueue inline (admission order)
+//   SAGE_ISSUE_LOOKAHEAD_MB    H2D bytes kept queued per GPU (default 32)
+//   SAGE_ISSUE_MAX_DEFER_US    age that overrides the balance order (3000)
 #include "common.h"
 
 namespace sage {
@@ -19,7 +38,14 @@ struct Inv {
   sage_handle slot = 0;
   sage_handle ctx_b = 0, ctx_e = 0, sync_b = 0, sync_e = 0, comp_b = 0, comp_e = 0, ret_b = 0, ret_e = 0;
   sage_handle ro_load = 0, ro_end = 0, in_load = 0, in_end = 0;
+  // handed out at submit, recorded at issue: RO landed, context bound, done
+  sage_handle pre_ro = 0, pre_ctx = 0, pre_done = 0;
+  sage_handle hold[4] = {0, 0, 0, 0};   // retained wait events (released after issue)
+  sage_invoke_desc d{};                 // the submitted descriptor (waits -> hold)
   int64_t t_enqueue = 0;
+  int64_t h2d = 0, d2h = 0;             // PCIe bytes each way (issue order)
+  std::atomic<bool> issued{false};
+  std::string err;                      // issue failure (reported by collect)
   sage_invoke_info info{};
   std::atomic<int> resolved{0};   // 1: `info` computed by the completion thread, 2: done (lazy)
 };
@@ -47,6 +73,7 @@ std::deque<uint64_t> ready_q;      // resolved, not yet handed out
 }  // namespace
 
 static int resolve_info(Inv *I, sage_invoke_info *out);
+static void issuer_shutdown();
 
 static void CUDART_CB on_device_done(void *p) {
   {
@@ -95,6 +122,7 @@ static void collector_start() {
 }
 
 void invoke_shutdown() {
+  issuer_shutdown();   // enqueues everything still queued first
   {
     std::lock_guard<std::mutex> lk(done_mu);
     collector_stop = true;
@@ -132,7 +160,8 @@ static uint32_t load_flags(int kind) {
 
 static void inv_free(Inv *I) {
   for (sage_handle h : {I->ctx_b, I->ctx_e, I->sync_b, I->sync_e, I->comp_b, I->comp_e, I->ret_b, I->ret_e,
-                        I->ro_end, I->in_end})
+                        I->ro_end, I->in_end, I->pre_ro, I->pre_ctx, I->pre_done, I->hold[0], I->hold[1],
+                        I->hold[2], I->hold[3]})
     if (h) sage_event_release(h);
   if (I->ro_load) sage_load_release(I->ro_load);
   if (I->in_load) sage_load_release(I->in_load);
@@ -183,25 +212,42 @@ static int resolve_info(Inv *I, sage_invoke_info *out) {
   return SAGE_OK;
 }
 
-}  // namespace sage
+// ---------------------------------------------------------------- issue ----
+static bool pcie_kind(int k) { return k == SAGE_SRC_HOST || k == SAGE_SRC_PINNED; }
 
-using namespace sage;
-
-extern "C" {
-
-int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *done_ev, sage_handle *ro_end,
-                sage_handle *ctx_end) {
-  SAGE_TRY(require_up());
-  if (!d || !inv_out || !done_ev) return fail(SAGE_EINVAL, "invoke: null argument");
-  if (!gpu_get(d->gpu)) return fail(SAGE_ENODEV, "invoke: bad gpu");
-  auto *I = new Inv();
-  I->gpu = d->gpu;
-  I->id = g_inv_next++;
-  {
-    std::lock_guard<std::mutex> lk(g_inv_mu);
-    g_invs[I->id] = I;
+// submit side: retain the events the invocation waits on, create the events
+// handed back, and size its PCIe traffic
+static int submit_prepare(Inv *I) {
+  sage_invoke_desc &d = I->d;
+  for (int i = 0; i < d.n_wait; ++i) {
+    SAGE_TRY(event_alias(d.wait[i], &I->hold[i]));
+    d.wait[i] = I->hold[i];
   }
-  I->t_enqueue = host_now_us();
+  for (int i = 0; i < d.n_ro_wait; ++i) {
+    SAGE_TRY(event_alias(d.ro_wait[i], &I->hold[2 + i]));
+    d.ro_wait[i] = I->hold[2 + i];
+  }
+  Event *e;
+  SAGE_TRY(event_new(d.gpu, &I->pre_done, &e));
+  e->pending.store(true);
+  if (d.flags & SAGE_INV_RO) {
+    SAGE_TRY(event_new(d.gpu, &I->pre_ro, &e));
+    e->pending.store(true);
+  }
+  if (d.flags & SAGE_INV_CTX) {
+    SAGE_TRY(event_new(d.gpu, &I->pre_ctx, &e));
+    e->pending.store(true);
+  }
+  if ((d.flags & SAGE_INV_RO) && pcie_kind(d.ro_kind)) I->h2d += (int64_t)d.ro_src_bytes;
+  if ((d.flags & SAGE_INV_INPUT) && pcie_kind(d.in_kind)) I->h2d += (int64_t)d.in_bytes;
+  if (d.flags & SAGE_INV_RET_HOST) I->d2h = (int64_t)d.ret_bytes;
+  return SAGE_OK;
+}
+
+// enqueue the whole Parallel DAG of one invocation (admission order when
+// inline, the issuer's order otherwise)
+static int issue(Inv *I) {
+  const sage_invoke_desc *d = &I->d;
   int rc = sage_ctx_acquire(d->gpu, &I->slot);
   Gpu *G = nullptr;
   cudaStream_t s = nullptr;
@@ -214,6 +260,10 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
     SAGE_TRY(event_new(d->gpu, h, &e));
     return event_record(e, s);
   };
+  auto rec_pre = [&](sage_handle pre, sage_handle *h) -> int {
+    SAGE_TRY(event_alias(pre, h));
+    return event_record(event_get(pre), s);
+  };
   sage_handle last = 0;  // the boundary most recently recorded on s
   // GPU_CTX: bind the function context on the invocation's pooled stream
   // (zero its 64 KiB header: descriptor table, scratch counters)
@@ -223,7 +273,7 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
       cudaError_t e = cudaMemsetAsync((void *)d->ctx_dptr, 0, std::min<uint64_t>(d->ctx_bytes, 64 << 10), s);
       if (e != cudaSuccess) rc = cuda_fail(e, "ctx bind memset");
     }
-    if (rc == SAGE_OK) rc = rec(&I->ctx_e);
+    if (rc == SAGE_OK) rc = rec_pre(I->pre_ctx, &I->ctx_e);
     last = I->ctx_e;
   }
   // CPU_LOAD -> GPU_LOAD: the read-only segment ...
@@ -238,7 +288,7 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
     L.wait = d->ro_wait;
     L.n_wait = d->n_ro_wait;
     L.src_gpu = d->ro_src_gpu;
-    rc = sage_segment_load(&L, &I->ro_load, &I->ro_end);
+    rc = segment_load(&L, &I->ro_load, &I->ro_end, I->pre_ro);
   }
   // ... and the invocation input (identity layout)
   if (rc == SAGE_OK && (d->flags & SAGE_INV_INPUT)) {
@@ -248,7 +298,7 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
     L.dst = d->in_dst;
     L.src = d->in_src;
     L.src_bytes = d->in_bytes;
-    rc = sage_segment_load(&L, &I->in_load, &I->in_end);
+    rc = segment_load(&L, &I->in_load, &I->in_end, 0);
   }
   // the join before COMPUTE: loads ran on other streams
   sage_handle deps[6];
@@ -271,20 +321,238 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
   if (rc == SAGE_OK) rc = rec(&I->comp_e);
   // RETURN
   if (rc == SAGE_OK) rc = return_enqueue(G, s, I->comp_e, d->ret_src, d->ret_dst, d->ret_bytes,
-                                        (d->flags & SAGE_INV_RET_HOST) != 0, &I->ret_b, &I->ret_e);
+                                        (d->flags & SAGE_INV_RET_HOST) != 0, &I->ret_b, &I->ret_e, I->pre_done);
   if (rc == SAGE_OK) {
-    // completion notice: on the slot stream, after RETURN (which may have
-    // run on a return stream)
-    collector_start();
+    // the completion notice waits on RETURN (which may have run on a return
+    // stream); issue_notify launches it
     Event *re = event_get(I->ret_e);
     cudaError_t e = re ? cudaStreamWaitEvent(s, re->ev, 0) : cudaErrorInvalidResourceHandle;
-    if (e == cudaSuccess) e = cudaLaunchHostFunc(s, on_device_done, I);
-    if (e != cudaSuccess) rc = cuda_fail(e, "invoke completion notice");
+    if (e != cudaSuccess) rc = cuda_fail(e, "invoke completion wait");
   }
   if (rc != SAGE_OK) {
-    std::string msg = sage_last_error();
+    // waiters on this invocation's events must not hang: record whatever was
+    // handed out and never reached (followers then fail their own checks)
+    Gpu *H = G ? G : gpu_get(d->gpu);
     cudaSetDevice(dev_of(d->gpu));
+    for (sage_handle h : {I->pre_ro, I->pre_ctx, I->pre_done}) {
+      Event *e = h ? event_get(h) : nullptr;
+      if (e && !e->recorded.load() && H) event_record(e, H->aux);
+    }
     cudaDeviceSynchronize();  // error path only: nothing may still reference I
+  }
+  for (int i = 0; i < 4; ++i)
+    if (I->hold[i]) { sage_event_release(I->hold[i]); I->hold[i] = 0; }
+  I->issued.store(true, std::memory_order_release);
+  return rc;
+}
+
+// the device tells the completion thread when the invocation is done: a host
+// function on the slot stream.  The last touch of I by the issuing thread --
+// after this the caller may collect and release it at any time.
+static int issue_notify(Inv *I) {
+  Gpu *G;
+  cudaStream_t s;
+  SAGE_TRY(slot_stream(I->slot, &G, &s));
+  SAGE_CUDA(cudaLaunchHostFunc(s, on_device_done, I));
+  return SAGE_OK;
+}
+
+namespace {
+std::mutex iss_mu;
+std::condition_variable iss_cv;       // work arrived / stop
+std::condition_variable iss_idle_cv;  // something was issued
+std::deque<Inv *> iss_q;              // submitted, not yet issued (submit order)
+int iss_busy = 0;                     // being issued right now
+bool iss_stop = false;
+std::thread *issuer = nullptr;
+struct Flight { sage_handle ev; int64_t bytes; int gpu; };
+}  // namespace
+
+static bool env_flag(const char *name, bool dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) != 0 : dflt;
+}
+static int64_t env_i64(const char *name, int64_t dflt) {
+  const char *e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+static bool issuer_enabled() {
+  static const bool on = env_flag("SAGE_ISSUER", true);
+  return on;
+}
+
+static bool inv_ready(const Inv *I) {
+  for (sage_handle h : I->hold) {
+    if (!h) continue;
+    Event *e = event_get(h);
+    if (!e) continue;
+    if (e->ev ? !e->recorded.load(std::memory_order_acquire) : !e->host_done.load(std::memory_order_acquire))
+      return false;
+  }
+  return true;
+}
+
+// an invocation the issuer could not enqueue: complete it as failed
+static void complete_failed(Inv *I, int rc, const std::string &msg) {
+  for (int i = 0; i < 16; ++i) I->info.t[i] = -1;
+  I->info.status = rc;
+  I->err = msg;
+  I->resolved.store(1, std::memory_order_release);
+  {
+    std::lock_guard<std::mutex> lk(ready_mu);
+    ready_q.push_back(I->id);
+  }
+  ready_cv.notify_all();
+  fprintf(stderr, "sage: invocation %llu failed at issue: %s\n", (unsigned long long)I->id, msg.c_str());
+}
+
+static void issuer_main() {
+  const int64_t lookahead = env_i64("SAGE_ISSUE_LOOKAHEAD_MB", 32) << 20;
+  const int64_t max_defer = env_i64("SAGE_ISSUE_MAX_DEFER_US", 3000);
+  std::deque<Flight> flights;   // H2D queued by this thread, not yet landed
+  std::vector<int64_t> pending;
+  for (;;) {
+    // retire landed H2D (issuer-only state, no lock)
+    pending.assign(st.gpus.size() + 1, 0);
+    for (auto it = flights.begin(); it != flights.end();) {
+      if (sage_event_query(it->ev) != SAGE_ENOTREADY) {
+        sage_event_release(it->ev);
+        it = flights.erase(it);
+      } else {
+        pending[it->gpu] += it->bytes;
+        ++it;
+      }
+    }
+    Inv *pick = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(iss_mu);
+      if (iss_q.empty()) {
+        if (iss_stop) break;
+        if (flights.empty()) {
+          iss_cv.wait(lk, [] { return iss_stop || !iss_q.empty(); });
+          continue;
+        }
+        iss_cv.wait_for(lk, std::chrono::microseconds(50));
+        continue;
+      }
+      const int64_t now = host_now_us();
+      auto best = iss_q.end();
+      int64_t best_key = INT64_MAX;
+      for (auto it = iss_q.begin(); it != iss_q.end(); ++it) {
+        Inv *I = *it;
+        if (!inv_ready(I)) continue;
+        if (I->h2d > 0 && pending[I->gpu] > 0 && pending[I->gpu] >= lookahead) continue;   // PCIe queue full
+        if (now - I->t_enqueue >= max_defer) { best = it; break; }                         // overdue: FIFO
+        const int64_t key = I->h2d - I->d2h;
+        if (key < best_key) { best_key = key; best = it; }
+      }
+      if (best == iss_q.end()) {
+        iss_cv.wait_for(lk, std::chrono::microseconds(20));
+        continue;
+      }
+      pick = *best;
+      iss_q.erase(best);
+      ++iss_busy;
+    }
+    int rc = issue(pick);
+    if (rc == SAGE_OK && pick->h2d > 0) {
+      const sage_invoke_desc &d = pick->d;
+      if (pick->ro_end && (d.flags & SAGE_INV_RO) && pcie_kind(d.ro_kind)) {
+        Flight f{0, (int64_t)d.ro_src_bytes, pick->gpu};
+        if (event_alias(pick->ro_end, &f.ev) == SAGE_OK) flights.push_back(f);
+      }
+      if (pick->in_end && (d.flags & SAGE_INV_INPUT) && pcie_kind(d.in_kind)) {
+        Flight f{0, (int64_t)d.in_bytes, pick->gpu};
+        if (event_alias(pick->in_end, &f.ev) == SAGE_OK) flights.push_back(f);
+      }
+    }
+    if (rc == SAGE_OK) rc = issue_notify(pick);
+    if (rc != SAGE_OK) complete_failed(pick, rc, sage_last_error());   // (pick may be released from here on)
+    {
+      std::lock_guard<std::mutex> lk(iss_mu);
+      --iss_busy;
+    }
+    iss_idle_cv.notify_all();
+  }
+  for (auto &f : flights) sage_event_release(f.ev);
+}
+
+static void issuer_submit(Inv *I) {
+  {
+    std::lock_guard<std::mutex> lk(iss_mu);
+    if (!issuer) {
+      iss_stop = false;
+      issuer = new std::thread(issuer_main);
+    }
+    iss_q.push_back(I);
+  }
+  iss_cv.notify_one();
+}
+
+void issuer_drain(int gpu) {
+  std::unique_lock<std::mutex> lk(iss_mu);
+  iss_idle_cv.wait(lk, [gpu] {
+    if (iss_busy) return false;
+    for (Inv *I : iss_q)
+      if (gpu < 0 || I->gpu == gpu) return false;
+    return true;
+  });
+}
+
+static void issuer_shutdown() {
+  {
+    std::lock_guard<std::mutex> lk(iss_mu);
+    iss_stop = true;
+  }
+  iss_cv.notify_all();
+  if (issuer) {
+    issuer->join();
+    delete issuer;
+    issuer = nullptr;
+  }
+}
+
+}  // namespace sage
+
+using namespace sage;
+
+extern "C" {
+
+int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *done_ev, sage_handle *ro_end,
+                sage_handle *ctx_end) {
+  SAGE_TRY(require_up());
+  if (!d || !inv_out || !done_ev) return fail(SAGE_EINVAL, "invoke: null argument");
+  if (!gpu_get(d->gpu)) return fail(SAGE_ENODEV, "invoke: bad gpu");
+  if (d->n_wait < 0 || d->n_wait > 2 || d->n_ro_wait < 0 || d->n_ro_wait > 2)
+    return fail(SAGE_EINVAL, "invoke: at most two wait events per list");
+  auto *I = new Inv();
+  I->gpu = d->gpu;
+  I->id = g_inv_next++;
+  I->d = *d;
+  I->t_enqueue = host_now_us();
+  int rc = submit_prepare(I);
+  if (rc != SAGE_OK) {
+    std::string msg = sage_last_error();
+    inv_free(I);
+    return fail(rc, msg);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_inv_mu);
+    g_invs[I->id] = I;
+  }
+  *inv_out = make_handle(Kind::Inv, I->id);
+  *done_ev = I->pre_done;
+  if (ro_end) *ro_end = I->pre_ro;
+  if (ctx_end) *ctx_end = I->pre_ctx;
+  collector_start();
+  if (issuer_enabled()) {
+    issuer_submit(I);
+    return SAGE_OK;
+  }
+  rc = issue(I);
+  if (rc == SAGE_OK) rc = issue_notify(I);
+  if (rc != SAGE_OK) {
+    std::string msg = sage_last_error();
     {
       std::lock_guard<std::mutex> lk(g_inv_mu);
       g_invs.erase(I->id);
@@ -292,11 +560,6 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
     inv_free(I);
     return fail(rc, msg);
   }
-  const uint64_t id = I->id;
-  *inv_out = make_handle(Kind::Inv, id);
-  *done_ev = I->ret_e;
-  if (ro_end) *ro_end = I->ro_end;
-  if (ctx_end) *ctx_end = I->ctx_e;
   return SAGE_OK;
 }
 
@@ -305,8 +568,10 @@ int sage_invoke_collect(sage_handle h, sage_invoke_info *out) {
   if (!I || !out) return fail(SAGE_ESTATE, "invoke_collect: unknown invocation");
   if (I->resolved.load(std::memory_order_acquire) == 1) {
     *out = I->info;
+    if (I->info.status != SAGE_OK && !I->err.empty()) return fail(I->info.status, I->err);
     return I->info.status;
   }
+  if (!I->issued.load(std::memory_order_acquire) || !I->ret_e) return SAGE_ENOTREADY;
   int rc = sage_event_query(I->ret_e);
   if (rc != SAGE_OK) return rc;
   return resolve_info(I, out);
@@ -329,7 +594,8 @@ int sage_invoke_release(sage_handle h) {
   Inv *I = inv_get(h);
   if (I && !I->resolved.load(std::memory_order_acquire)) {
     // the completion thread still owns I: only a finished invocation may go
-    if (sage_event_query(I->ret_e) != SAGE_OK) return fail(SAGE_ESTATE, "invoke_release: still running");
+    if (!I->issued.load(std::memory_order_acquire) || !I->ret_e || sage_event_query(I->ret_e) != SAGE_OK)
+      return fail(SAGE_ESTATE, "invoke_release: still running");
     std::unique_lock<std::mutex> lk(ready_mu);
     ready_cv.wait(lk, [I] { return I->resolved.load(std::memory_order_acquire) != 0; });
   }

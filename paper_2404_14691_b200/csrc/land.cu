@@ -253,10 +253,31 @@ static int wait_list(cudaStream_t s, const sage_handle *w, int n) {
       while (!e->host_done.load()) std::this_thread::sleep_for(std::chrono::microseconds(20));
       continue;
     }
-    if (!e->recorded) return fail(SAGE_ESTATE, "load: wait on an unrecorded event");
+    SAGE_TRY(event_await_recorded(e));
     SAGE_CUDA(cudaStreamWaitEvent(s, e->ev, 0));
   }
   return SAGE_OK;
+}
+
+// SAGE_LAND_TMA=1 (opt-in): launches of >= 1 MiB take land_tma_kernel.  Off by
+// default: in the bench probe it measured 4.14 TB/s vs land_kernel's 4.80, and
+// its one 65 KB-smem CTA per SM keeps concurrent invocations' kernels off the
+// SMs (value leg 15.6k vs 20.4k inv/s; profiles/r1_land_tma_ab.txt)
+constexpr int kTmaSmem = kTmaStages * kTmaStageBytes + 128;
+static bool land_tma_enabled(int dev) {
+  static const bool env_on = [] {
+    const char *e = getenv("SAGE_LAND_TMA");
+    return e && atoi(e) != 0;
+  }();
+  static std::atomic<int> ok[64];   // per device: 0 unknown, 1 usable, -1 not
+  if (!env_on || dev < 0 || dev >= 64) return false;
+  int v = ok[dev].load(std::memory_order_acquire);
+  if (v == 0) {   // the smem opt-in is per device (current device = dev)
+    v = cudaFuncSetAttribute(land_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) == cudaSuccess
+            ? 1 : -1;
+    ok[dev].store(v, std::memory_order_release);
+  }
+  return v > 0;
 }
 
 static int enqueue_land(Gpu *G, const Plan &P, const ChunkPlan &C, int gpu, const uint8_t *slot,
@@ -274,7 +295,13 @@ static int enqueue_land(Gpu *G, const Plan &P, const ChunkPlan &C, int gpu, cons
   a.slot_bytes = C.se - C.sb;
   a.dst = dst;
   cudaEvent_t sb = stat_begin(G, G->land);
-  land_kernel<<<C.nvec ? land_grid(G, C.nvec) : 1, kLandThreads, 0, G->land>>>(a);
+  if (C.nvec >= kTmaMinVec && land_tma_enabled(G->dev)) {
+    const uint32_t units = (C.nvec + kTmaUnitVec - 1) / kTmaUnitVec;
+    const int grid = (int)std::min<uint32_t>(units, (uint32_t)G->sm_count);
+    land_tma_kernel<<<grid, kTmaThreads, kTmaSmem, G->land>>>(a);
+  } else {
+    land_kernel<<<C.nvec ? land_grid(G, C.nvec) : 1, kLandThreads, 0, G->land>>>(a);
+  }
   // algorithmic bytes: the packed bytes read + the segment vectors written
   stat_end(G, G->land, SAGE_KERNEL_LAND, sb, (C.se - C.sb) + 16ull * C.nvec);
   SAGE_CUDA(cudaGetLastError());
@@ -368,6 +395,12 @@ int sage_layout_chunks(sage_handle h, uint32_t *n) {
 }
 
 int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev) {
+  return segment_load(d, load_out, end_ev, 0);
+}
+
+}  // extern "C"
+
+int sage::segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev, sage_handle pre_end) {
   SAGE_TRY(require_up());
   if (!d || !load_out || !end_ev) return fail(SAGE_EINVAL, "segment_load: null argument");
   Gpu *G = gpu_get(d->gpu);
@@ -402,7 +435,14 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
   Event *Eb, *Ee;
   {
     int rc = event_new(d->gpu, &L->hb, &Eb);
-    if (rc == SAGE_OK) rc = event_new(d->gpu, &L->he, &Ee);
+    if (rc == SAGE_OK) {
+      if (pre_end) {   // the END event was handed out before this load was issued
+        Ee = event_get(pre_end);
+        rc = Ee ? event_alias(pre_end, &L->he) : fail(SAGE_ESTATE, "segment_load: unknown pre-created end event");
+      } else {
+        rc = event_new(d->gpu, &L->he, &Ee);
+      }
+    }
     if (rc != SAGE_OK) { delete L; return rc; }
   }
   L->ev_begin = Eb->ev;
@@ -522,6 +562,8 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
   *load_out = make_handle(Kind::Load, id);
   return SAGE_OK;
 }
+
+extern "C" {
 
 int sage_load_info_get(sage_handle h, sage_load_info *out) {
   if (handle_kind(h) != Kind::Load || !out) return fail(SAGE_EINVAL, "not a load handle");

@@ -227,6 +227,175 @@ __global__ void __launch_bounds__(kLandThreads, 4) land_kernel(const __grid_cons
   land_finalize(a);
 }
 
+// ------------------------------------------------------ TMA-staged land ------
+// Large launches: the source bytes move global -> shared with 1-D bulk copies
+// (cp.async.bulk, the copy engine inside the SM), kTmaStages deep per CTA, so
+// HBM sees ~64 KB in flight per SM without holding it in registers.  A unit is
+// kTmaUnitVec destination vectors.  Thread 0 maps a unit to its item; a unit
+// inside one data run gets one bulk copy of its (16-B aligned) source span,
+// the others take the per-vector path straight from global memory.  Consumers
+// funnel-shift out of shared memory, mask the tensor tail, store 16 B and
+// accumulate the checksum exactly as land_kernel does.
+constexpr int kTmaUnitVec = 1024;                       // 16 KB of segment per unit
+constexpr int kTmaStages = 4;
+constexpr int kTmaStageBytes = kTmaUnitVec * 16 + 32;   // + misalignment + the funnel's next vector
+constexpr int kTmaThreads = 256;
+constexpr uint32_t kTmaMinVec = 1u << 16;               // launches below 1 MiB use land_kernel
+
+__device__ __forceinline__ uint32_t land_smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void land_mbar_init(uint64_t *b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(land_smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void land_mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(land_smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void land_mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(land_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void land_mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAND_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAND_WAIT_%=;\n\t}" ::"r"(land_smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void land_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   land_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(land_smem_u32(bar))
+               : "memory");
+}
+
+struct TmaUnit {
+  uint32_t mode;   // 1: bulk-staged single run, 0: per-vector path
+  uint32_t it;     // item index (mode 1)
+  uint32_t loc0;   // first vector of the unit inside the item
+  uint32_t nv;     // vectors in the unit
+  uint32_t sh;     // source misalignment (bytes)
+  uint32_t nq;     // 16-B source vectors staged
+};
+
+// one destination vector from the per-vector path (item lookup by search)
+__device__ __forceinline__ unsigned long long land_one_vector(const LandArgs &a, uint32_t v, const uint8_t *slot_end) {
+  uint32_t lo = 0, hi = a.n_items;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a.prefix + mid) <= v) lo = mid; else hi = mid;
+  }
+  const LandItem I = a.items[lo];
+  const uint32_t loc = v - __ldg(a.prefix + lo);
+  const long long s = I.src_rel0 + 16ll * loc;
+  const long long d = I.data0 - 16ll * loc;
+  const unsigned long long dv = I.dst_vec0 + loc;
+  uint4 o = make_uint4(0, 0, 0, 0);
+  if (d > 0) {
+    const uint8_t *p = a.slot + s;
+    const uint4 *q = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 15);
+    uint4 A = __ldg(q), B = make_uint4(0, 0, 0, 0);
+    if (sh && reinterpret_cast<const uint8_t *>(q + 1) < slot_end) B = __ldg(q + 1);
+    o = sh ? funnel16(A, B, sh) : A;
+    if (d < 16) o = mask_tail(o, d);
+  }
+  reinterpret_cast<uint4 *>(a.dst)[dv] = o;
+  return vec_sum(o, dv * 2ull);
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) land_tma_kernel(const __grid_constant__ LandArgs a) {
+  extern __shared__ __align__(128) uint8_t land_sm_raw[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ TmaUnit meta[kTmaStages];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(land_sm_raw) + 127) & ~(uintptr_t)127);
+  const uint32_t units = (a.total_vec + kTmaUnitVec - 1) / kTmaUnitVec;
+  const uint8_t *slot_end = a.slot + a.slot_bytes;
+  const uintptr_t src_lim = (reinterpret_cast<uintptr_t>(slot_end) + 15) & ~(uintptr_t)15;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) land_mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // producer: map unit u to stage st and start its copy
+  auto stage_unit = [&](uint32_t u, int st) {
+    const uint32_t t0 = u * kTmaUnitVec;
+    const uint32_t tend = dmin<uint32_t>(t0 + kTmaUnitVec, a.total_vec);
+    uint32_t lo = 0, hi = a.n_items;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(a.prefix + mid) <= t0) lo = mid; else hi = mid;
+    }
+    TmaUnit m{0, lo, 0, tend - t0, 0, 0};
+    const uint32_t cur = __ldg(a.prefix + lo), nxt = __ldg(a.prefix + lo + 1);
+    const LandItem I = a.items[lo];
+    if (tend <= nxt && I.data0 > 0) {
+      m.loc0 = t0 - cur;
+      const uintptr_t src = reinterpret_cast<uintptr_t>(a.slot + I.src_rel0) + 16ull * m.loc0;
+      const uintptr_t q0 = src & ~(uintptr_t)15;
+      m.sh = (uint32_t)(src & 15);
+      uintptr_t qend = q0 + 16ull * m.nv + (m.sh ? 16 : 0);
+      if (qend > src_lim) qend = src_lim;
+      if (qend > q0) {
+        m.mode = 1;
+        m.nq = (uint32_t)((qend - q0) >> 4);
+        meta[st] = m;
+        land_mbar_expect_tx(&full[st], m.nq * 16u);
+        land_bulk_g2s(sm + st * kTmaStageBytes, reinterpret_cast<const void *>(q0), m.nq * 16u, &full[st]);
+        return;
+      }
+    }
+    meta[st] = m;
+    land_mbar_arrive(&full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kTmaStages; ++k)
+      if (blockIdx.x + (uint32_t)k * gridDim.x < units) stage_unit(blockIdx.x + k * gridDim.x, k);
+  unsigned long long acc = 0;
+  uint32_t k = 0;
+  for (uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+    const int st = (int)(k % kTmaStages);
+    land_mbar_wait(&full[st], (k / kTmaStages) & 1u);
+    const TmaUnit m = meta[st];
+    if (m.mode == 1) {
+      const LandItem I = a.items[m.it];
+      const uint4 *q = reinterpret_cast<const uint4 *>(sm + st * kTmaStageBytes);
+      uint4 *dbase = reinterpret_cast<uint4 *>(a.dst) + I.dst_vec0;
+      const long long d0 = I.data0;
+      const uint32_t nfull = (uint32_t)dmin<long long>(d0 >> 4, 0xFFFFFFFFll);
+      const uint32_t ndata = (uint32_t)dmin<long long>((d0 + 15) >> 4, 0xFFFFFFFFll);
+      const uint32_t bs = (m.sh & 3u) * 8u;
+#define LAND_TMA_BODY(SHIFT)                                                                 \
+      for (uint32_t v = threadIdx.x; v < m.nv; v += kTmaThreads) {                          \
+        const uint32_t loc = m.loc0 + v;                                                     \
+        uint4 o = q[v];                                                                      \
+        SHIFT                                                                                \
+        if (loc >= nfull) o = (loc < ndata) ? mask_tail(o, d0 - 16ll * loc) : make_uint4(0, 0, 0, 0); \
+        dbase[loc] = o;                                                                      \
+        acc += vec_sum(o, 2ull * (I.dst_vec0 + loc));                                        \
+      }
+#define LAND_TMA_WS(W) { const uint4 B = v + 1 < m.nq ? q[v + 1] : make_uint4(0, 0, 0, 0); o = funnel_ws<W>(o, B, bs); }
+      switch (m.sh == 0 ? -1 : (int)(m.sh >> 2)) {
+        case -1: LAND_TMA_BODY(;) break;
+        case 0: LAND_TMA_BODY(LAND_TMA_WS(0)) break;
+        case 1: LAND_TMA_BODY(LAND_TMA_WS(1)) break;
+        case 2: LAND_TMA_BODY(LAND_TMA_WS(2)) break;
+        default: LAND_TMA_BODY(LAND_TMA_WS(3)) break;
+      }
+#undef LAND_TMA_WS
+#undef LAND_TMA_BODY
+    } else {
+      const uint32_t t0 = u * kTmaUnitVec;
+      for (uint32_t v = threadIdx.x; v < m.nv; v += kTmaThreads) acc += land_one_vector(a, t0 + v, slot_end);
+    }
+    __syncthreads();   // stage st consumed by every thread
+    if (threadIdx.x == 0 && u + kTmaStages * gridDim.x < units) stage_unit(u + kTmaStages * gridDim.x, st);
+  }
+  block_reduce_add(acc, a.acc);
+  land_finalize(a);
+}
+
 // checksum of a landed segment (verify / dedup): one read-only pass
 __global__ void __launch_bounds__(256) checksum_kernel(const uint4 *__restrict__ p, unsigned long long nvec,
                                                        unsigned long long *out) {

@@ -379,7 +379,8 @@ int sage_pool_free(sage_handle h) {
 int sage_pool_free_after(sage_handle h, sage_handle evh) {
   if (handle_kind(h) != Kind::Alloc) return fail(SAGE_EINVAL, "not a pool handle");
   Event *E = event_get(evh);
-  if (!E || !E->ev || !E->recorded) return fail(SAGE_ESTATE, "free_after: unknown or unrecorded event");
+  if (!E || !E->ev) return fail(SAGE_ESTATE, "free_after: unknown event");
+  SAGE_TRY(event_await_recorded(E));
   Alloc *A = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_alloc_mu);

@@ -1,0 +1,117 @@
+"""The invocation issuer (csrc/invoke.cu) changes only WHEN an admitted
+invocation's DAG is enqueued, never what it computes.  The same cold cfg-2
+burst (scaled down), run once with the issuer off (enqueue at admission) and
+once on, must produce identical warmth classes, RO-load sources, landed
+checksums, input checksums and byte-identical results, each equal to the CPU
+oracle; followers must still compute only after their leader's segment landed.
+"""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+CHILD = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+from paper_2404_14691_b200 import device as D
+from paper_2404_14691_b200.functions import Stage
+from paper_2404_14691_b200.parboil import cfg2_functions
+from paper_2404_14691_b200.policies import policy_preset
+from paper_2404_14691_b200.runtime import ClusterSpec, Simulation
+table, data = cfg2_functions(scale=4)
+names = [sorted(table)[k % 3] for k in range(24)]
+sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=3, function_data=data)
+pls = []
+for n in names:
+    pb = D.PinnedBuffer(data[n].input_bytes)
+    pb.view()[:] = data[n].input
+    pls.append(pb)
+sim.dataplane.pin_host_store()
+out = []
+for rep in range(2):
+    for r in list(sim.sharing.residents.values()):
+        sim.sharing._evict(r)
+    invs = sim.submit_many(names, payloads=pls)
+    sim.drain()
+    land = {}
+    for i in invs:
+        if i.ro_landed_us is not None and i.warmth.label() != "Stage1Hot":
+            land[i.spec.name] = i.ro_landed_us
+    for i in invs:
+        assert i.outcome == "completed", i.fail_reason
+        c = i.stages[Stage.COMPUTE][0]
+        assert c >= land[i.spec.name], ("follower computed before its leader's RO landed", i.id)
+        out.append([i.spec.name, i.warmth.label(), i.ro_source, i.ro_checksum, i.input_checksum,
+                    hashlib.sha256(bytes(i.result)).hexdigest()])
+sim.dataplane.unpin_host_store()
+sim.close()
+print("RESULT " + json.dumps(out))
+"""
+
+
+def run_child(issuer: str):
+    env = dict(os.environ, SAGE_ISSUER=issuer)
+    res = subprocess.run([sys.executable, "-c", CHILD, str(ROOT)], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = [ln for ln in res.stdout.splitlines() if ln.startswith("RESULT ")][-1]
+    return json.loads(line[len("RESULT "):])
+
+
+def test_issuer_changes_order_not_results(built):
+    from conftest import gpu_available
+    if not gpu_available():
+        pytest.fail("gpu test run without a visible CUDA device")
+    off = run_child("0")
+    on = run_child("1")
+    assert len(off) == len(on) == 48
+    assert off == on
+
+
+def test_issuer_results_match_oracle(built):
+    """Every returned output equals the numpy body on the oracle-landed bytes
+    (one invocation per function, issuer on)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2404_14691_b200 import device as D
+    from paper_2404_14691_b200.parboil import cfg2_functions
+    from paper_2404_14691_b200.policies import policy_preset
+    from paper_2404_14691_b200.runtime import ClusterSpec, Simulation
+    from conftest import gpu_available
+    if not gpu_available():
+        pytest.fail("gpu test run without a visible CUDA device")
+    table, data = cfg2_functions(scale=8)
+    names = [sorted(table)[k % 3] for k in range(12)]
+    with Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=5, function_data=data) as sim:
+        invs = sim.submit_many(names)
+        sim.drain()
+        for i in invs:
+            fd = data[i.spec.name]
+            lay = fd.layout
+            seg, want_sum = O.land_c(fd.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+            assert i.ro_checksum is None or i.ro_checksum == want_sum
+            x = fd.input
+            if fd.body == "sgemm":
+                m, n, k = fd.args
+                want = O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(n, k).T)
+                got = i.result.view(np.float32).reshape(m, n)
+                np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
+            elif fd.body == "stencil":
+                nx, ny, nz, bits = fd.args
+                beta = float(np.int32(bits).view(np.float32))
+                want = O.stencil_ref(seg.view(np.float32)[:nx * ny * nz].reshape(nz, ny, nx),
+                                     x.view(np.float32).reshape(nz, ny, nx), beta)
+                np.testing.assert_allclose(i.result.view(np.float32).reshape(nz, ny, nx), want, rtol=1e-3, atol=1e-5)
+            else:
+                rows, nnz, o_rp, o_col, o_val = fd.args
+                want = O.spmv_ref(seg[o_rp:o_rp + 4 * (rows + 1)].view(np.int32),
+                                  seg[o_col:o_col + 4 * nnz].view(np.int32), seg[o_val:o_val + 4 * nnz].view(np.float32),
+                                  x.view(np.float32))
+                np.testing.assert_allclose(i.result.view(np.float32)[:rows], want, rtol=1e-3, atol=1e-4)
