@@ -141,3 +141,55 @@ def test_direct_path_identity_pinned(dp):
         seg.free()
         pb.free()
         junk.free()
+
+
+def test_two_gib_segment_full_size(dp):
+    """BASELINE cfg 4's largest read-only record (2048 MiB, 97 ragged tensors,
+    one misaligned every few bytes) at full size: the load's checksum, an
+    independent device re-checksum of the landed bytes and the C oracle agree
+    (bit-exact), across 256 staging chunks of the ring."""
+    total = 2048 << 20
+    rng = np.random.default_rng(2048)
+    cuts = np.unique(rng.integers(1, total, 96))   # (random_layout_sizes would materialise arange(total))
+    sizes = np.diff(np.concatenate([[0], cuts, [total]])).tolist()
+    lay = SegmentLayout.packed(sizes, align=256)
+    db = O.db_bytes(2048, lay.packed_bytes)
+    _, want = O.land_c(db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+    seg = D.pool_alloc(0, lay.seg_bytes, D._lib.CLASS_READ_ONLY)
+    try:
+        op = D.load(0, seg.dptr, db, lay)
+        res = op.wait()
+        op.release()
+        assert res.chunks >= 256
+        assert res.checksum == want
+        assert D.segment_checksum(0, seg.dptr, lay.seg_bytes) == want
+    finally:
+        seg.free()
+
+
+def test_stage2_cache_round_trip(dp):
+    """Stage1 -> Stage2 -> rejoin at full cfg-1 size (100 MiB): D2H of the
+    landed segment into a pinned cache, then an identity reload from that
+    cache into a fresh segment, is byte-identical (same checksum, same hash)."""
+    lay = SegmentLayout.packed(O.random_layout_sizes(5, 64, 100 << 20), align=256)
+    db = O.db_bytes(5, lay.packed_bytes)
+    want_seg, want = O.land_c(db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+    a = D.pool_alloc(0, lay.seg_bytes, D._lib.CLASS_READ_ONLY)
+    b = D.pool_alloc(0, lay.seg_bytes, D._lib.CLASS_READ_ONLY)
+    cache = D.PinnedBuffer(lay.seg_bytes)
+    try:
+        op = D.load(0, a.dptr, db, lay)
+        assert op.wait().checksum == want
+        ev = D.d2h(0, a.dptr, cache, lay.seg_bytes, wait=[op.end])
+        ev.sync()
+        op.release()
+        ev.release()
+        assert hashlib.sha256(cache.view()).digest() == hashlib.sha256(want_seg).digest()
+        re = D.load(0, b.dptr, cache, None)
+        assert re.wait().checksum == want
+        re.release()
+        assert hashlib.sha256(D.read_device(0, b.dptr, lay.seg_bytes)).digest() == hashlib.sha256(want_seg).digest()
+    finally:
+        cache.free()
+        a.free()
+        b.free()
