@@ -192,10 +192,18 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+", choices=sorted(RUNNERS))
     ap.add_argument("--out", default=None)
+    ap.add_argument("--rate", type=float, default=None, help="cfg3: Poisson rate (/s)")
+    ap.add_argument("--gpus", default=None, help="cfg3: comma-separated logical GPU counts")
     args = ap.parse_args(argv)
     for c in args.configs:
         t0 = time.perf_counter()
-        res = RUNNERS[c]()
+        kw = {}
+        if c == "cfg3":
+            if args.rate is not None:
+                kw["rate"] = args.rate
+            if args.gpus:
+                kw["gpus_list"] = tuple(int(g) for g in args.gpus.split(","))
+        res = RUNNERS[c](**kw)
         res["elapsed_s"] = round(time.perf_counter() - t0, 1)
         line = json.dumps({c: res})
         print(line, flush=True)

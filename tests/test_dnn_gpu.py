@@ -35,3 +35,37 @@ def test_resnet50_function_matches_torch(built):
             np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
     finally:
         sim.close()
+
+
+def test_resnet50_graph_replays_distinct_inputs(built):
+    """Ten concurrent invocations with ten different request payloads: the
+    captured CUDA graphs (4 per segment, reused round robin) must read each
+    invocation's own input and return its own logits."""
+    import torch
+    import torchvision
+    from paper_2404_14691_b200 import device as D
+    from paper_2404_14691_b200 import dnn
+    spec, data = dnn.resnet50(batch=8, seed=0)
+    rng = np.random.default_rng(7)
+    xs = [rng.standard_normal((8, 3, 224, 224), dtype=np.float32) for _ in range(10)]
+    pls = []
+    for x in xs:
+        pb = D.PinnedBuffer(x.nbytes)
+        pb.view()[:] = x.reshape(-1).view(np.uint8)
+        pls.append(pb)
+    sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), {spec.name: spec}, seed=1,
+                     function_data={spec.name: data})
+    try:
+        invs = sim.submit_many([spec.name] * 10, payloads=pls)
+        sim.drain()
+        torch.manual_seed(0)
+        ref = torchvision.models.resnet50(weights=None).eval().cuda()
+        for inv, x in zip(invs, xs):
+            with torch.inference_mode():
+                want = ref(torch.from_numpy(x).cuda()).float().cpu().numpy()
+            got = inv.result.view(np.float32).reshape(8, 1000)
+            np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
+    finally:
+        for pb in pls:           # before close(): shutdown frees every pinned buffer
+            pb.free()
+        sim.close()
