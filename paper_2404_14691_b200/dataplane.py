@@ -139,6 +139,44 @@ class _PinnedPool:
         self.free.clear()
 
 
+class _PlanFacts:
+    """What the one-call path needs to know about a plan, computed once per
+    plan object (plans are cached, functions.py:_plan_cached)."""
+
+    __slots__ = ("fast", "cpu_ctx", "gpu_ctx", "gpu_load_ro", "host_ro", "sync", "timed")
+
+    def __init__(self, plan: StagePlan):
+        stages = {n.stage for n in plan.nodes}
+        self.fast = Stage.CONTAINER not in stages and not (plan.mode is PlanMode.SERIAL and Stage.GPU_CTX in stages)
+        self.cpu_ctx = Stage.CPU_CTX in stages
+        self.gpu_ctx = Stage.GPU_CTX in stages
+        g = plan.node_index(Stage.GPU_LOAD)
+        self.gpu_load_ro = g is not None and plan.nodes[g].ro
+        c = plan.node_index(Stage.CPU_LOAD)
+        self.host_ro = c is not None and plan.nodes[c].ro
+        self.sync = bool(plan.wait_ro or plan.wait_ctx)
+        # stages whose device times sage_invoke reports: (index in _STAGES, stage)
+        self.timed = tuple((k, st) for k, st in enumerate(_STAGES)
+                           if st is not Stage.CPU_CTX and st in stages)
+
+
+def _plan_facts(plan: StagePlan) -> _PlanFacts:
+    pf = plan.__dict__.get("_facts")
+    if pf is None:
+        pf = plan.__dict__["_facts"] = _PlanFacts(plan)
+    return pf
+
+
+def _body_template(fd: "FunctionData") -> "_lib.BodyDesc":
+    """The function's COMPUTE descriptor without pointers, built once."""
+    b = fd.__dict__.get("_body_tmpl")
+    if b is None:
+        b = D.body_desc(_BODY[fd.body], ro_bytes=fd.layout.seg_bytes, inp_bytes=(fd.input_bytes + 15) // 16 * 16,
+                        out_bytes=max(16, fd.out_bytes), args=fd.args)
+        fd.__dict__["_body_tmpl"] = b
+    return b
+
+
 @dataclass
 class _Run:
     inv: object
@@ -215,9 +253,17 @@ class DataPlane:
         self.data: dict[str, FunctionData] = {}
         self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
         self._free_slots: dict[int, list] = {}
-        self._fast_cache: dict[int, bool] = {}
         self._fast = _FastCompletions(self)
+        self._scratch: dict[tuple[int, int], list] = {}
         self._fast_source = False
+
+    def _scratch_get(self, gpu: int, nbytes: int) -> D.Segment:
+        """Runtime scratch outside the ledger (results kept in HBM, inputs that
+        do not fit the writable allocation), reused by size."""
+        lst = self._scratch.get((gpu, nbytes))
+        if lst:
+            return lst.pop()
+        return D.pool_alloc(gpu, nbytes, _lib.CLASS_WRITABLE, unaccounted=True)
 
     def _slot(self, gpu: int) -> D.Slot:
         """A pooled stream of the pre-created context, kept acquired across invocations."""
@@ -343,37 +389,40 @@ class DataPlane:
     def _fast_ok(self, plan: StagePlan) -> bool:
         """Plans whose DAG is the Parallel shape (also Serial plans without a
         GPU_CTX node, e.g. DGSF's pre-created contexts): one sage_invoke call."""
-        ok = self._fast_cache.get(id(plan))
-        if ok is None:
-            stages = {n.stage for n in plan.nodes}
-            ok = Stage.CONTAINER not in stages and not (plan.mode is PlanMode.SERIAL and Stage.GPU_CTX in stages)
-            self._fast_cache[id(plan)] = ok
-        return ok
+        return _plan_facts(plan).fast
 
     def _enqueue_fast(self, run: _Run, fd: FunctionData, wait_tokens) -> None:
         inv, plan, gpu = run.inv, run.plan, run.gpu
+        pf = _plan_facts(plan)
         d = _lib.InvokeDesc()
         d.gpu = gpu
         flags = 0
-        stages = [n.stage for n in plan.nodes]
-        if Stage.CPU_CTX in stages:
+        if pf.cpu_ctx:
             t = self.sim.engine.tick()
             run.marks[Stage.CPU_CTX] = (t, t)     # host-side, synchronous
         in_dst, out_dst = self._input_dst(run, fd)
-        grant = getattr(inv, "grant", None)
+        grant = inv.grant
         resident = grant.resident if grant is not None else None
-        if Stage.GPU_CTX in stages:
+        if pf.gpu_ctx:
             flags |= _lib.INV_CTX
             d.ctx_dptr, d.ctx_bytes = self._ctx_dst(run)
-        gnode = plan.nodes[plan.node_index(Stage.GPU_LOAD)]
-        i_cpu = plan.node_index(Stage.CPU_LOAD)
-        host_ro = i_cpu is not None and plan.nodes[i_cpu].ro
-        if gnode.ro and fd.layout.seg_bytes:
+        ro = 0
+        if fd.layout.seg_bytes:
+            if resident is not None and resident.gpu_ro is not None:
+                ro = resident.gpu_ro.dptr
+            else:
+                try:
+                    ro = self._ro_dst(run)
+                except SimulationError:
+                    ro = 0
+        if pf.gpu_load_ro and fd.layout.seg_bytes:
+            if not ro:
+                raise SimulationError(f"{inv}: no read-only segment to land into")
             flags |= _lib.INV_RO
-            d.ro_dst = self._ro_dst(run)
+            d.ro_dst = ro
             cache = resident.cpu_ro_cache.segment if (resident is not None and resident.cpu_ro_cache is not None) else None
-            peer = self._peer_source(run) if host_ro else None
-            if not host_ro and isinstance(cache, D.PinnedBuffer):
+            peer = self._peer_source(run) if pf.host_ro else None
+            if not pf.host_ro and isinstance(cache, D.PinnedBuffer):
                 # Stage2 / Stage3 rejoin: the pinned cache holds the landed bytes
                 d.ro_kind, d.ro_src, d.ro_src_bytes = _lib.SRC_PINNED, cache.ptr, cache.nbytes
                 if resident.cache_event is not None:
@@ -400,7 +449,7 @@ class DataPlane:
         if fd.input_bytes:
             flags |= _lib.INV_INPUT
             d.in_dst, d.in_bytes = in_dst, fd.input_bytes
-            payload = getattr(inv, "payload", None)
+            payload = inv.payload
             if payload is None and fd.input_dev is not None:
                 d.in_kind, d.in_src = _lib.SRC_HBM, fd.input_dev.dptr
             else:
@@ -410,18 +459,22 @@ class DataPlane:
                 else:
                     d.in_kind, d.in_src = _lib.SRC_HOST, p.ctypes.data
                 run.keep = p
-        if plan.wait_ro or plan.wait_ctx:
+        if pf.sync:
             flags |= _lib.INV_SYNC
-            evs = [t.event.h for t in wait_tokens if not t.ready and t.event is not None][:2]
-            for k, h in enumerate(evs):
-                d.wait[k] = h
-            d.n_wait = len(evs)
-        d.flags = flags
-        d.body = self._body(run, fd, resident, in_dst, out_dst)
+            n = 0
+            for t in wait_tokens:
+                if n < 2 and not t.ready and t.event is not None:
+                    d.wait[n] = t.event.h
+                    n += 1
+            d.n_wait = n
+        # COMPUTE: the function's body template + this invocation's pointers
+        d.body = _body_template(fd)
+        body = d.body
+        body.ro, body.input, body.out = ro, in_dst, out_dst
         run.out_bytes = fd.out_bytes
         d.ret_src, d.ret_bytes = out_dst, fd.out_bytes
         if self.results_in_hbm:
-            seg = D.pool_alloc(gpu, max(256, fd.out_bytes), _lib.CLASS_WRITABLE, unaccounted=True)
+            seg = self._scratch_get(gpu, max(256, fd.out_bytes))
             run.scratch.append(seg)
             d.ret_dst = seg.dptr
         else:
@@ -434,12 +487,13 @@ class DataPlane:
                                           _lib.C.byref(ctx_end)), "sage_invoke")
         run.invh = h.value
         run.end = _Borrowed(done.value)
-        tok = run.hooks.get(Stage.GPU_LOAD)
-        if tok is not None:
-            tok.attach(_Borrowed(ro_end.value or done.value))
-        tok = run.hooks.get(Stage.GPU_CTX)
-        if tok is not None:
-            tok.attach(_Borrowed(ctx_end.value or done.value))
+        if run.hooks:
+            tok = run.hooks.get(Stage.GPU_LOAD)
+            if tok is not None:
+                tok.attach(_Borrowed(ro_end.value or done.value))
+            tok = run.hooks.get(Stage.GPU_CTX)
+            if tok is not None:
+                tok.attach(_Borrowed(ctx_end.value or done.value))
 
     def _collect_fast(self, run: _Run) -> None:
         inv = run.inv
@@ -447,25 +501,24 @@ class DataPlane:
         rc = _lib.check(_lib.lib().sage_invoke_collect(run.invh, _lib.C.byref(info)), "sage_invoke_collect")
         if rc == _lib.SAGE_ENOTREADY:
             raise SimulationError(f"{inv}: collected before completion")
-        eng = self.sim.engine
+        to_eng = self.sim.engine.to_engine_time
         t = info.t
-        for k, st in enumerate(_STAGES):
-            if st is Stage.CPU_CTX or t[2 * k] < 0:
-                continue
-            if run.plan.node_index(st) is None:
-                continue
-            inv.stages[st] = [eng.to_engine_time(t[2 * k]), eng.to_engine_time(t[2 * k + 1])]
+        stages = inv.stages
+        for k, st in _plan_facts(run.plan).timed:
+            if t[2 * k] >= 0:
+                stages[st] = [to_eng(t[2 * k]), to_eng(t[2 * k + 1])]
         for st, (b, e) in run.marks.items():
-            inv.stages[st] = [self._t(b), self._t(e)]
-        inv.measured["host_bytes"] = info.host_bytes
+            stages[st] = [self._t(b), self._t(e)]
+        m = inv.measured
+        m["host_bytes"] = info.host_bytes
         if run.ro_source == "nvlink":
-            inv.measured["nvlink_bytes"] = run.fd.layout.seg_bytes
-            inv.measured["pcie_bytes"] = info.link_bytes - run.fd.layout.seg_bytes
+            m["nvlink_bytes"] = run.fd.layout.seg_bytes
+            m["pcie_bytes"] = info.link_bytes - run.fd.layout.seg_bytes
         else:
-            inv.measured["pcie_bytes"] = info.link_bytes
+            m["pcie_bytes"] = info.link_bytes
         if info.ro_landed_us >= 0:
             self._verify_ro(run, info.ro_checksum)
-            inv.ro_landed_us = eng.to_engine_time(info.ro_landed_us)
+            inv.ro_landed_us = to_eng(info.ro_landed_us)
         if run.fd.input_bytes:
             inv.input_checksum = info.in_checksum
         inv.ro_source = run.ro_source
@@ -477,11 +530,13 @@ class DataPlane:
         unaccounted scratch segment when writable is too small."""
         inv = run.inv
         need = _a256(fd.input_bytes + 16) + _a256(fd.out_bytes)
-        wr = next((a for a in inv.allocations if a.cls is AllocClass.WRITABLE), None)
+        wr = inv.private.get(AllocClass.WRITABLE) if inv.private else None
+        if wr is None:
+            wr = next((a for a in inv.allocations if a.cls is AllocClass.WRITABLE), None)
         if wr is not None and wr.requested >= need and wr.dptr:
             base = wr.dptr
         else:
-            seg = D.pool_alloc(run.gpu, need, _lib.CLASS_WRITABLE, unaccounted=True)
+            seg = self._scratch_get(run.gpu, need)
             run.scratch.append(seg)
             base = seg.dptr
         return base, base + _a256(fd.input_bytes + 16)
@@ -815,8 +870,8 @@ class DataPlane:
         if run.result is not None:
             self.pinned.put(run.result)
             run.result = None
-        for s in run.scratch:
-            s.free()
+        for s in run.scratch:     # device work on them is complete: back to the pool
+            self._scratch.setdefault((s.gpu, s.nbytes), []).append(s)
         run.scratch.clear()
         if run.job is not None:
             run.job.release()
@@ -827,6 +882,10 @@ class DataPlane:
     def close(self) -> None:
         self.unpin_host_store()
         self.drop_hbm_sources()
+        for lst in self._scratch.values():
+            for seg in lst:
+                seg.free()
+        self._scratch.clear()
         for lst in self._free_slots.values():
             for s in lst:
                 s.release()

@@ -35,6 +35,8 @@ class EventKind(Enum):
     MEASUREMENT_TICK = "MeasurementTick"
     DEVICE_COMPLETE = "DeviceComplete"
 
+    __hash__ = object.__hash__   # members are singletons: identity hash (hot dict keys)
+
 
 def ms_to_us(ms: float) -> int:
     return int(round(ms * US_PER_MS))

@@ -34,6 +34,8 @@ class AllocClass(Enum):
     WRITABLE = 2
     INSTANCE_FIXED = 3
 
+    __hash__ = object.__hash__   # members are singletons: identity hash (hot dict keys)
+
 
 def round_up(size: int, granularity: int) -> int:
     """Least multiple of the granularity >= size (0 = exact)."""
