@@ -261,6 +261,18 @@ def sum_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
+def ro_checksums_agree(dist, data) -> bool:
+    """Every rank verified the same landed bytes for every function."""
+    import torch
+    mine = [data[n].ro_checksum or 0 for n in sorted(data)]
+    t = torch.tensor([c - (1 << 64) if c >= (1 << 63) else c for c in mine], dtype=torch.int64,
+                     device="cuda" if torch.cuda.is_available() else "cpu")
+    lo, hi = t.clone(), t.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    return bool(torch.equal(lo, hi))
+
+
 def load_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -352,6 +364,13 @@ def our_arm(args, rank, world, dist) -> dict:
     names = burst_names(table, args.burst)
     sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=1, function_data=data,
                      copy_results=False)
+    box = None
+    if world > 1 and not args.no_fanout:
+        # PCIe once per box: each function's home rank loads its segment over
+        # PCIe, the other ranks receive it by ncclBroadcast over NVLink
+        from paper_2404_14691_b200.fanout import BoxFanout
+        box = BoxFanout(rank, world, table)
+        sim.dataplane.box = box
     L = _lib.lib()
     try:
         _lib.check(L.sage_stats_enable(1), "stats_enable")
@@ -462,6 +481,12 @@ def our_arm(args, rank, world, dist) -> dict:
         "rooflines": rooflines,
         "kernels_e2e": stats_e2e,
         "gpu_launches": gpu_launches,
+        "fanout": None if box is None else {
+            "how": "home rank loads each RO segment over PCIe; ncclBroadcast to the other ranks, "
+                   "then land+checksum from HBM there (e2e / pageable legs)",
+            "homes": box.homes, "rank0": box.stats(),
+            "nvlink_bytes_in_all_ranks": int(sum_over_ranks(dist, box.bytes_in)),
+            "ro_checksums_agree": ro_checksums_agree(dist, data)},
         "clocks": clocks_val,
         "clocks_e2e": clocks_e2e,
     }
@@ -502,6 +527,7 @@ def main():
     ap.add_argument("--burst", type=int, default=64)
     ap.add_argument("--no-cfg1", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fanout", action="store_true", help="N>1: every rank loads its own segments over PCIe")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

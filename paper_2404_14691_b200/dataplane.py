@@ -255,6 +255,7 @@ class DataPlane:
         self._free_slots: dict[int, list] = {}
         self._fast = _FastCompletions(self)
         self._scratch: dict[tuple[int, int], list] = {}
+        self.box = None               # fanout.BoxFanout: PCIe once per box across processes
         self._fast_source = False
 
     def _scratch_get(self, gpu: int, nbytes: int) -> D.Segment:
@@ -406,6 +407,8 @@ class DataPlane:
         if pf.gpu_ctx:
             flags |= _lib.INV_CTX
             d.ctx_dptr, d.ctx_bytes = self._ctx_dst(run)
+        box = self.box
+        publish = False
         ro = 0
         if fd.layout.seg_bytes:
             if resident is not None and resident.gpu_ro is not None:
@@ -441,11 +444,24 @@ class DataPlane:
                 d.ro_kind, d.ro_layout = _lib.SRC_HBM, fd.layout.handle()
                 d.ro_src, d.ro_src_bytes = fd.db_dev.dptr, fd.layout.packed_bytes
                 run.ro_source = "hbm"
+            elif box is not None and grant is not None and grant.leader_ro and not box.is_home(inv.spec.name):
+                # PCIe once per box (multi-process): the segment arrives from its
+                # home rank over NVLink; GPU_LOAD lands (and verifies) it locally
+                nb = fd.layout.seg_bytes
+                buf = self._scratch_get(gpu, nb)
+                run.scratch.append(buf)
+                ev = box.receive(gpu, buf.dptr, nb, inv.spec.name)
+                run.events.append(ev)
+                d.ro_kind, d.ro_layout, d.ro_src, d.ro_src_bytes = _lib.SRC_HBM, 0, buf.dptr, nb
+                d.ro_wait[0] = ev.h
+                d.n_ro_wait = 1
+                run.ro_source = "nccl"
             else:
                 d.ro_kind = _lib.SRC_PINNED if fd.db_pinned else _lib.SRC_HOST
                 d.ro_layout = fd.layout.handle()
                 d.ro_src, d.ro_src_bytes = fd.db.ctypes.data, fd.layout.packed_bytes
                 run.ro_source = "pcie"
+                publish = box is not None and grant is not None and grant.leader_ro
         if fd.input_bytes:
             flags |= _lib.INV_INPUT
             d.in_dst, d.in_bytes = in_dst, fd.input_bytes
@@ -487,6 +503,13 @@ class DataPlane:
                                           _lib.C.byref(ctx_end)), "sage_invoke")
         run.invh = h.value
         run.end = _Borrowed(done.value)
+        if publish:
+            # home rank: send the landed segment to the other ranks; eviction
+            # waits for the send (sharing._evict)
+            ev = box.publish(gpu, ro, fd.layout.seg_bytes, _Borrowed(ro_end.value))
+            if resident.ro_busy is not None:
+                resident.ro_busy.release()
+            resident.ro_busy = ev
         if run.hooks:
             tok = run.hooks.get(Stage.GPU_LOAD)
             if tok is not None:
@@ -511,7 +534,10 @@ class DataPlane:
             stages[st] = [self._t(b), self._t(e)]
         m = inv.measured
         m["host_bytes"] = info.host_bytes
-        if run.ro_source == "nvlink":
+        if run.ro_source == "nccl":             # RO bytes came over NVLink, landed from HBM
+            m["nvlink_bytes"] = run.fd.layout.seg_bytes
+            m["pcie_bytes"] = info.link_bytes
+        elif run.ro_source == "nvlink":
             m["nvlink_bytes"] = run.fd.layout.seg_bytes
             m["pcie_bytes"] = info.link_bytes - run.fd.layout.seg_bytes
         else:
@@ -661,7 +687,7 @@ class DataPlane:
                     run.slot.wait(deps)
                     b = run.slot.record()
                     dnn.run_resnet50(fd, self._ro_dst(run), in_dst, out_dst, run.slot.stream(),
-                                     gpu % max(1, _lib.device_count()))
+                                     gpu % max(1, _lib.device_count()), plane=gpu)
                     e = run.slot.record()
                 else:
                     body = self._body(run, fd, resident, in_dst, out_dst)

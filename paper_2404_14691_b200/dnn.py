@@ -84,10 +84,11 @@ def view(ptr: int, nbytes: int, device):
     return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
 
 
-def _params(fd: FunctionData, ro_ptr: int, dev):
-    """Zero-copy parameter views over the landed segment (cached per segment)."""
+def _params(fd: FunctionData, ro_ptr: int, dev, plane: int):
+    """Zero-copy parameter views over the landed segment (cached per segment
+    and logical GPU -- several logical planes may share one device)."""
     import torch
-    key = (id(fd), ro_ptr, dev.index)
+    key = (id(fd), ro_ptr, plane)
     params = _PARAMS.get(key)
     if params is None:
         meta, lay = fd.meta, fd.layout
@@ -124,6 +125,7 @@ class _GraphPool:
 
 GRAPHS_PER_SEGMENT = 4
 _GRAPHS: dict = {}
+CAPTURES = {"count": 0, "seconds": 0.0}   # graph captures so far (reported by experiments.cfg3)
 
 
 def _graphs_enabled() -> bool:
@@ -150,7 +152,8 @@ def _capture(model, params, batch: int, dev, ext) -> _GraphEntry:
     return _GraphEntry(g, x, y)
 
 
-def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, stream_ptr: int, device_index: int) -> None:
+def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, stream_ptr: int, device_index: int,
+                 plane: int = 0) -> None:
     """Enqueue one ResNet-50 forward on the invocation's stream, reading the
     weights in place from the landed segment and writing logits to out.
 
@@ -160,7 +163,7 @@ def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, strea
     graphs.  SAGE_DNN_GRAPHS=0 runs the forward eagerly."""
     import torch
     dev = torch.device("cuda", device_index)
-    params = _params(fd, ro_ptr, dev)
+    params = _params(fd, ro_ptr, dev, plane)
     batch = fd.args[0]
     x = view(in_ptr, fd.input_bytes, dev).view(torch.float32).view(batch, 3, 224, 224)
     out = view(out_ptr, fd.out_bytes, dev).view(torch.float32).view(batch, 1000)
@@ -170,14 +173,18 @@ def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, strea
         with torch.cuda.stream(ext), torch.inference_mode():
             out.copy_(torch.func.functional_call(model, params, (x,)))
         return
-    key = (id(fd), ro_ptr, device_index)
+    key = (id(fd), ro_ptr, plane)
     pool = _GRAPHS.get(key)
     if pool is None:
         for k in [k for k in _GRAPHS if k[0] == key[0] and k[2] == key[2]]:
             del _GRAPHS[k]         # graphs over a segment that has gone
         pool = _GRAPHS[key] = _GraphPool()
     if len(pool.entries) < GRAPHS_PER_SEGMENT:
+        import time
+        t0 = time.perf_counter()
         pool.entries.append(_capture(model, params, batch, dev, ext))
+        CAPTURES["count"] += 1
+        CAPTURES["seconds"] += time.perf_counter() - t0
     entry = pool.entries[pool.next % len(pool.entries)]
     pool.next += 1
     with torch.cuda.stream(ext):

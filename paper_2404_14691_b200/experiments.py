@@ -90,6 +90,8 @@ def cfg3(rate: float = 300.0, duration_s: float = 4.0, gpus_list=(1, 2, 4), seed
                 if i.ro_source:
                     srcs[i.ro_source] = srcs.get(i.ro_source, 0) + 1
             s = summarize_setup(invs)
+            from . import dnn
+            s.update(graph_captures=dict(dnn.CAPTURES))
             s.update(gpus=g, throughput_per_s=len(invs) / wall, wall_s=wall, ro_loads=srcs,
                      pcie_ro_bytes=sum(i.measured["pcie_bytes"] for i in invs),
                      nvlink_bytes=sum(i.measured.get("nvlink_bytes", 0) for i in invs),

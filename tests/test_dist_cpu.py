@@ -30,7 +30,17 @@ def _worker(rank, world, port, q):
         bench.barrier(dist)
         mx = bench.max_over_ranks(dist, 10.0 + rank)          # per-rank elapsed µs
         sm = bench.sum_over_ranks(dist, 64.0)                 # per-rank invocations
-        q.put((r, w, local, os.environ.get("CUDA_VISIBLE_DEVICES"), mx, sm))
+        # box fan-out: every rank derives the same homes; the checksum check
+        # agrees when ranks landed identical bytes and not otherwise
+        from paper_2404_14691_b200.fanout import BoxFanout
+
+        class _FD:
+            def __init__(self, c):
+                self.ro_checksum = c
+        homes = BoxFanout(rank, world, ["spmv", "sgemm", "stencil"]).homes
+        same = bench.ro_checksums_agree(dist, {"a": _FD(0xFEDCBA9876543210), "b": _FD(7)})
+        differ = bench.ro_checksums_agree(dist, {"a": _FD(0xFEDCBA9876543210 + rank), "b": _FD(7)})
+        q.put((r, w, local, os.environ.get("CUDA_VISIBLE_DEVICES"), mx, sm, sorted(homes.items()), same, differ))
     finally:
         dist.destroy_process_group()
 
@@ -51,6 +61,8 @@ def test_two_rank_max_and_sum_over_gloo():
     assert [o[3] for o in out] == ["0", "1"]                  # one GPU per rank
     assert all(o[4] == 11.0 for o in out)                      # max over ranks
     assert all(o[5] == 128.0 for o in out)                     # whole-job invocations
+    assert out[0][6] == out[1][6] == [("sgemm", 0), ("spmv", 1), ("stencil", 0)]   # same homes on every rank
+    assert all(o[7] is True and o[8] is False for o in out)
 
 
 def test_weak_scaling_value_formula():
