@@ -197,6 +197,10 @@ class Simulation:
             fd = self.dataplane.data_for(self.spec_table[name])
             if fd.layout.n:
                 fd.layout.handle()
+            if fd.body == "resnet50":
+                from . import dnn
+                for dev in sorted({g % max(1, _lib.device_count()) for g in range(self.gpu_count)}):
+                    dnn.prewarm(fd, dev)
 
     # -- workload entry points ----------------------------------------------------------
     def submit(self, fn_name: str, arrival_us: Optional[int] = None, payload=None) -> Invocation:
