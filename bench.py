@@ -427,11 +427,21 @@ def our_arm(args, rank, world, dist) -> dict:
         avg_us = s["total_us"] / s["launches"]
         per_launch = s["work"] / s["launches"]
         if name == "sgemm":
+            # tcgen05 kind::tf32: dense TF32 rate is half the measured dense BF16 rate
+            tf32 = peaks["bf16_tflops"] / 2
             ach = per_launch / (avg_us * 1e-6) / 1e12
-            rooflines[name] = {"bound": "tensor", "achieved": round(ach, 2), "peak": peaks["bf16_tflops"],
-                               "unit": "TFLOP/s", "frac": round(ach / peaks["bf16_tflops"], 4),
+            rooflines[name] = {"bound": "tensor (tf32)", "achieved": round(ach, 2), "peak": round(tf32, 1),
+                               "unit": "TFLOP/s", "frac": round(ach / tf32, 4),
+                               "peak_source": "MEASURED_PEAKS bf16_tflops / 2 (TF32 MMA rate)",
                                "avg_launch_us": round(avg_us, 2), "launches": s["launches"],
                                "share_of_kernel_time": None}
+        elif name == "spmv":
+            ach = per_launch / (avg_us * 1e-6) / 1e9
+            rooflines[name] = {"bound": "l2 gather", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": round(ach / peaks["hbm_gbs"], 4), "avg_launch_us": round(avg_us, 2),
+                               "launches": s["launches"], "alg_bytes_per_launch": int(per_launch),
+                               "note": "one random 32-B L2 sector per non-zero for x (4 MiB, L2-resident): "
+                                       "L2 sector-rate bound, not HBM (DESIGN.md §3)"}
         else:
             ach = per_launch / (avg_us * 1e-6) / 1e9
             rooflines[name] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",

@@ -40,7 +40,7 @@ __global__ void copy_u4(const uint4 *__restrict__ s, uint4 *__restrict__ d, unsi
   for (; i < n; i += stride) d[i] = __ldg(s + i);
 }
 
-template <int U>
+template <int U, int CS = 0>
 __global__ void __launch_bounds__(256) sum_u(const uint4 *__restrict__ s, uint4 *__restrict__ d, unsigned long long n,
                                              unsigned long long *acc_out) {
   unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -49,9 +49,12 @@ __global__ void __launch_bounds__(256) sum_u(const uint4 *__restrict__ s, uint4 
   for (; i + (U - 1) * stride < n; i += U * stride) {
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldg(s + i + u * stride);
+    for (int u = 0; u < U; ++u) v[u] = CS & 2 ? __ldcs(s + i + u * stride) : __ldg(s + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < U; ++u) { d[i + u * stride] = v[u]; acc += vec_sum(v[u], 2 * (i + u * stride)); }
+    for (int u = 0; u < U; ++u) {
+      if (CS & 1) __stcs(d + i + u * stride, v[u]); else d[i + u * stride] = v[u];
+      acc += vec_sum(v[u], 2 * (i + u * stride));
+    }
   }
   for (; i < n; i += stride) { uint4 v = __ldg(s + i); d[i] = v; acc += vec_sum(v, 2 * i); }
   block_reduce_add(acc, acc_out);
@@ -207,6 +210,12 @@ int main(int argc, char **argv) {
     run("sum_u4", [&] { sum_u<4><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
     run("sum_u8", [&] { sum_u<8><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
     run("sum_u8_g8", [&] { sum_u<8><<<sm * 8, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
+    run("sum_u4_stcs", [&] { sum_u<4, 1><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
+    run("sum_u4_ldcs_stcs", [&] { sum_u<4, 3><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
+    run("sum_u8_stcs", [&] { sum_u<8, 1><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
+    run("sum_u8_ldcs", [&] { sum_u<8, 2><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
+    run("sum_u8_b2", [&] { sum_u<8><<<sm * 2, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
+    run("sum_u16_b4", [&] { sum_u<16><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
 #define TMA(ST, SB, BS, BPS)                                                                                   \
     {                                                                                                          \
       auto k = tma_land<ST, SB, BS>;                                                                           \
@@ -214,13 +223,6 @@ int main(int argc, char **argv) {
       run("tma_" #ST "x" #SB "_" #BS "_b" #BPS, [&] { k<<<sm * BPS, TB, ST * SB, st>>>(src, dst, S, acc); }, true, 20, F); \
     }
     TMA(4, 16384, false, 1)
-    TMA(6, 16384, false, 1)
-    TMA(4, 32768, false, 1)
-    TMA(3, 32768, false, 2)
-    TMA(6, 32768, false, 1)
-    TMA(4, 16384, true, 1)
-    TMA(6, 32768, true, 1)
-    TMA(3, 32768, true, 2)
   }
   return 0;
 }
