@@ -1,0 +1,7 @@
+#!/bin/bash
+# compute-sanitizer memcheck over the smoke path and the body / land parity tests
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+timeout 900 compute-sanitizer --tool memcheck --leak-check no --report-api-errors no --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/sanitize_smoke.log 2>&1; echo "smoke rc=$?"; tail -5 gpurun_out/sanitize_smoke.log
+timeout 1500 compute-sanitizer --tool memcheck --leak-check no --report-api-errors no --error-exitcode 9 python -m pytest tests/test_bodies_gpu.py tests/test_land_gpu.py -x -q -k "not two_gib and not hundred and not round_trip" > gpurun_out/sanitize_tests.log 2>&1; echo "tests rc=$?"; tail -5 gpurun_out/sanitize_tests.log
+SAGE_LAND_TMA=1 timeout 900 compute-sanitizer --tool memcheck --leak-check no --report-api-errors no --error-exitcode 9 python -m pytest tests/test_land_gpu.py -x -q -k "random_layouts or golden" > gpurun_out/sanitize_tma.log 2>&1; echo "tma rc=$?"; tail -5 gpurun_out/sanitize_tma.log
