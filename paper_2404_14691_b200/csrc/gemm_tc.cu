@@ -13,6 +13,12 @@
 //               tcgen05.mma (K = 8 each) per K-block, tcgen05.commit frees
 //               the smem slot; a final commit signals the epilogue
 //   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
+// Cluster variant (MC): CTAs that own vertically adjacent M tiles of the same
+// N tile and K range run as a 2-CTA cluster.  Each loads its own A block and
+// HALF of the shared B block, multicast by TMA into both CTAs' smem, so the
+// L2 -> SM traffic for B halves (this skinny GEMM re-reads B once per M
+// tile).  A slot is refilled only when BOTH CTAs' MMAs have read it: each
+// MMA thread commits to the slot's empty barrier in both CTAs (count 2).
 // Operands use the canonical K-major SWIZZLE_128B layout: 8-row x 128-B
 // core groups 1024 B apart (SBO = 64 x 16 B), start address advanced by
 // 32 B per K = 8 step inside the swizzle atom.
@@ -54,6 +60,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -81,7 +98,7 @@ __device__ __forceinline__ uint32_t tf32_idesc() {
          | ((uint32_t)(TC_BM >> 4) << 24);
 }
 
-template <int BN>
+template <int BN, bool MC = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
                       int M, int N, int K) {
@@ -102,6 +119,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int kblocks = K / TC_BK / gridDim.z;
   const int kb0 = blockIdx.z * kblocks;
   const bool split = gridDim.z > 1;
+  uint32_t crank = 0;
+  if constexpr (MC) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -111,7 +130,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       for (int s = 0; s < TC_STAGES; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], 1);
+        mbar_init(&empty[s], MC ? 2 : 1);   // MC: both CTAs' MMAs must release a slot
       }
       mbar_init(tmem_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -124,6 +143,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();   // the peer's barriers exist before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -135,7 +155,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&empty[s], (round & 1) ^ 1);
         mbar_expect_tx(&full[s], S::STAGE);
         tma_load_2d(sA + s * S::A_BYTES, &mapA, &full[s], (kb0 + kb) * TC_BK, m0);
-        tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], (kb0 + kb) * TC_BK, n0);
+        if constexpr (MC)   // this CTA's half of B, into both CTAs (same smem offset)
+          tma_load_2d_mc(sB + s * S::B_BYTES + crank * (S::B_BYTES / 2), &mapB, &full[s], (kb0 + kb) * TC_BK,
+                         n0 + (int)crank * (BN / 2), (uint16_t)0x3);
+        else
+          tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], (kb0 + kb) * TC_BK, n0);
       }
     }
   } else if (warp == 1) {
@@ -159,10 +183,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
               "l"(a), "l"(b), "r"(idesc), "r"(acc));
         }
-        // free the smem slot once these MMAs have read it
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&empty[s]))
-                     : "memory");
+        // free the smem slot once these MMAs have read it (MC: in both CTAs,
+        // whose producers both write into it)
+        if constexpr (MC)
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[s])),
+              "h"((uint16_t)0x3)
+              : "memory");
+        else
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[s]))
+                       : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(tmem_full))
@@ -213,6 +245,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
   }
+  // MC: the peer may still signal this CTA's empty barriers / land multicast
+  // bytes in its smem until it is done; neither CTA exits before both are
+  if constexpr (MC) cluster_sync_all();
 }
 
 // ------------------------------------------------------------------ host -----
@@ -238,25 +273,70 @@ static int encode_kmajor(CUtensorMap *map, const void *base, uint64_t rows, uint
   return SAGE_OK;
 }
 
+static int sm_count_of(int dev) {
+  static int counts[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (!counts[dev]) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    counts[dev] = n;
+  }
+  return counts[dev];
+}
+
+// SAGE_SGEMM_MC=1 (opt-in): 2-CTA clusters with B multicast.  Off by default:
+// on the cfg-2 shape (4096 x 256 x 4096) it measured 29.1 vs 27.1 us; ncu
+// shows both variants latency-bound (DRAM 37%, L2 34-36%, SM 32% of peak),
+// so halving B's L2 traffic buys nothing (profiles/r1_sgemm_mc_ab.txt)
+static bool sgemm_mc_enabled() {
+  static const bool on = [] { const char *e = getenv("SAGE_SGEMM_MC"); return e && atoi(e) != 0; }();
+  return on;
+}
+
+template <int BN, bool MC>
+static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float *C, int M, int N, int K, int split,
+                            cudaStream_t s) {
+  // the smem opt-in is per device and context (FixedGSL instances launch from
+  // fresh contexts): cheap, so set it on every launch
+  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TcSmem<BN>::TOTAL));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(N / BN, M / TC_BM, split);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = TcSmem<BN>::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (MC) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 2;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  SAGE_CUDA(cudaLaunchKernelEx(&cfg, sgemm_tf32_kernel<BN, MC>, ma, mb, C, M, N, K));
+  return SAGE_OK;
+}
+
 template <int BN>
 static int launch_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
+  // 2-CTA clusters along M when the M tiles pair up
+  const bool mc = sgemm_mc_enabled() && (M / TC_BM) % 2 == 0;
   CUtensorMap ma, mb;
   SAGE_TRY(encode_kmajor(&ma, A, (uint64_t)M, (uint64_t)K, TC_BM));
-  SAGE_TRY(encode_kmajor(&mb, BT, (uint64_t)N, (uint64_t)K, BN));
-  // per context (FixedGSL instances launch from fresh contexts)
-  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TcSmem<BN>::TOTAL));
+  SAGE_TRY(encode_kmajor(&mb, BT, (uint64_t)N, (uint64_t)K, mc ? BN / 2 : BN));
   // split K so the grid covers the SMs: a skinny GEMM (N <= 256) has only
   // M/128 full-width tiles; splitting K keeps every A element read once
-  int dev = 0, sms = 148;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count_of(dev);
   const int tiles = (N / BN) * (M / TC_BM), kblk = K / TC_BK;
   int split = 1;
   while (split * 2 * tiles <= sms && kblk % (split * 2) == 0 && kblk / (split * 2) >= 8) split *= 2;
   if (split > 1) SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
-  dim3 grid(N / BN, M / TC_BM, split);
-  sgemm_tf32_kernel<BN><<<grid, TC_THREADS, TcSmem<BN>::TOTAL, s>>>(ma, mb, C, M, N, K);
+  const int rc = mc ? launch_tc_kernel<BN, true>(ma, mb, C, M, N, K, split, s)
+                    : launch_tc_kernel<BN, false>(ma, mb, C, M, N, K, split, s);
+  if (rc != SAGE_OK) return rc;
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
 }
@@ -279,6 +359,9 @@ int touch_tc_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64>));
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128>));
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64, true>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, true>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, true>));
   return SAGE_OK;
 }
 
