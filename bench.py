@@ -56,18 +56,41 @@ def _rank_env():
 
 # --------------------------------------------------------------- clocks -------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled DURING a timed region: NVML polled
+    every 5 ms from a thread (the value leg lasts only tens of ms), else
+    `nvidia-smi -lms 100`."""
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, gpu: int = 0):
         self.gpu = gpu
         self.proc = None
         self.lines: list[str] = []
+        self.samples: list[tuple] = []
+        self._stop = threading.Event()
+        self._t = None
+        self._nvml = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._nvml = (pynvml, h, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self._nvml = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu),
+                                          "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                                          "clocks_event_reasons.hw_thermal_slowdown,"
+                                          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
@@ -76,35 +99,57 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h, _ = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), r))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 8:
-                continue
+        if self._nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+            nv, _, smax = self._nvml
+            for clk, r in self.samples:
+                sm.append(clk)
+                for name, attr in self.REASONS.items():
+                    if r & getattr(nv, attr, 0):
+                        reasons.add(name)
+            src = "nvml 5 ms"
+        elif self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(p[0]))
-                smax = float(p[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, p[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            for ln in self.lines:
+                p = [x.strip() for x in ln.split(",")]
+                if len(p) < 6:
+                    continue
+                try:
+                    sm.append(float(p[0]))
+                    smax = float(p[1])
+                except ValueError:
+                    continue
+                for n, v in zip(self.REASONS, p[2:6]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            src = "nvidia-smi 100 ms"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": src}
 
 
 # ------------------------------------------------------------- our arm --------
