@@ -283,6 +283,57 @@ def land_traffic(segment: str):
     return d["dram_bytes_read"] + d["dram_bytes_write"]
 
 
+def pcie_probe(gpu: int = 0, chunk_mib: int = 4, n: int = 48) -> dict:
+    """The PCIe ceiling for the e2e transfer mix, measured in the same run
+    (plumbing probe, torch copies from/to pinned memory): n x chunk H2D on one
+    stream alone, then concurrently with n x chunk D2H on another."""
+    import torch
+    c = chunk_mib << 20
+    h_in = torch.empty(n * c, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(n * c, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(n * c, dtype=torch.uint8, device=f"cuda:{gpu}")
+    d_out = torch.empty(n * c, dtype=torch.uint8, device=f"cuda:{gpu}")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(both: bool) -> tuple[float, float]:
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        s1.wait_event(e0)
+        s2.wait_event(e0)
+        with torch.cuda.stream(s1):
+            for k in range(n):
+                d_in[k * c:(k + 1) * c].copy_(h_in[k * c:(k + 1) * c], non_blocking=True)
+            e1.record()
+        with torch.cuda.stream(s2):
+            if both:
+                for k in range(n):
+                    h_out[k * c:(k + 1) * c].copy_(d_out[k * c:(k + 1) * c], non_blocking=True)
+            e2.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3, e0.elapsed_time(e2) / 1e3
+
+    run(False)
+    t_alone, _ = run(False)
+    t_h, t_d = run(True)
+    out = {"h2d_alone_GBps": round(n * c / t_alone / 1e9, 1),
+           "h2d_with_d2h_GBps": round(n * c / t_h / 1e9, 1), "d2h_with_h2d_GBps": round(n * c / t_d / 1e9, 1),
+           "how": f"{n} x {chunk_mib} MiB pinned copies per direction, torch, same process"}
+    del h_in, h_out, d_in, d_out
+    return out
+
+
+def e2e_floor_ms(h2d: int, d2h: int, p: dict) -> float:
+    """Fastest a step moving h2d / d2h bytes can be on this PCIe link: the
+    D2H runs at its duplex rate while H2D shares the link, the rest of the
+    H2D at the one-direction rate."""
+    hd, dd, ha = p["h2d_with_d2h_GBps"] * 1e9, p["d2h_with_h2d_GBps"] * 1e9, p["h2d_alone_GBps"] * 1e9
+    t_overlap = min(d2h / dd, h2d / hd)
+    h_rest = max(0.0, h2d - t_overlap * hd)
+    d_rest = max(0.0, d2h - t_overlap * dd)
+    return round((t_overlap + h_rest / ha + d_rest / dd) * 1e3, 3)
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -442,6 +493,7 @@ def our_arm(args, rank, world, dist) -> dict:
             pb.free()
         stats_e2e = kernel_stats()
         per_step = len(names)
+        pcie = pcie_probe(0)
         h2d = sum(i.measured.get("pcie_bytes", 0) for i in invs_e2e) / args.steps
         d2h = sum(data[n].out_bytes for n in names)
         setups_e2e = [i.setup_us for i in invs_e2e]
@@ -518,6 +570,11 @@ def our_arm(args, rank, world, dist) -> dict:
                 "setup_p50_ms": round(percentile(setups_e2e, 50) / 1e3, 3),
                 "setup_p99_ms": round(percentile(setups_e2e, 99) / 1e3, 3),
                 "h2d_GBps": round(h2d * args.steps / e2e_us / 1e3, 2),
+                "pcie_both_directions_GBps": round((h2d + d2h) * args.steps / e2e_us / 1e3, 2),
+                "roofline": {"bound": "pcie (duplex, this box)", "floor_ms_per_step": e2e_floor_ms(h2d, d2h, pcie),
+                             "ms_per_step": round(e2e_us / 1e3 / args.steps, 3),
+                             "frac": round(e2e_floor_ms(h2d, d2h, pcie) / (e2e_us / 1e3 / args.steps), 4),
+                             "probe": pcie},
                 "step_ms": e2e_steps,
                 "inputs": "request payloads in pinned host buffers; DB records in the pinned host store",
                 "pageable_db": {"value": round(total_inv / (pg_us / 1e6), 2), "unit": UNIT,
