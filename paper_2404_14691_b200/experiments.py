@@ -187,19 +187,99 @@ def cfg5(ns=(1, 2, 4, 8, 16, 32, 64, 128, 256, 512), reps: int = 3) -> dict:
     return out
 
 
-RUNNERS = {"cfg1": cfg1, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+def _workload(kind: str):
+    """(spec table, function data) of a named workload."""
+    if kind == "cfg3":
+        from .dnn import resnet50
+        spec, data = resnet50()
+        return {spec.name: spec}, {spec.name: data}
+    from .parboil import cfg2_functions
+    return cfg2_functions()
+
+
+def trace(path: str, workload: str = "cfg2", policy: str = "SAGE", time_scale: float = 1.0, seed: int = 1,
+          out_dir=None) -> dict:
+    """Replay a flat trace CSV (reference format) on the real plane and write
+    the reference's artifacts (summary.json, invocations.csv,
+    memory_timeline.csv) -- reference `gslsim run` with a trace workload."""
+    from . import reports
+    from .replay import TraceSpec, trace_arrivals
+    table, data = _workload(workload)
+    arrivals = trace_arrivals(TraceSpec(path, time_scale), known_functions=set(table))
+    sim = Simulation(ClusterSpec(gpus=1), policy_preset(policy), table, seed=seed, function_data=data,
+                     copy_results=False)
+    try:
+        sim.prepare()
+        tls = [reports.MemoryTimeline(g, l, lambda: sim.engine.now) for g, l in enumerate(sim.gpu_ledgers)]
+        src = OpenLoopSource(arrivals)
+        t0 = sim.engine.tick()
+        src.attach(sim)
+        sim.source = src
+        sim.drain()
+        duration = max(1, sim.engine.tick() - t0)
+        for tl in tls:
+            tl.close()
+        summary = reports.summarize(sim.invocations, duration, table, tls)
+        if out_dir:
+            reports.write_artifacts(out_dir, sim, duration, tls)
+        summary["workload"] = f"trace {path} ({len(arrivals)} arrivals, time scale {time_scale:g}) over {workload}"
+        return summary
+    finally:
+        sim.close()
+
+
+def peak(workload: str = "cfg2", probe_s: float = 2.0, rate_min: float = 50.0, rate_ceiling: float = 65536.0,
+         resolution: float = 0.05, seed: int = 1) -> dict:
+    """Largest stable Poisson rate of a workload on one B200 (reference
+    `gslsim peak`, experiments.py:128-155): doubling + bisection over
+    `probe_s`-second probes on one warm plane."""
+    from .replay import find_peak_throughput, run_probe
+    table, data = _workload(workload)
+    sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=seed, function_data=data,
+                     copy_results=False)
+    probes = []
+    try:
+        sim.prepare()
+        dur = int(probe_s * 1e6)
+
+        def probe(rate: float):
+            arr = generate_arrivals(PoissonOpenSpec(rate, probe_s, {n: 1.0 for n in table}), seed)
+            st = run_probe(sim, arr, dur)
+            probes.append({"rate_per_s": rate, "arrivals": len(arr), "queue_early": st.queue_early,
+                           "queue_end": st.queue_end, "p99_first_ms": st.p99_first_quartile_ms,
+                           "p99_last_ms": st.p99_last_quartile_ms})
+            return st
+
+        res = find_peak_throughput(probe, rate_min=rate_min, rate_ceiling=rate_ceiling, resolution=resolution)
+        return {"workload": f"{workload} Poisson probes of {probe_s:g} s, SAGE, 1 GPU",
+                "peak_rate_per_s": res.rate_per_s, "hit_ceiling": res.hit_ceiling, "diagnostic": res.diagnostic,
+                "trajectory": [[r, ok] for r, ok in res.trajectory], "probes": probes}
+    finally:
+        sim.close()
+
+
+RUNNERS = {"cfg1": cfg1, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5, "peak": peak}
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("configs", nargs="+", choices=sorted(RUNNERS))
+    ap.add_argument("configs", nargs="*", choices=sorted(RUNNERS))
     ap.add_argument("--out", default=None)
     ap.add_argument("--rate", type=float, default=None, help="cfg3: Poisson rate (/s)")
     ap.add_argument("--gpus", default=None, help="cfg3: comma-separated logical GPU counts")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"], help="peak / trace: function set")
+    ap.add_argument("--trace", default=None, help="trace: flat trace CSV (timestamp_ms,function)")
+    ap.add_argument("--time-scale", type=float, default=1.0)
     args = ap.parse_args(argv)
+    if args.trace:
+        res = trace(args.trace, args.workload, time_scale=args.time_scale, out_dir=args.out)
+        print(json.dumps({"trace": res}), flush=True)
+        return
     for c in args.configs:
         t0 = time.perf_counter()
         kw = {}
+        if c == "peak":
+            kw["workload"] = args.workload
         if c == "cfg3":
             if args.rate is not None:
                 kw["rate"] = args.rate

@@ -112,3 +112,4 @@ class OpenLoopSource:
         self._idx += 1
         self._schedule_next()
         self._sim.submit(self.arrivals[i].function, arrival_us=self._at(i))
+
