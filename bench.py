@@ -283,7 +283,7 @@ def land_traffic(segment: str):
     return d["dram_bytes_read"] + d["dram_bytes_write"]
 
 
-def pcie_probe(gpu: int = 0, chunk_mib: int = 4, n: int = 48) -> dict:
+def pcie_probe(gpu: int = 0, chunk_mib: int = 4, n: int = 64) -> dict:
     """The PCIe ceiling for the e2e transfer mix, measured in the same run
     (plumbing probe, torch copies from/to pinned memory): n x chunk H2D on one
     stream alone, then concurrently with n x chunk D2H on another."""
@@ -314,8 +314,10 @@ def pcie_probe(gpu: int = 0, chunk_mib: int = 4, n: int = 48) -> dict:
         return e0.elapsed_time(e1) / 1e3, e0.elapsed_time(e2) / 1e3
 
     run(False)
-    t_alone, _ = run(False)
-    t_h, t_d = run(True)
+    run(True)
+    t_alone = min(run(False)[0] for _ in range(3))     # best of 3: a ceiling
+    both = [run(True) for _ in range(3)]
+    t_h, t_d = min(b[0] for b in both), min(b[1] for b in both)
     out = {"h2d_alone_GBps": round(n * c / t_alone / 1e9, 1),
            "h2d_with_d2h_GBps": round(n * c / t_h / 1e9, 1), "d2h_with_h2d_GBps": round(n * c / t_d / 1e9, 1),
            "how": f"{n} x {chunk_mib} MiB pinned copies per direction, torch, same process"}
