@@ -250,8 +250,10 @@ def peak(workload: str = "cfg2", probe_s: float = 2.0, rate_min: float = 50.0, r
                            "p99_last_ms": st.p99_last_quartile_ms})
             return st
 
-        res = find_peak_throughput(probe, rate_min=rate_min, rate_ceiling=rate_ceiling, resolution=resolution)
+        res = find_peak_throughput(probe, rate_min=rate_min, rate_ceiling=rate_ceiling, resolution=resolution,
+                                   queue_slack=16, p99_slack_ms=5.0)
         return {"workload": f"{workload} Poisson probes of {probe_s:g} s, SAGE, 1 GPU",
+                "stability": "reference rule (replay.is_stable) + slack: backlog +16 invocations, p99 +5 ms",
                 "peak_rate_per_s": res.rate_per_s, "hit_ceiling": res.hit_ceiling, "diagnostic": res.diagnostic,
                 "trajectory": [[r, ok] for r, ok in res.trajectory], "probes": probes}
     finally:

@@ -113,17 +113,22 @@ class StabilityStats:
     completed_last_quartile: int
 
 
-def is_stable(s: StabilityStats, p99_growth_limit: float = 2.0) -> bool:
+def is_stable(s: StabilityStats, p99_growth_limit: float = 2.0, queue_slack: int = 0,
+              p99_slack_ms: float = 0.0) -> bool:
     """No backlog growth over the probe, and late arrivals' p99 latency within
     `p99_growth_limit` x that of early arrivals (idle probes are stable; a
-    probe that stopped completing is not)."""
-    grew = s.queue_end > s.queue_early
+    probe that stopped completing is not).  The slacks (0 = the reference's
+    rule) absorb the jitter of real hardware: a backlog of in-flight work that
+    wanders by a few invocations, millisecond-scale p99s that double by
+    chance."""
+    grew = s.queue_end > s.queue_early + queue_slack
     idle = s.completed_first_quartile == 0 and s.completed_last_quartile == 0
     if grew or (not idle and s.completed_last_quartile == 0):
         return False
     if idle or not s.p99_first_quartile_ms:
         return True
-    return s.p99_last_quartile_ms <= p99_growth_limit * s.p99_first_quartile_ms
+    return s.p99_last_quartile_ms <= max(p99_growth_limit * s.p99_first_quartile_ms,
+                                         s.p99_first_quartile_ms + p99_slack_ms)
 
 
 @dataclass
@@ -135,13 +140,14 @@ class PeakSearchResult:
 
 
 def find_peak_throughput(probe, *, rate_min: float = 0.5, rate_ceiling: float = 4096.0, resolution: float = 0.01,
-                         p99_growth_limit: float = 2.0) -> PeakSearchResult:
+                         p99_growth_limit: float = 2.0, queue_slack: int = 0, p99_slack_ms: float = 0.0
+                         ) -> PeakSearchResult:
     """Largest stable rate: probe rate_min, double until a probe is unstable
     (or the ceiling is stable), then bisect the bracket to `resolution`."""
     res = PeakSearchResult(0.0, False, [])
 
     def stable(rate: float) -> bool:
-        verdict = is_stable(probe(rate), p99_growth_limit)
+        verdict = is_stable(probe(rate), p99_growth_limit, queue_slack, p99_slack_ms)
         res.trajectory.append((rate, verdict))
         return verdict
 

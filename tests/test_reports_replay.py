@@ -153,3 +153,11 @@ def test_peak_search_floor_and_ceiling():
     assert res.rate_per_s == 0.0 and "minimum probe" in res.diagnostic
     res = find_peak_throughput(lambda r: _stats(), rate_min=1, rate_ceiling=64)
     assert res.hit_ceiling and res.rate_per_s == 64
+
+
+def test_stability_slack_absorbs_hardware_jitter():
+    jitter = _stats(queue_early=1, queue_end=2, p99_first=2.0, p99_last=4.5)
+    assert not is_stable(jitter)                                  # the reference rule
+    assert is_stable(jitter, queue_slack=4, p99_slack_ms=5.0)
+    overload = _stats(queue_early=60, queue_end=250, p99_first=50.0, p99_last=200.0)
+    assert not is_stable(overload, queue_slack=16, p99_slack_ms=5.0)
