@@ -30,7 +30,9 @@ namespace sage {
 
 constexpr int TC_BM = 128;        // UMMA M (rows of A / C per CTA)
 constexpr int TC_BK = 32;         // fp32 elements per K-block = 128 bytes
-constexpr int TC_STAGES = 4;
+// smem ring depth per N tile: as many 128-B K-blocks as fit in ~200 KB
+template <int BN>
+constexpr int tc_stages() { return BN >= 256 ? 4 : BN >= 128 ? 6 : 8; }
 constexpr int TC_THREADS = 192;
 
 template <int BN>
@@ -38,7 +40,8 @@ struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 4;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = TC_STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGES = tc_stages<BN>();
+  static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -103,6 +106,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
                       int M, int N, int K) {
   using S = TcSmem<BN>;
+  constexpr int TC_STAGES = S::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *sA = smem;                                  // STAGES x A_BYTES
@@ -349,6 +353,9 @@ int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cud
     return fail(SAGE_EINVAL, "sgemm (tcgen05): operands must be 16-byte aligned");
   // widest N tile that divides N: A (the shared weights, the dominant
   // operand of these skinny GEMMs) is then streamed through smem once
+  static const int force_bn = [] { const char *e = getenv("SAGE_SGEMM_BN"); return e ? atoi(e) : 0; }();
+  if (force_bn == 64) return launch_tc<64>(A, BT, C, M, N, K, s);       // diagnostics: tile sweep
+  if (force_bn == 128 && N % 128 == 0) return launch_tc<128>(A, BT, C, M, N, K, s);
   if (N % 256 == 0) return launch_tc<256>(A, BT, C, M, N, K, s);
   if (N % 128 == 0) return launch_tc<128>(A, BT, C, M, N, K, s);
   return launch_tc<64>(A, BT, C, M, N, K, s);
