@@ -155,35 +155,43 @@ def cfg4(rate: float = 10.0, duration_s: float = 6.0, seed: int = 1, include_fix
     return out
 
 
-def cfg5(ns=(1, 2, 4, 8, 16, 32, 64, 128, 256, 512), reps: int = 3) -> dict:
+def cfg5(ns=(1, 2, 4, 8, 16, 32, 64, 128, 256, 512), reps: int = 3, gpus_list=(1,)) -> dict:
+    """N simultaneous cold starts of one 100 MiB function on G GPUs: SAGE
+    (PCIe once per box + NVLink peer lands, shared) vs the host-only loading
+    path (SAGE-NR: every invocation lands its own copy over PCIe).  G > 1
+    runs logical GPUs on this pool's one device: placement, sharing and the
+    PCIe-once invariant are real, the NVLink bandwidth is not."""
     spec, data = synthetic_function("fn100", 100, 10, 1, tensors=64)
-    out = {"workload": "N simultaneous cold starts of one 100 MiB function on 1 GPU: SAGE (PCIe once, shared) vs "
-                       "host-only loading (SAGE-NR: every invocation lands its own copy)"}
-    for pol in ("SAGE", "SAGE_NR"):
-        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), {spec.name: spec}, seed=1,
-                         function_data={spec.name: data}, copy_results=False)
-        try:
-            sim.prepare()
-            _evict_all(sim)
-            sim.submit_many([spec.name] * 4)         # warm the process
-            sim.drain()
-            rows = {}
-            for n in ns:
-                setups, walls, pcie = [], [], 0
-                for _ in range(reps):
-                    _evict_all(sim)
-                    t0 = time.perf_counter()
-                    invs = sim.submit_many([spec.name] * n)
-                    sim.drain()
-                    walls.append(time.perf_counter() - t0)
-                    setups += [i.setup_us for i in invs]
-                    pcie = sum(i.measured["pcie_bytes"] for i in invs)
-                rows[str(n)] = {"setup_p50_ms": round(percentile(setups, 50) / 1e3, 3),
-                                "setup_p99_ms": round(percentile(setups, 99) / 1e3, 3),
-                                "burst_ms": round(1e3 * min(walls), 3), "pcie_bytes": pcie}
-            out[pol] = rows
-        finally:
-            sim.close()
+    out = {"workload": "N simultaneous cold starts of one 100 MiB function: SAGE (PCIe once, shared, NVLink "
+                       "fan-out) vs host-only loading (SAGE-NR: every invocation lands its own copy)"}
+    for g in gpus_list:
+        for pol in ("SAGE", "SAGE_NR"):
+            sim = Simulation(ClusterSpec(gpus=g), policy_preset(pol), {spec.name: spec}, seed=1,
+                             function_data={spec.name: data}, copy_results=False)
+            try:
+                sim.prepare()
+                _evict_all(sim)
+                sim.submit_many([spec.name] * 4 * g)         # warm the process
+                sim.drain()
+                rows = {}
+                for n in ns:
+                    setups, walls, pcie, nvl = [], [], 0, 0
+                    for _ in range(reps):
+                        _evict_all(sim)
+                        t0 = time.perf_counter()
+                        invs = sim.submit_many([spec.name] * n)
+                        sim.drain()
+                        walls.append(time.perf_counter() - t0)
+                        setups += [i.setup_us for i in invs]
+                        pcie = sum(i.measured["pcie_bytes"] for i in invs)
+                        nvl = sum(i.measured.get("nvlink_bytes", 0) for i in invs)
+                    rows[str(n)] = {"setup_p50_ms": round(percentile(setups, 50) / 1e3, 3),
+                                    "setup_p99_ms": round(percentile(setups, 99) / 1e3, 3),
+                                    "burst_ms": round(1e3 * min(walls), 3), "pcie_bytes": pcie,
+                                    "nvlink_bytes": nvl}
+                out[pol if g == 1 else f"{pol}_G{g}"] = rows
+            finally:
+                sim.close()
     return out
 
 
@@ -282,6 +290,8 @@ def main(argv=None):
         kw = {}
         if c == "peak":
             kw["workload"] = args.workload
+        if c == "cfg5" and args.gpus:
+            kw["gpus_list"] = tuple(int(g) for g in args.gpus.split(","))
         if c == "cfg3":
             if args.rate is not None:
                 kw["rate"] = args.rate
