@@ -28,6 +28,19 @@
 
 namespace sage {
 
+// phase timestamps per CTA (tools/gemm_phases.cu builds with SAGE_GEMM_TRACE)
+#ifdef SAGE_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[1024 * 12];
+__device__ __forceinline__ void gemm_mark(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (cta < 1024) g_gemm_trace[cta * 12 + slot] = t;
+}
+#else
+__device__ __forceinline__ void gemm_mark(int) {}
+#endif
+
 constexpr int TC_BM = 128;        // UMMA M (rows of A / C per CTA)
 constexpr int TC_BK = 32;         // fp32 elements per K-block = 128 bytes
 // smem ring depth per N tile: as many 128-B K-blocks as fit in ~200 KB
@@ -101,7 +114,7 @@ __device__ __forceinline__ uint32_t tf32_idesc() {
          | ((uint32_t)(TC_BM >> 4) << 24);
 }
 
-template <int BN, bool MC = false>
+template <int BN, bool MC = false, bool CR = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
                       int M, int N, int K) {
@@ -117,6 +130,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) gemm_mark(0);
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
   // split-K: CTA z covers K-blocks [z*kblocks, (z+1)*kblocks) and adds its
   // partial tile into C (zeroed by the host) with vector reductions
@@ -150,6 +164,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if constexpr (MC) cluster_sync_all();   // the peer's barriers exist before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) gemm_mark(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -173,6 +188,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % TC_STAGES, round = kb / TC_STAGES;
         mbar_wait(&full[s], round & 1);
+        if (kb == 0) gemm_mark(2);
+        if (kb == kblocks / 2) gemm_mark(3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint64_t da = kmajor_sw128_desc(smem_u32(sA + s * S::A_BYTES));
         const uint64_t db = kmajor_sw128_desc(smem_u32(sB + s * S::B_BYTES));
@@ -200,6 +217,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                            smem_u32(&empty[s]))
                        : "memory");
       }
+      gemm_mark(4);
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(tmem_full))
                    : "memory");
@@ -207,6 +225,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---- epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) ----
     mbar_wait(tmem_full, 0);
+    if (warp == 2 && lane == 0) gemm_mark(5);
+  }
+  if (warp >= 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int quad = warp & 3;
     const int row = m0 + quad * 32 + lane;
@@ -225,7 +246,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < M) {
+      if constexpr (CR) {
+        // split-K partial -> this CTA's smem (the drained operand ring),
+        // rows padded by 16 B so a warp's 16-B stores hit distinct banks
+        float4 *prow = reinterpret_cast<float4 *>(smem + (size_t)(quad * 32 + lane) * (BN * 4 + 16) + c * 4);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          prow[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+      } else if (row < M) {
         float4 *dst = reinterpret_cast<float4 *>(crow + c);
         if (split) {
 #pragma unroll
@@ -243,8 +272,60 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   }
+  if constexpr (CR) {
+    // split-K reduction over the cluster (the gridDim.z CTAs of one tile):
+    // CTA z sums rows [z*R, (z+1)*R) of every CTA's partial through DSMEM and
+    // stores them -- no atomics and no zeroed C (saves the memset launch;
+    // in-kernel it is ~1.5 us slower than red.add, profiles/r1_sgemm_mc_ab.txt)
+    if (threadIdx.x == 64) gemm_mark(7);
+    cluster_sync_all();    // every partial is in its CTA's smem
+    if (threadIdx.x == 64) gemm_mark(8);
+    if (warp >= 2) {
+      const int nz = (int)gridDim.z, rows = TC_BM / nz, t = threadIdx.x - 64;
+      const int r0 = (int)blockIdx.z * rows;
+      constexpr int U = 4;   // outputs per thread in flight, each summing up to 8 partials
+      for (int f0 = t; f0 < rows * (BN / 4); f0 += 128 * U) {
+        float4 acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= nz) break;
+          float4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {   // independent remote loads, issued back to back
+            const int f = f0 + u * 128;
+            const int row = r0 + f / (BN / 4), c4 = f % (BN / 4);
+            const uint32_t la = smem_u32(smem + (size_t)row * (BN * 4 + 16) + c4 * 16);
+            uint32_t ra;
+            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(q));
+            if (f < rows * (BN / 4))
+              asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                           : "r"(ra));
+            else
+              v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int f = f0 + u * 128;
+          const int row = r0 + f / (BN / 4), c4 = f % (BN / 4);
+          if (f < rows * (BN / 4) && m0 + row < M)
+            *reinterpret_cast<float4 *>(C + (size_t)(m0 + row) * N + n0 + 4 * c4) = acc[u];
+        }
+      }
+    }
+    if (threadIdx.x == 64) gemm_mark(9);
+    cluster_sync_all();   // peers are done reading this CTA's partial
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) gemm_mark(6);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
@@ -297,12 +378,12 @@ static bool sgemm_mc_enabled() {
   return on;
 }
 
-template <int BN, bool MC>
+template <int BN, bool MC, bool CR = false>
 static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float *C, int M, int N, int K, int split,
                             cudaStream_t s) {
   // the smem opt-in is per device and context (FixedGSL instances launch from
   // fresh contexts): cheap, so set it on every launch
-  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN, MC, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  TcSmem<BN>::TOTAL));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(N / BN, M / TC_BM, split);
@@ -310,15 +391,15 @@ static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float 
   cfg.dynamicSmemBytes = TcSmem<BN>::TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  if (MC) {
+  if (MC || CR) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 2;
-    attr[0].val.clusterDim.z = 1;
+    attr[0].val.clusterDim.y = MC ? 2 : 1;
+    attr[0].val.clusterDim.z = CR ? split : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  SAGE_CUDA(cudaLaunchKernelEx(&cfg, sgemm_tf32_kernel<BN, MC>, ma, mb, C, M, N, K));
+  SAGE_CUDA(cudaLaunchKernelEx(&cfg, sgemm_tf32_kernel<BN, MC, CR>, ma, mb, C, M, N, K));
   return SAGE_OK;
 }
 
@@ -337,9 +418,14 @@ static int launch_tc(const float *A, const float *BT, float *C, int M, int N, in
   const int tiles = (N / BN) * (M / TC_BM), kblk = K / TC_BK;
   int split = 1;
   while (split * 2 * tiles <= sms && kblk % (split * 2) == 0 && kblk / (split * 2) >= 8) split *= 2;
-  if (split > 1) SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+  // split-K partials are reduced inside the cluster of the split CTAs (DSMEM)
+  // unless disabled (SAGE_SGEMM_CR=0) or B-multicast clusters are requested
+  static const bool cr_on = [] { const char *e = getenv("SAGE_SGEMM_CR"); return !(e && atoi(e) == 0); }();
+  const bool cr = cr_on && !mc && split > 1 && split <= 8 && TC_BM % split == 0;
+  if (split > 1 && !cr) SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
   const int rc = mc ? launch_tc_kernel<BN, true>(ma, mb, C, M, N, K, split, s)
-                    : launch_tc_kernel<BN, false>(ma, mb, C, M, N, K, split, s);
+                 : cr ? launch_tc_kernel<BN, false, true>(ma, mb, C, M, N, K, split, s)
+                      : launch_tc_kernel<BN, false>(ma, mb, C, M, N, K, split, s);
   if (rc != SAGE_OK) return rc;
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
@@ -369,6 +455,9 @@ int touch_tc_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64, true>));
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, true>));
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, true>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64, false, true>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, false, true>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, true>));
   return SAGE_OK;
 }
 
