@@ -271,6 +271,33 @@ def d2d_reference(dst: int, src: int, nbytes: int, iters: int = 20) -> float:
     return round(2 * nbytes * iters / us.value / 1e3, 1)
 
 
+_TRAFFIC = {"spmv": "r1_spmv_traffic.json", "land": "r1_land_traffic.json"}
+
+
+def dominant_roofline(rooflines: dict, stats: dict, peaks: dict) -> dict:
+    """`roofline` of the bench contract: the kernel with the largest summed
+    device time over the timed region, its achieved rate = algorithmic work
+    per launch / mean launch time (CUDA events around every launch on the
+    launching stream), DRAM traffic per launch from its committed ncu
+    --set full capture when there is one."""
+    name = max(stats, key=lambda k: stats[k]["total_us"])
+    r = dict(rooflines[name])
+    r["kernel"] = name
+    if r["bound"] not in ("hbm", "tensor"):     # contract vocabulary; the real limiter stays recorded
+        r["limiter"] = r["bound"]
+        r["bound"] = "tensor" if r["unit"] == "TFLOP/s" else "hbm"
+    r["how"] = (f"{r['launches']} launches inside the timed value leg, CUDA events on each launch's stream; "
+                f"launches overlap other invocations' kernels, so per-launch times include contention")
+    r["peak_source"] = peaks["source"]
+    r["traffic"] = None
+    f = ROOT / "profiles" / _TRAFFIC.get(name, "-")
+    if f.exists():
+        d = json.loads(f.read_text())
+        r["traffic"] = d["dram_bytes_read"] + d["dram_bytes_write"]
+        r["traffic_source"] = f"profiles/{f.name} (ncu --set full, one launch)"
+    return r
+
+
 def land_traffic(segment: str):
     """DRAM bytes per launch of the probe's land from the committed ncu --set
     full capture (profiles/r1_land_traffic.json), if it is the same segment."""
@@ -584,14 +611,19 @@ def our_arm(args, rank, world, dist) -> dict:
                                 "setup_p50_ms": round(percentile([i.setup_us for i in invs_pg], 50) / 1e3, 3),
                                 "setup_p99_ms": round(percentile([i.setup_us for i in invs_pg], 99) / 1e3, 3),
                                 "note": "DB records pageable: cold loads include the CPU_LOAD memcpy"}},
-        "roofline": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": land["frac"], "traffic": land_traffic(probe["segment"]),
-                     "traffic_source": "profiles/r1_land_traffic.json (ncu --set full, one launch)",
-                     "peak_source": peaks["source"], "same_size_d2d_GBps": probe["d2d_GBps"],
-                     "frac_of_same_size_d2d": round(land["achieved"] / probe["d2d_GBps"], 4),
-                     "avg_launch_us": land["avg_launch_us"], "alg_bytes_per_launch": land["alg_bytes_per_launch"],
-                     "launches": land["launches"], "how": f"{land['launches']} back-to-back HBM-resident lands of "
-                                                           f"{land['segment']}, CUDA events on the land stream"},
+        # the contract's roofline: the kernel with the largest share of device
+        # time in the timed value leg, timed there with CUDA events on its own
+        # stream; the data plane's own kernel (land) is reported beside it
+        "roofline": dominant_roofline(rooflines, stats_val, peaks),
+        "roofline_land": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
+                          "unit": "GB/s", "frac": land["frac"], "traffic": land_traffic(probe["segment"]),
+                          "traffic_source": "profiles/r1_land_traffic.json (ncu --set full, one launch)",
+                          "peak_source": peaks["source"], "same_size_d2d_GBps": probe["d2d_GBps"],
+                          "frac_of_same_size_d2d": round(land["achieved"] / probe["d2d_GBps"], 4),
+                          "avg_launch_us": land["avg_launch_us"], "alg_bytes_per_launch": land["alg_bytes_per_launch"],
+                          "launches": land["launches"],
+                          "how": f"{land['launches']} back-to-back HBM-resident lands of {land['segment']}, CUDA "
+                                 f"events on the land stream (in-burst launches: rooflines.land)"},
         "rooflines": rooflines,
         "kernels_e2e": stats_e2e,
         "gpu_launches": gpu_launches,

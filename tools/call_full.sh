@@ -13,7 +13,8 @@ import json
 d=json.load(open('gpurun_out/bench.json'))
 print('value', d['value'], 'ms', d['ms_per_step'], 'setup', d['setup_p50_ms'], d['setup_p99_ms'], 'launches', d['gpu_launches'])
 e=d['e2e']; print('e2e', e['value'], e['ms_per_step'], e['setup_p50_ms'], e['setup_p99_ms'], 'pg', e['pageable_db']['value'])
-print('roofline', {k: d['roofline'][k] for k in ('achieved','frac','traffic','same_size_d2d_GBps','frac_of_same_size_d2d')})
+print('roofline', {k: d['roofline'].get(k) for k in ('kernel','achieved','frac','traffic','limiter')})
+print('roofline_land', {k: d['roofline_land'][k] for k in ('achieved','frac','traffic','same_size_d2d_GBps','frac_of_same_size_d2d')})
 print('cfg1', d.get('cfg1_sage_vs_fixedgsl', {}).get('p50_setup_ratio_fixedgsl_over_sage'), 'cpu', d.get('cpu_baseline'))
 print(open('gpurun_out/bench_ref.json').read())
 PY
