@@ -92,6 +92,14 @@ int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total,
  * SAGE_INIT_PEER_ACCESS is set; this returns the (shared) VA               */
 int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes);
 
+/* ---- cross-process sharing (the paper's memory daemon -> function engines,
+ * PAPER.md:279-281, 358-379): a segment's physical pages
+ * leave as a POSIX file descriptor (pass it over a Unix socket, SCM_RIGHTS)
+ * and are mapped zero-copy into another process on the same GPU.           */
+int sage_pool_export(sage_handle h, int *fd, uint64_t *phys_bytes);
+int sage_segment_import(int gpu, int fd, uint64_t phys_bytes, sage_handle *h, uint64_t *dptr);
+int sage_segment_unimport(sage_handle h);
+
 /* ---- pinned host buffers (the Stage-2 CPU read-only cache, sharing.py:226-228) */
 int sage_host_alloc(uint64_t bytes, sage_handle *h, void **ptr);
 int sage_host_free(sage_handle h);

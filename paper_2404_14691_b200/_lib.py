@@ -128,6 +128,9 @@ _SIGS = {
     "sage_segment_checksum": (C.c_int, [C.c_int, u64, u64, C.POINTER(u64)]),
     "sage_d2h_cache": (C.c_int, [C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
     "sage_fanout": (C.c_int, [C.c_int, u64, C.c_int, u64, u64, C.POINTER(H), C.c_int, C.POINTER(H)]),
+    "sage_pool_export": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(u64)]),
+    "sage_segment_import": (C.c_int, [C.c_int, C.c_int, u64, C.POINTER(H), C.POINTER(u64)]),
+    "sage_segment_unimport": (C.c_int, [H]),
     "sage_launch": (C.c_int, [H, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_launch_after": (C.c_int, [H, C.POINTER(H), C.c_int, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_return_after": (C.c_int, [H, C.POINTER(H), C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),

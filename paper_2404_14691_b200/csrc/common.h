@@ -59,6 +59,8 @@ struct Driver {
   PFN_cuCtxSetCurrent_v4000 CtxSetCurrent = nullptr;
   PFN_cuCtxGetCurrent_v4000 CtxGetCurrent = nullptr;
   PFN_cuDevicePrimaryCtxRetain_v7000 DevicePrimaryCtxRetain = nullptr;
+  PFN_cuMemExportToShareableHandle_v10020 MemExportToShareableHandle = nullptr;
+  PFN_cuMemImportFromShareableHandle_v10020 MemImportFromShareableHandle = nullptr;
 };
 extern Driver drv;
 int load_driver();

@@ -67,6 +67,8 @@ int load_driver() {
   SAGE_TRY(get_entry("cuCtxSetCurrent", &drv.CtxSetCurrent, 4000));
   SAGE_TRY(get_entry("cuCtxGetCurrent", &drv.CtxGetCurrent, 4000));
   SAGE_TRY(get_entry("cuDevicePrimaryCtxRetain", &drv.DevicePrimaryCtxRetain, 7000));
+  SAGE_TRY(get_entry("cuMemExportToShareableHandle", &drv.MemExportToShareableHandle, 10020));
+  SAGE_TRY(get_entry("cuMemImportFromShareableHandle", &drv.MemImportFromShareableHandle, 10020));
   return SAGE_OK;
 }
 

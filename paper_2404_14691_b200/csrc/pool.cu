@@ -119,6 +119,9 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = G->dev;
+    // exportable as a POSIX file descriptor: function processes map shared
+    // segments zero-copy (sage_pool_export / sage_segment_import)
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     CUresult r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
     if (r == CUDA_ERROR_OUT_OF_MEMORY && (P->cached || !P->zombies.empty())) {
       reap(P, true);
@@ -431,3 +434,92 @@ int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------- cross-process sharing ----
+// The paper's memory daemon lands a function's read-only data once and the
+// per-function engines (separate processes) map it (PAPER.md:279-281,
+// 358-379): the segment's physical handle leaves as a POSIX file descriptor
+// and is mapped into the importer's address space -- no copy.
+namespace {
+struct Import {
+  int gpu = -1;
+  uint64_t phys = 0;
+  CUdeviceptr va = 0;
+  CUmemGenericAllocationHandle ph = 0;
+};
+std::mutex g_imp_mu;
+std::unordered_map<uint64_t, Import *> g_imports;
+std::atomic<uint64_t> g_imp_next{1};
+}  // namespace
+
+extern "C" int sage_pool_export(sage_handle h, int *fd, uint64_t *phys_bytes) {
+  SAGE_TRY(require_up());
+  if (!fd || !phys_bytes) return fail(SAGE_EINVAL, "pool_export: null argument");
+  Alloc *A = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_allocs.find(h & ((1ull << 56) - 1));
+    if (handle_kind(h) == Kind::Alloc && it != g_allocs.end()) A = it->second;
+  }
+  if (!A || !A->ph) return fail(SAGE_ESTATE, "pool_export: unknown or unmapped segment");
+  int out = -1;
+  SAGE_CU(drv.MemExportToShareableHandle(&out, A->ph, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  *fd = out;
+  *phys_bytes = A->phys;
+  return SAGE_OK;
+}
+
+extern "C" int sage_segment_import(int gpu, int fd, uint64_t phys_bytes, sage_handle *h, uint64_t *dptr) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || fd < 0 || !phys_bytes || !h || !dptr) return fail(SAGE_EINVAL, "segment_import: bad argument");
+  auto *I = new Import();
+  I->gpu = gpu;
+  I->phys = phys_bytes;
+  cudaSetDevice(G->dev);
+  CUresult r = drv.MemImportFromShareableHandle(&I->ph, reinterpret_cast<void *>(static_cast<uintptr_t>(fd)),
+                                                CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  if (r != CUDA_SUCCESS) { delete I; return cu_fail(r, "cuMemImportFromShareableHandle"); }
+  r = drv.MemAddressReserve(&I->va, phys_bytes, G->pool ? G->pool->vmm_gran : 0, 0, 0);
+  if (r == CUDA_SUCCESS) r = drv.MemMap(I->va, phys_bytes, 0, I->ph, 0);
+  if (r == CUDA_SUCCESS) {
+    CUmemAccessDesc a{};
+    a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    a.location.id = G->dev;
+    a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = drv.MemSetAccess(I->va, phys_bytes, &a, 1);
+  }
+  if (r != CUDA_SUCCESS) {
+    if (I->va) { drv.MemUnmap(I->va, phys_bytes); drv.MemAddressFree(I->va, phys_bytes); }
+    drv.MemRelease(I->ph);
+    delete I;
+    return cu_fail(r, "segment_import map");
+  }
+  uint64_t id = g_imp_next++;
+  {
+    std::lock_guard<std::mutex> lk(g_imp_mu);
+    g_imports[id] = I;
+  }
+  *h = make_handle(Kind::Alloc, (1ull << 55) | id);   // import ids live in the upper half of the alloc space
+  *dptr = I->va;
+  return SAGE_OK;
+}
+
+extern "C" int sage_segment_unimport(sage_handle h) {
+  Import *I = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_imp_mu);
+    auto it = g_imports.find(h & ((1ull << 55) - 1));
+    if (handle_kind(h) != Kind::Alloc || !(h & (1ull << 55)) || it == g_imports.end())
+      return fail(SAGE_ESTATE, "double or unknown segment unimport");
+    I = it->second;
+    g_imports.erase(it);
+  }
+  cudaSetDevice(dev_of(I->gpu));
+  cudaDeviceSynchronize();   // no kernel of this process may still read the mapping
+  drv.MemUnmap(I->va, I->phys);
+  drv.MemAddressFree(I->va, I->phys);
+  drv.MemRelease(I->ph);
+  delete I;
+  return SAGE_OK;
+}
