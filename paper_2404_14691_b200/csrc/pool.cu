@@ -121,7 +121,8 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
     prop.location.id = G->dev;
     // exportable as a POSIX file descriptor: function processes map shared
     // segments zero-copy (sage_pool_export / sage_segment_import)
-    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    static const bool shareable = [] { const char *e = getenv("SAGE_POOL_SHAREABLE"); return !(e && atoi(e) == 0); }();
+    if (shareable) prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     CUresult r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
     if (r == CUDA_ERROR_OUT_OF_MEMORY && (P->cached || !P->zombies.empty())) {
       reap(P, true);

@@ -94,6 +94,15 @@ class MemoryDaemon:
         if not ledger.fits(preview.resident_delta) and not sharing.force_demote(gpu, preview.resident_delta, name):
             raise SimulationError(f"{name}: no room for its read-only segment")
         grant = sharing.admit(spec, gpu, preview)
+        try:
+            return self._land_and_export(name, grant, fd)
+        except Exception:
+            sharing.release(name, gpu)       # the engine never got it: undo the admission
+            raise
+
+    def _land_and_export(self, name: str, grant, fd) -> tuple[dict, int]:
+        from .resources import SimulationError
+        sim, gpu = self.sim, self.gpu
         r = grant.resident
         if r.gpu_ro is None:
             raise SimulationError(f"{name}: no read-only segment (ro_sharing off?)")
