@@ -87,7 +87,13 @@ __device__ __forceinline__ void land_finalize(const LandArgs &a) {
 }
 
 constexpr int kLandThreads = 256;
-constexpr int kLandU = 4;  // vectors per lane per tile
+#ifndef SAGE_LAND_U
+#define SAGE_LAND_U 4
+#endif
+#ifndef SAGE_LAND_MINB
+#define SAGE_LAND_MINB 4
+#endif
+constexpr int kLandU = SAGE_LAND_U;  // vectors per lane per tile
 
 // fastest path: a full tile of whole data vectors (no tail, no padding, no
 // bound checks) -- the common case inside every large tensor
@@ -152,7 +158,7 @@ __device__ __forceinline__ unsigned long long land_tile_uniform(const uint4 *__r
   return acc;
 }
 
-__global__ void __launch_bounds__(kLandThreads, 4) land_kernel(const __grid_constant__ LandArgs a) {
+__global__ void __launch_bounds__(kLandThreads, SAGE_LAND_MINB) land_kernel(const __grid_constant__ LandArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
