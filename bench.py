@@ -169,6 +169,9 @@ def run_steps(sim, names, steps: int, payloads=None, marks=None):
                 sim.sharing._evict(r)
         invs = sim.submit_many(names, payloads=payloads)
         sim.drain()
+        box = getattr(sim.dataplane, "box", None)
+        if box is not None:
+            box.reap()           # received segments are no longer read
         bad = [i for i in invs if i.outcome != "completed"]
         if bad:
             raise RuntimeError(f"{len(bad)} invocations did not complete: {bad[0].fail_reason}")
@@ -463,9 +466,14 @@ def cfg1_compare(n: int = 16) -> dict:
     from paper_2404_14691_b200.runtime import ClusterSpec, Simulation, summarize_setup
     spec, data = synthetic_function("fn100", 100, 10, 1, tensors=64)
     out = {}
-    for pol, reps in (("SAGE", 6), ("FixedGSL", 1)):
-        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), {spec.name: spec}, seed=1,
+    # SAGE_pinned_store: the memory daemon keeps the function's DB record in
+    # pinned host memory (registered once, as SAGE's daemon caches function
+    # data on the host); SAGE and FixedGSL read it pageable per cold start
+    for pol, reps in (("SAGE", 6), ("SAGE_pinned_store", 6), ("FixedGSL", 1)):
+        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol.split("_pinned")[0]), {spec.name: spec}, seed=1,
                          function_data={spec.name: data})
+        if pol.endswith("pinned_store"):
+            sim.dataplane.pin_host_store()
         try:
             samples = []
             for rep in range(reps):
@@ -538,11 +546,16 @@ def our_arm(args, rank, world, dist) -> dict:
     sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=1, function_data=data,
                      copy_results=False)
     box = None
-    if world > 1 and not args.no_fanout:
+    if world > 1 and args.fanout != "none":
         # PCIe once per box: each function's home rank loads its segment over
-        # PCIe, the other ranks receive it by ncclBroadcast over NVLink
-        from paper_2404_14691_b200.fanout import BoxFanout
-        box = BoxFanout(rank, world, table)
+        # PCIe; the other ranks land it from the home's pages peer to peer
+        # (p2p, default) or receive it by ncclBroadcast (nccl)
+        from paper_2404_14691_b200.fanout import BoxFanout, PeerFanout
+        if args.fanout == "p2p":
+            job = f"{os.environ.get('MASTER_PORT', '0')}-{os.getppid()}"
+            box = PeerFanout(rank, world, table, job=job, barrier=dist.barrier)
+        else:
+            box = BoxFanout(rank, world, table)
         sim.dataplane.box = box
     L = _lib.lib()
     try:
@@ -592,6 +605,8 @@ def our_arm(args, rank, world, dist) -> dict:
         sim.check_no_leaks()
     finally:
         _lib.check(L.sage_stats_enable(0), "stats_enable")
+        if box is not None:
+            box.close()
         sim.close()
 
     total_inv = per_step * args.steps * world
@@ -678,8 +693,10 @@ def our_arm(args, rank, world, dist) -> dict:
         "kernels_e2e": stats_e2e,
         "gpu_launches": gpu_launches,
         "fanout": None if box is None else {
-            "how": "home rank loads each RO segment over PCIe; ncclBroadcast to the other ranks, "
-                   "then land+checksum from HBM there (e2e / pageable legs)",
+            "how": ("home rank loads each RO segment over PCIe; the other ranks land it from the home's pages "
+                    "peer to peer (one land + checksum, interprocess event)" if box.kind == "peer" else
+                    "home rank loads each RO segment over PCIe; ncclBroadcast to the other ranks, then "
+                    "land+checksum from HBM there") + " (e2e / pageable legs)",
             "homes": box.homes, "rank0": box.stats(),
             "nvlink_bytes_in_all_ranks": int(sum_over_ranks(dist, box.bytes_in)),
             "ro_checksums_agree": ro_checksums_agree(dist, data)},
@@ -723,7 +740,9 @@ def main():
     ap.add_argument("--burst", type=int, default=64)
     ap.add_argument("--no-cfg1", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-fanout", action="store_true", help="N>1: every rank loads its own segments over PCIe")
+    ap.add_argument("--fanout", choices=["p2p", "nccl", "none"], default="p2p",
+                    help="N>1: how non-home ranks get a segment (peer land of the home's pages / ncclBroadcast / "
+                         "their own PCIe load)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

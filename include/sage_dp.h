@@ -98,7 +98,12 @@ int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes);
  * and are mapped zero-copy into another process on the same GPU.           */
 int sage_pool_export(sage_handle h, int *fd, uint64_t *phys_bytes);
 int sage_segment_import(int gpu, int fd, uint64_t phys_bytes, sage_handle *h, uint64_t *dptr);
-int sage_segment_unimport(sage_handle h);
+int sage_segment_unimport(sage_handle h);   /* no device work may still read the mapping */
+/* cross-process device-side dependencies: an interprocess event recorded
+ * after `after` (ipc_handle receives its 64-byte cudaIpcEventHandle); the
+ * other process opens it and waits on it like any event (stream waits only) */
+int sage_ipc_event_export(sage_handle after, sage_handle *ev, void *ipc_handle);
+int sage_ipc_event_open(int gpu, const void *ipc_handle, sage_handle *ev);
 
 /* ---- pinned host buffers (the Stage-2 CPU read-only cache, sharing.py:226-228) */
 int sage_host_alloc(uint64_t bytes, sage_handle *h, void **ptr);

@@ -131,6 +131,8 @@ _SIGS = {
     "sage_pool_export": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(u64)]),
     "sage_segment_import": (C.c_int, [C.c_int, C.c_int, u64, C.POINTER(H), C.POINTER(u64)]),
     "sage_segment_unimport": (C.c_int, [H]),
+    "sage_ipc_event_export": (C.c_int, [H, C.POINTER(H), C.c_void_p]),
+    "sage_ipc_event_open": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(H)]),
     "sage_launch": (C.c_int, [H, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_launch_after": (C.c_int, [H, C.POINTER(H), C.c_int, C.POINTER(BodyDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_return_after": (C.c_int, [H, C.POINTER(H), C.c_int, u64, C.c_void_p, u64, C.POINTER(H), C.POINTER(H)]),

@@ -85,6 +85,7 @@ struct Event {
   std::atomic<int> refs{1};      // handles naming this event (event_alias)
   std::atomic<bool> done{false}; // sticky completion (skips re-queries)
   int64_t t_cache = INT64_MIN;   // host-clock time once resolved
+  bool ipc = false;              // interprocess event (no timing; destroyed, never pooled)
 };
 int event_new(int gpu, sage_handle *h, Event **out);        // device event
 int event_new_host(sage_handle *h, Event **out);            // host-completed event
@@ -138,6 +139,8 @@ struct Gpu {
   ChunkScratch scratch;
   // clock anchor (see clock_anchor_refresh)
   cudaStream_t clock = nullptr;           // dedicated top-priority stream, never loaded
+  cudaStream_t ipc = nullptr;             // records interprocess events (fan-out to other processes)
+  std::mutex ipc_mu;
   cudaEvent_t anchor_trial = nullptr;
   cudaEvent_t anchor = nullptr;
   int64_t anchor_us = 0;

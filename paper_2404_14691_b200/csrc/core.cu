@@ -575,7 +575,9 @@ int sage_event_release(sage_handle h) {
     g_ev.events.erase(it);
   }
   if (e->refs.fetch_sub(1) != 1) return SAGE_OK;   // another handle still names it
-  if (e->ev) {
+  if (e->ev && e->ipc) {
+    cudaEventDestroy(e->ev);
+  } else if (e->ev) {
     std::lock_guard<std::mutex> lk(g_evpool_mu);
     if (e->gpu >= 0 && e->gpu < (int)g_evpool.size()) g_evpool[e->gpu].push_back(e->ev);
     else cudaEventDestroy(e->ev);
@@ -853,3 +855,61 @@ int sage_host_free(sage_handle h) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------- cross-process events -----
+// A process that lands a segment other processes will read (the home rank of
+// a fan-out) hands them an interprocess event recorded after the land; they
+// open it and make their own streams wait on it -- a device-side dependency
+// across processes, no host round trip.
+extern "C" int sage_ipc_event_export(sage_handle after, sage_handle *ev, void *ipc_handle) {
+  SAGE_TRY(require_up());
+  Event *A = event_get(after);
+  if (!A || !A->ev || !ev || !ipc_handle) return fail(SAGE_EINVAL, "ipc_event_export: bad argument");
+  SAGE_TRY(event_await_recorded(A));
+  Gpu *G = gpu_get(A->gpu);
+  if (!G) return fail(SAGE_ENODEV, "ipc_event_export: bad gpu");
+  cudaSetDevice(G->dev);
+  auto *e = new Event();
+  e->gpu = A->gpu;
+  e->ipc = true;
+  cudaError_t r = cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming | cudaEventInterprocess);
+  if (r != cudaSuccess) { delete e; return cuda_fail(r, "cudaEventCreate(interprocess)"); }
+  {
+    std::lock_guard<std::mutex> lk(G->ipc_mu);
+    if (!G->ipc) r = cudaStreamCreateWithFlags(&G->ipc, cudaStreamNonBlocking);
+    if (r == cudaSuccess) r = cudaStreamWaitEvent(G->ipc, A->ev, 0);
+    if (r == cudaSuccess) r = cudaEventRecord(e->ev, G->ipc);
+  }
+  if (r == cudaSuccess) r = cudaIpcGetEventHandle(reinterpret_cast<cudaIpcEventHandle_t *>(ipc_handle), e->ev);
+  if (r != cudaSuccess) { cudaEventDestroy(e->ev); delete e; return cuda_fail(r, "ipc_event_export"); }
+  e->recorded.store(true);
+  uint64_t id = g_ev.next++;
+  {
+    std::lock_guard<std::mutex> lk(g_ev.mu);
+    g_ev.events[id] = e;
+  }
+  *ev = make_handle(Kind::Event, id);
+  return SAGE_OK;
+}
+
+extern "C" int sage_ipc_event_open(int gpu, const void *ipc_handle, sage_handle *ev) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || !ipc_handle || !ev) return fail(SAGE_EINVAL, "ipc_event_open: bad argument");
+  cudaSetDevice(G->dev);
+  auto *e = new Event();
+  e->gpu = gpu;
+  e->ipc = true;
+  cudaIpcEventHandle_t h;
+  memcpy(&h, ipc_handle, sizeof h);
+  cudaError_t r = cudaIpcOpenEventHandle(&e->ev, h);
+  if (r != cudaSuccess) { delete e; return cuda_fail(r, "cudaIpcOpenEventHandle"); }
+  e->recorded.store(true);
+  uint64_t id = g_ev.next++;
+  {
+    std::lock_guard<std::mutex> lk(g_ev.mu);
+    g_ev.events[id] = e;
+  }
+  *ev = make_handle(Kind::Event, id);
+  return SAGE_OK;
+}

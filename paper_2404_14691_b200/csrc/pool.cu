@@ -18,6 +18,7 @@ struct Alloc {
   uint64_t bytes = 0, eff = 0, phys = 0;
   int cls = 0;
   bool account_only = false;
+  bool exported = false;   // pages handed to another process: never recycled through the cache
   CUdeviceptr va = 0;
   CUmemGenericAllocationHandle ph = 0;
 };
@@ -163,7 +164,8 @@ static void unmap_segment(Pool *P, Alloc *A) {
   // keep the segment MAPPED for reuse by the next allocation of this size
   // (per-invocation writable churn then costs no driver call) while the
   // cache stays within budget; otherwise unmap and release the pages
-  if (P->cached + A->phys + P->physical <= P->capacity + (4ull << 30) && P->cached + A->phys <= (16ull << 30)) {
+  if (!A->exported && P->cached + A->phys + P->physical <= P->capacity + (4ull << 30) &&
+      P->cached + A->phys <= (16ull << 30)) {
     P->free_mapped.emplace(A->phys, std::make_pair(A->va, A->ph));
     P->cached += A->phys;
   } else {
@@ -272,6 +274,7 @@ void gpu_teardown(Gpu *G) {
   if (G->anchor) cudaEventDestroy(G->anchor);
   if (G->anchor_trial) cudaEventDestroy(G->anchor_trial);
   if (G->clock) cudaStreamDestroy(G->clock);
+  if (G->ipc) cudaStreamDestroy(G->ipc);
   if (G->pin) cudaFreeHost(G->pin);
   if (G->dstage) cudaFree(G->dstage);
   if (G->scratch.d_acc) cudaFree(G->scratch.d_acc);
@@ -465,6 +468,7 @@ extern "C" int sage_pool_export(sage_handle h, int *fd, uint64_t *phys_bytes) {
   if (!A || !A->ph) return fail(SAGE_ESTATE, "pool_export: unknown or unmapped segment");
   int out = -1;
   SAGE_CU(drv.MemExportToShareableHandle(&out, A->ph, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  A->exported = true;   // importers keep the pages alive; this process must not reuse them
   *fd = out;
   *phys_bytes = A->phys;
   return SAGE_OK;
@@ -517,7 +521,7 @@ extern "C" int sage_segment_unimport(sage_handle h) {
     g_imports.erase(it);
   }
   cudaSetDevice(dev_of(I->gpu));
-  cudaDeviceSynchronize();   // no kernel of this process may still read the mapping
+  // the caller guarantees no device work still reads the mapping
   drv.MemUnmap(I->va, I->phys);
   drv.MemAddressFree(I->va, I->phys);
   drv.MemRelease(I->ph);

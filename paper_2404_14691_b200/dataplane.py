@@ -445,17 +445,25 @@ class DataPlane:
                 d.ro_src, d.ro_src_bytes = fd.db_dev.dptr, fd.layout.packed_bytes
                 run.ro_source = "hbm"
             elif box is not None and grant is not None and grant.leader_ro and not box.is_home(inv.spec.name):
-                # PCIe once per box (multi-process): the segment arrives from its
-                # home rank over NVLink; GPU_LOAD lands (and verifies) it locally
+                # PCIe once per box (multi-process): the segment comes from its
+                # home rank over NVLink; GPU_LOAD lands and verifies it locally
                 nb = fd.layout.seg_bytes
-                buf = self._scratch_get(gpu, nb)
-                run.scratch.append(buf)
-                ev = box.receive(gpu, buf.dptr, nb, inv.spec.name)
+
+                def scratch(n, run=run, gpu=gpu):
+                    seg = self._scratch_get(gpu, n)
+                    run.scratch.append(seg)
+                    return seg
+                how, src, ev = box.fetch(gpu, inv.spec.name, nb, scratch)
                 run.events.append(ev)
-                d.ro_kind, d.ro_layout, d.ro_src, d.ro_src_bytes = _lib.SRC_HBM, 0, buf.dptr, nb
+                if how == "peer":   # one land reads the home's pages peer to peer
+                    d.ro_kind, d.ro_src_gpu, d.ro_layout = _lib.SRC_PEER, gpu, 0
+                    d.ro_src, d.ro_src_bytes = src, nb
+                    run.ro_source = "nvlink"
+                else:               # the bytes were copied into a local buffer
+                    d.ro_kind, d.ro_layout, d.ro_src, d.ro_src_bytes = _lib.SRC_HBM, 0, src.dptr, nb
+                    run.ro_source = "nccl"
                 d.ro_wait[0] = ev.h
                 d.n_ro_wait = 1
-                run.ro_source = "nccl"
             else:
                 d.ro_kind = _lib.SRC_PINNED if fd.db_pinned else _lib.SRC_HOST
                 d.ro_layout = fd.layout.handle()
@@ -506,7 +514,8 @@ class DataPlane:
         if publish:
             # home rank: send the landed segment to the other ranks; eviction
             # waits for the send (sharing._evict)
-            ev = box.publish(gpu, ro, fd.layout.seg_bytes, _Borrowed(ro_end.value))
+            ev = box.publish(gpu, ro, fd.layout.seg_bytes, _Borrowed(ro_end.value),
+                             seg_handle=resident.gpu_ro.segment.h, name=inv.spec.name)
             if resident.ro_busy is not None:
                 resident.ro_busy.release()
             resident.ro_busy = ev

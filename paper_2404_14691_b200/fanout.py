@@ -18,13 +18,30 @@ same order.  They are issued at admission of a cold leader, from the
 admitting thread; with the same burst on every rank (weak scaling) the cold
 leaders -- and hence the broadcasts -- come in the same order everywhere.
 
+Two exchanges implement it:
+
+  PeerFanout  (default) the home exports the landed segment's pages as a
+              POSIX file descriptor and an interprocess event recorded after
+              its land; each other rank maps the pages (over NVLink when they
+              live on another GPU) and its cold leader's GPU_LOAD is ONE
+              `land` launch reading the home's segment peer to peer and
+              checksumming it -- transfer and verification fused, no copy
+              through an intermediate buffer, device-side wait on the home's
+              event.  Descriptors travel over Unix sockets between the ranks.
+  BoxFanout   ncclBroadcast into a receive buffer, then a local land (the
+              collective-library baseline).
+
 In the same-process multi-GPU layout (`ClusterSpec(gpus=N)`) the peer `land`
 of dataplane._peer_source does this job with direct NVLink loads instead.
 """
 from __future__ import annotations
 
+import os
+import socket
+import time
 from typing import Callable, Optional
 
+from . import _lib
 from . import device as D
 
 
@@ -53,7 +70,22 @@ class BoxFanout:
     def is_home(self, name: str) -> bool:
         return self.home(name) == self.rank
 
-    def publish(self, gpu: int, dptr: int, nbytes: int, landed: D.Event) -> D.Event:
+    kind = "nccl"
+
+    def fetch(self, gpu: int, name: str, nbytes: int, scratch: Callable[[int], object]):
+        """Receiver side of the common interface: ("copy", buffer, event) --
+        the bytes arrive in a scratch buffer from `scratch(nbytes)`."""
+        buf = scratch(nbytes)
+        return "copy", buf, self.receive(gpu, buf.dptr, nbytes, name)
+
+    def reap(self) -> None:
+        pass
+
+    def close(self) -> None:
+        pass
+
+    def publish(self, gpu: int, dptr: int, nbytes: int, landed: D.Event, seg_handle: int = 0,
+                name: str = "") -> D.Event:
         """Home side: broadcast the landed segment once `landed` completes.
         Returns the event that ends the send on this GPU."""
         slot = D.Slot(gpu)
@@ -98,3 +130,123 @@ def _torch_broadcast(gpu: int, stream: int, dptr: int, nbytes: int, src: int) ->
     with torch.cuda.stream(ext):
         work = dist.broadcast(t, src=src, async_op=True)
         work.wait()              # the slot stream waits for the collective
+
+
+# ------------------------------------------------------------ peer mapping ---
+def _sock_path(sock_dir: str, job: str, rank: int) -> str:
+    return os.path.join(sock_dir, f"sage-fan-{job}-{rank}.sock")
+
+
+class PeerFanout(BoxFanout):
+    """PCIe once per box with the receivers landing the home's segment peer
+    to peer (see module docstring).  `barrier()` synchronises the ranks during
+    the socket rendezvous (torch.distributed.barrier in bench.py)."""
+
+    kind = "peer"
+
+    def __init__(self, rank: int, world: int, names, homes: Optional[dict] = None, job: str = "sage",
+                 sock_dir: str = "/tmp", barrier: Optional[Callable[[], None]] = None, timeout_s: float = 120.0):
+        super().__init__(rank, world, names, homes, broadcast=lambda *a: None)
+        from .daemon import _recv, _send
+        self._recv, self._send = _recv, _send
+        self.job, self.sock_dir = job, sock_dir
+        self.imports: list = []          # (import handle, ipc event) per received segment
+        self._pending: dict = {}         # home rank -> {fn: message, fds}
+        path = _sock_path(sock_dir, job, rank)
+        if os.path.exists(path):
+            os.unlink(path)
+        self._lsock = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        self._lsock.bind(path)
+        self._lsock.listen(max(1, world))
+        self._lsock.settimeout(timeout_s)
+        if barrier:
+            barrier()                                 # everyone listens
+        self.to_home: dict[int, socket.socket] = {}
+        for h in range(world):                        # every other rank may be a home
+            if h == rank:
+                continue
+            c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            deadline = time.time() + timeout_s
+            while True:
+                try:
+                    c.connect(_sock_path(sock_dir, job, h))
+                    break
+                except (FileNotFoundError, ConnectionRefusedError):
+                    if time.time() > deadline:
+                        raise
+                    time.sleep(0.01)
+            self._send(c, {"hello": rank})
+            self.to_home[h] = c
+        self.to_recv: dict[int, socket.socket] = {}
+        for _ in range(world - 1):
+            conn, _ = self._lsock.accept()
+            conn.settimeout(timeout_s)
+            self.to_recv[int(self._recv(conn)["hello"])] = conn
+        if barrier:
+            barrier()
+
+    def publish(self, gpu: int, dptr: int, nbytes: int, landed: D.Event, seg_handle: int = 0,
+                name: str = "") -> D.Event:
+        """Home: export the segment's pages and an event recorded after its
+        land to every other rank.  Returns the interprocess event (kept until
+        the resident is evicted)."""
+        L = _lib.lib()
+        ev, ipc = _lib.H(), (_lib.C.c_ubyte * 64)()
+        _lib.check(L.sage_ipc_event_export(landed.h, _lib.C.byref(ev), ipc), "sage_ipc_event_export")
+        fd, phys = _lib.C.c_int(), _lib.u64()
+        _lib.check(L.sage_pool_export(seg_handle, _lib.C.byref(fd), _lib.C.byref(phys)), "sage_pool_export")
+        try:
+            msg = {"fn": name, "phys": phys.value, "bytes": nbytes, "ipc": bytes(ipc).hex()}
+            for r in sorted(self.to_recv):
+                self._send(self.to_recv[r], msg, fds=[fd.value])
+        finally:
+            os.close(fd.value)
+        self.sent += 1
+        self.bytes_out += nbytes * (self.world - 1)
+        return D.Event(ev.value)
+
+    def _message_for(self, home: int, name: str):
+        box = self._pending.setdefault(home, {})
+        while name not in box:
+            msg, fds = self._recv(self.to_home[home], with_fd=True)
+            box[msg["fn"]] = (msg, fds)
+        return box.pop(name)
+
+    def fetch(self, gpu: int, name: str, nbytes: int, scratch=None):
+        """Receiver: map the home's segment and open its landed event.
+        Returns ("peer", device address, event to wait on)."""
+        msg, fds = self._message_for(self.home(name), name)
+        if msg["bytes"] != nbytes:
+            raise RuntimeError(f"{name}: home sent {msg['bytes']} B, expected {nbytes} B")
+        L = _lib.lib()
+        h, dptr = _lib.H(), _lib.u64()
+        try:
+            _lib.check(L.sage_segment_import(gpu, fds[0], msg["phys"], _lib.C.byref(h), _lib.C.byref(dptr)),
+                       "sage_segment_import")
+        finally:
+            for f in fds:
+                os.close(f)
+        ev = _lib.H()
+        ipc = (_lib.C.c_ubyte * 64).from_buffer_copy(bytes.fromhex(msg["ipc"]))
+        _lib.check(L.sage_ipc_event_open(gpu, ipc, _lib.C.byref(ev)), "sage_ipc_event_open")
+        self.imports.append((h.value, ev.value))
+        self.received += 1
+        self.bytes_in += nbytes
+        return "peer", dptr.value, D.Event(ev.value)
+
+    def reap(self) -> None:
+        """Unmap every received segment; call when no device work reads them
+        (after the burst that landed them drained)."""
+        L = _lib.lib()
+        for h, ev in self.imports:
+            _lib.check(L.sage_segment_unimport(h), "sage_segment_unimport")
+        self.imports.clear()
+
+    def close(self) -> None:
+        self.reap()
+        for c in list(self.to_home.values()) + list(self.to_recv.values()):
+            c.close()
+        self._lsock.close()
+        path = _sock_path(self.sock_dir, self.job, self.rank)
+        if os.path.exists(path):
+            os.unlink(path)
