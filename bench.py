@@ -47,11 +47,23 @@ def _rank_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 and not _shared_gpu():
         vis = os.environ.get("CUDA_VISIBLE_DEVICES")
         ids = vis.split(",") if vis else [str(i) for i in range(64)]
         os.environ["CUDA_VISIBLE_DEVICES"] = ids[local]
     return rank, world, local
+
+
+def _shared_gpu() -> bool:
+    """Test mode (SAGE_BENCH_SHARE_GPU=1): every rank on device 0 and gloo for
+    the rank plumbing, so the N > 1 path (fan-out included) runs on a
+    one-GPU box.  Not a measurement mode."""
+    return os.environ.get("SAGE_BENCH_SHARE_GPU") == "1"
+
+
+def _reduce_device(dist) -> str:
+    import torch
+    return "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
 
 
 # --------------------------------------------------------------- clocks -------
@@ -423,7 +435,7 @@ def max_over_ranks(dist, v: float) -> float:
     if dist is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = torch.tensor([v], dtype=torch.float64, device=_reduce_device(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -432,7 +444,7 @@ def sum_over_ranks(dist, v: float) -> float:
     if dist is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = torch.tensor([v], dtype=torch.float64, device=_reduce_device(dist))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -442,7 +454,7 @@ def ro_checksums_agree(dist, data) -> bool:
     import torch
     mine = [data[n].ro_checksum or 0 for n in sorted(data)]
     t = torch.tensor([c - (1 << 64) if c >= (1 << 63) else c for c in mine], dtype=torch.int64,
-                     device="cuda" if torch.cuda.is_available() else "cpu")
+                     device=_reduce_device(dist))
     lo, hi = t.clone(), t.clone()
     dist.all_reduce(lo, op=dist.ReduceOp.MIN)
     dist.all_reduce(hi, op=dist.ReduceOp.MAX)
@@ -756,7 +768,7 @@ def main():
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(0)
-        tdist.init_process_group("nccl")
+        tdist.init_process_group("gloo" if _shared_gpu() else "nccl")
         dist = tdist
     from paper_2404_14691_b200 import _lib
     _lib.lib()  # fail loudly if the native library is missing
