@@ -244,6 +244,11 @@ class PeerFanout(BoxFanout):
 
     def close(self) -> None:
         self.reap()
+        for box in self._pending.values():          # descriptors received but never used
+            for _msg, fds in box.values():
+                for f in fds:
+                    os.close(f)
+        self._pending.clear()
         for c in list(self.to_home.values()) + list(self.to_recv.values()):
             c.close()
         self._lsock.close()
