@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 #define CK(x) do { CUresult r_ = (x); if (r_ != CUDA_SUCCESS) { const char *s; cuGetErrorString(r_, &s); \
@@ -38,7 +39,7 @@ int main() {
   memset(&p, 0, sizeof p);
   p.numDevices = 1;
   p.size = want;
-  p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  p.handleTypes = getenv("MC_HT") ? (CUmemAllocationHandleType)atoi(getenv("MC_HT")) : CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   size_t gran = 0;
   CK(cuMulticastGetGranularity(&gran, &p, CU_MULTICAST_GRANULARITY_RECOMMENDED));
   p.size = (want + gran - 1) / gran * gran;
