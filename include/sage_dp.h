@@ -266,7 +266,8 @@ typedef struct {
   int32_t in_kind;
   const void *in_src;
   uint64_t in_bytes, in_dst;
-  sage_handle wait[2];            /* SYNC_WAIT: leader RO / ctx END events          */
+  sage_handle wait[4];            /* SYNC_WAIT: leader RO / ctx END events, and the
+                                     compute-gate predecessor (ComputeGate)          */
   int32_t n_wait;
   int32_t pad_;
   sage_body_desc body;            /* COMPUTE                                        */

@@ -72,7 +72,7 @@ class InvokeDesc(C.Structure):
                 ("ro_kind", C.c_int32), ("ro_src_gpu", C.c_int32), ("ro_layout", H), ("ro_src", C.c_void_p),
                 ("ro_src_bytes", u64), ("ro_dst", u64), ("ro_wait", H * 2), ("n_ro_wait", C.c_int32),
                 ("in_kind", C.c_int32), ("in_src", C.c_void_p), ("in_bytes", u64), ("in_dst", u64),
-                ("wait", H * 2), ("n_wait", C.c_int32), ("pad_", C.c_int32), ("body", BodyDesc),
+                ("wait", H * 4), ("n_wait", C.c_int32), ("pad_", C.c_int32), ("body", BodyDesc),
                 ("ret_src", u64), ("ret_dst", C.c_void_p), ("ret_bytes", u64)]
 
 

@@ -40,7 +40,7 @@ struct Inv {
   sage_handle ro_load = 0, ro_end = 0, in_load = 0, in_end = 0;
   // handed out at submit, recorded at issue: RO landed, context bound, done
   sage_handle pre_ro = 0, pre_ctx = 0, pre_done = 0;
-  sage_handle hold[4] = {0, 0, 0, 0};   // retained wait events (released after issue)
+  sage_handle hold[6] = {0, 0, 0, 0, 0, 0};   // retained wait events (released after issue)
   sage_invoke_desc d{};                 // the submitted descriptor (waits -> hold)
   int64_t t_enqueue = 0;
   int64_t h2d = 0, d2h = 0;             // PCIe bytes each way (issue order)
@@ -161,7 +161,7 @@ static uint32_t load_flags(int kind) {
 static void inv_free(Inv *I) {
   for (sage_handle h : {I->ctx_b, I->ctx_e, I->sync_b, I->sync_e, I->comp_b, I->comp_e, I->ret_b, I->ret_e,
                         I->ro_end, I->in_end, I->pre_ro, I->pre_ctx, I->pre_done, I->hold[0], I->hold[1],
-                        I->hold[2], I->hold[3]})
+                        I->hold[2], I->hold[3], I->hold[4], I->hold[5]})
     if (h) sage_event_release(h);
   if (I->ro_load) sage_load_release(I->ro_load);
   if (I->in_load) sage_load_release(I->in_load);
@@ -224,8 +224,8 @@ static int submit_prepare(Inv *I) {
     d.wait[i] = I->hold[i];
   }
   for (int i = 0; i < d.n_ro_wait; ++i) {
-    SAGE_TRY(event_alias(d.ro_wait[i], &I->hold[2 + i]));
-    d.ro_wait[i] = I->hold[2 + i];
+    SAGE_TRY(event_alias(d.ro_wait[i], &I->hold[4 + i]));
+    d.ro_wait[i] = I->hold[4 + i];
   }
   Event *e;
   SAGE_TRY(event_new(d.gpu, &I->pre_done, &e));
@@ -301,12 +301,14 @@ static int issue(Inv *I) {
     rc = segment_load(&L, &I->in_load, &I->in_end, 0);
   }
   // the join before COMPUTE: loads ran on other streams
-  sage_handle deps[6];
+  sage_handle deps[8];
   int nd = 0;
   if (I->ro_end) deps[nd++] = I->ro_end;
   if (I->in_end) deps[nd++] = I->in_end;
+  // leader tokens (SYNC_WAIT) and the compute-gate predecessor: COMPUTE waits
+  // on all of them; only a SYNC_WAIT plan node records the stage
+  for (int i = 0; i < d->n_wait && i < 4; ++i) deps[nd++] = d->wait[i];
   if (rc == SAGE_OK && (d->flags & SAGE_INV_SYNC)) {
-    for (int i = 0; i < d->n_wait && i < 2; ++i) deps[nd++] = d->wait[i];
     rc = last ? event_alias(last, &I->sync_b) : rec(&I->sync_b);
     if (rc == SAGE_OK) rc = wait_events(s, deps, nd);
     if (rc == SAGE_OK) rc = rec(&I->sync_e);
@@ -340,7 +342,7 @@ static int issue(Inv *I) {
     }
     cudaDeviceSynchronize();  // error path only: nothing may still reference I
   }
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 6; ++i)
     if (I->hold[i]) { sage_event_release(I->hold[i]); I->hold[i] = 0; }
   I->issued.store(true, std::memory_order_release);
   return rc;
@@ -523,8 +525,8 @@ int sage_invoke(const sage_invoke_desc *d, sage_handle *inv_out, sage_handle *do
   SAGE_TRY(require_up());
   if (!d || !inv_out || !done_ev) return fail(SAGE_EINVAL, "invoke: null argument");
   if (!gpu_get(d->gpu)) return fail(SAGE_ENODEV, "invoke: bad gpu");
-  if (d->n_wait < 0 || d->n_wait > 2 || d->n_ro_wait < 0 || d->n_ro_wait > 2)
-    return fail(SAGE_EINVAL, "invoke: at most two wait events per list");
+  if (d->n_wait < 0 || d->n_wait > 4 || d->n_ro_wait < 0 || d->n_ro_wait > 2)
+    return fail(SAGE_EINVAL, "invoke: at most four SYNC_WAIT and two RO wait events");
   auto *I = new Inv();
   I->gpu = d->gpu;
   I->id = g_inv_next++;

@@ -26,6 +26,7 @@ FixedGSL instances (fresh_context) run as native serial jobs instead.
 """
 from __future__ import annotations
 
+from collections import deque
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -256,7 +257,35 @@ class DataPlane:
         self._fast = _FastCompletions(self)
         self._scratch: dict[tuple[int, int], list] = {}
         self.box = None               # fanout.BoxFanout: PCIe once per box across processes
+        self._gate_q: dict[int, deque] = {}
         self._fast_source = False
+
+    # ------------------------------------------------------- compute gate ----
+    def _gate_wait(self, run: _Run) -> Optional[int]:
+        """ComputeGate (functions.py:304-327, ClusterSpec.compute_concurrency):
+        at most K invocations of a GPU compute at once, FIFO.  On the device
+        that is a semaphore over the enqueue order: the n-th invocation's
+        COMPUTE waits for the (n-K)-th to finish (its RETURN END event: the
+        gate is released one stage later than in the model)."""
+        gates = self.sim.compute_gates
+        if not gates:
+            return None
+        q = self._gate_q.setdefault(run.gpu, deque())
+        while q and (q[0].inv is None or q[0].inv.run is not q[0]):
+            q.popleft()                              # completed and released
+        if len(q) < gates[run.gpu].slots:
+            return None
+        pred = q[0]
+        return pred.end.h if pred.end is not None and pred.end.h else None
+
+    def _gate_push(self, run: _Run) -> None:
+        gates = self.sim.compute_gates
+        if not gates:
+            return
+        q = self._gate_q.setdefault(run.gpu, deque())
+        q.append(run)
+        while len(q) > gates[run.gpu].slots:
+            q.popleft()
 
     def _scratch_get(self, gpu: int, nbytes: int) -> D.Segment:
         """Runtime scratch outside the ledger (results kept in HBM, inputs that
@@ -483,14 +512,18 @@ class DataPlane:
                 else:
                     d.in_kind, d.in_src = _lib.SRC_HOST, p.ctypes.data
                 run.keep = p
+        n = 0
         if pf.sync:
             flags |= _lib.INV_SYNC
-            n = 0
             for t in wait_tokens:
                 if n < 2 and not t.ready and t.event is not None:
                     d.wait[n] = t.event.h
                     n += 1
-            d.n_wait = n
+        gate = self._gate_wait(run)
+        if gate is not None:
+            d.wait[n] = gate
+            n += 1
+        d.n_wait = n
         # COMPUTE: the function's body template + this invocation's pointers
         d.body = _body_template(fd)
         body = d.body
@@ -511,6 +544,7 @@ class DataPlane:
                                           _lib.C.byref(ctx_end)), "sage_invoke")
         run.invh = h.value
         run.end = _Borrowed(done.value)
+        self._gate_push(run)
         if publish:
             # home rank: send the landed segment to the other ranks; eviction
             # waits for the send (sharing._evict)
@@ -689,6 +723,9 @@ class DataPlane:
                 ends[i].append(e)
                 run.marks[st] = (b, e)
             elif st is Stage.COMPUTE:
+                gate = self._gate_wait(run)
+                if gate is not None:
+                    deps = list(deps) + [_Borrowed(gate)]
                 if fd.body == "resnet50":
                     # DNN body: PyTorch on the invocation's stream, weights read in
                     # place from the landed (shared) segment
@@ -720,6 +757,7 @@ class DataPlane:
                 run.end = e
         if run.end is None:
             raise SimulationError("plan has no RETURN node")
+        self._gate_push(run)
 
     def _payload(self, inv, fd: FunctionData):
         p = getattr(inv, "payload", None)
