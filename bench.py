@@ -205,6 +205,8 @@ def timed(sim, names, steps, warmup, dist, payloads=None):
     gc.collect()
     gc.disable()
     _lib.check(L.sage_stats_reset(), "stats_reset")
+    box = getattr(sim.dataplane, "box", None)
+    box_in0 = box.bytes_in if box is not None else 0
     barrier(dist)
     _lib.check(L.sage_device_sync(0), "device_sync")
     a = _lib.H()
@@ -226,6 +228,7 @@ def timed(sim, names, steps, warmup, dist, payloads=None):
     gc.enable()
     elapsed = max_over_ranks(dist, us.value)
     timed.step_ms = step_ms
+    timed.box_bytes = (box.bytes_in - box_in0) if box is not None else 0
     return elapsed, invs
 
 
@@ -589,6 +592,7 @@ def our_arm(args, rank, world, dist) -> dict:
         clocks = ClockSampler(0).start()
         e2e_us, invs_e2e = timed(sim, names, args.steps, args.warmup, dist, payloads)
         e2e_steps = timed.step_ms
+        e2e_box_bytes = timed.box_bytes
         clocks_e2e = clocks.stop()
         sim.dataplane.unpin_host_store()
         for pb in payloads:
@@ -711,6 +715,9 @@ def our_arm(args, rank, world, dist) -> dict:
                     "land+checksum from HBM there") + " (e2e / pageable legs)",
             "homes": box.homes, "rank0": box.stats(),
             "nvlink_bytes_in_all_ranks": int(sum_over_ranks(dist, box.bytes_in)),
+            "nvlink_GBps_e2e": round(sum_over_ranks(dist, e2e_box_bytes) / (e2e_us / 1e6) / 1e9, 2),
+            "nvlink_GBps_note": "segment bytes received by all ranks in the timed e2e steps over the e2e time "
+                                "(a traffic rate, not a link benchmark)",
             "ro_checksums_agree": ro_checksums_agree(dist, data)},
         "clocks": clocks_val,
         "clocks_e2e": clocks_e2e,
