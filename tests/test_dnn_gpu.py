@@ -69,3 +69,27 @@ def test_resnet50_graph_replays_distinct_inputs(built):
         for pb in pls:           # before close(): shutdown frees every pinned buffer
             pb.free()
         sim.close()
+
+
+def test_resnet50_bf16_function_within_rtol(built):
+    """The BF16 variant (51 MB of bfloat16 weights landed, bf16 input, fp32
+    logits): within the north star's BF16 tolerance of the fp32 network on the
+    same (bf16-rounded) input."""
+    import torch
+    import torchvision
+    from paper_2404_14691_b200 import dnn
+    spec, data = dnn.resnet50(batch=8, seed=0, dtype="bf16")
+    assert data.layout.seg_bytes < 52 << 20
+    with Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), {spec.name: spec}, seed=1,
+                    function_data={spec.name: data}) as sim:
+        invs = sim.submit_many([spec.name] * 5)
+        sim.drain()
+        assert [i.warmth.label() for i in invs] == ["Cold"] + ["Stage1Hot"] * 4
+        torch.manual_seed(0)
+        ref = torchvision.models.resnet50(weights=None).eval().cuda()
+        x = torch.from_numpy(data.input.copy()).view(torch.bfloat16).float().view(8, 3, 224, 224).cuda()
+        with torch.inference_mode():
+            want = ref(x).float().cpu().numpy()
+        for inv in invs:
+            got = inv.result.view(np.float32).reshape(8, 1000)
+            np.testing.assert_allclose(got, want, rtol=1e-2, atol=2e-2 * np.abs(want).max())
