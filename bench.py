@@ -236,7 +236,7 @@ def kernel_stats():
     from paper_2404_14691_b200 import _lib
     L = _lib.lib()
     out = {}
-    for kind, name in enumerate(["land", "touch", "sgemm", "stencil", "spmv", "verify"]):
+    for kind, name in enumerate(["land", "touch", "sgemm", "stencil", "spmv", "verify", "gather"]):
         n, t, b = _lib.u64(), _lib.C.c_double(), _lib.u64()
         _lib.check(L.sage_stats_get(0, kind, _lib.C.byref(n), _lib.C.byref(t), _lib.C.byref(b)), "stats_get")
         if n.value:
@@ -282,6 +282,46 @@ def body_probe(data, body: str, iters: int = 20) -> dict | None:
     finally:
         slot.release()
         for x in (seg, inp, out):
+            x.free()
+
+
+def gather_probe(data, iters: int = 20) -> dict | None:
+    """The random-gather ceiling spmv's x accesses run against: the
+    diagnostic GATHER body does as many hashed 4-B gathers as spmv has
+    non-zeros, from an array of x's size, with no col / val streams
+    (tools/gather_micro.cu sweeps the array size and cache hints: the rate
+    is flat from 1 to 64 MiB, a per-SM L1TEX miss-issue limit)."""
+    from paper_2404_14691_b200 import _lib
+    from paper_2404_14691_b200 import device as D
+    name = next((n for n in sorted(data) if data[n].body == "spmv"), None)
+    if name is None:
+        return None
+    fd = data[name]
+    rows, nnz = int(fd.args[0]), int(fd.args[1])
+    elems = 1 << max(0, (rows - 1).bit_length())
+    inp = D.pool_alloc(0, elems * 4, _lib.CLASS_WRITABLE, unaccounted=True)
+    out = D.pool_alloc(0, 256, _lib.CLASS_WRITABLE, unaccounted=True)
+    slot = D.Slot(0)
+    try:
+        desc = D.body_desc(_lib.BODY_GATHER, ro=0, ro_bytes=0, inp=inp.dptr, inp_bytes=elems * 4, out=out.dptr,
+                           out_bytes=16, args=(nnz // 4 * 4,))
+        slot.launch(desc)[1].sync()                      # warm: x in L2, module loaded
+        _lib.check(_lib.lib().sage_stats_reset(), "stats_reset")
+        evs = [slot.launch(desc) for _ in range(iters)]
+        evs[-1][1].sync()
+        for b, e in evs:
+            b.release()
+            e.release()
+        g = kernel_stats().get("gather")
+        if not g:
+            return None
+        us = g["total_us"] / g["launches"]
+        return {"gathers_per_launch": g["work"] // g["launches"], "avg_launch_us": round(us, 2),
+                "G_gathers_per_s": round(g["work"] / g["launches"] / us / 1e3, 1), "array_bytes": elems * 4,
+                "launches": g["launches"]}
+    finally:
+        slot.release()
+        for x in (inp, out):
             x.free()
 
 
@@ -333,7 +373,8 @@ def d2d_reference(dst: int, src: int, nbytes: int, iters: int = 20) -> float:
 _TRAFFIC = {"spmv": "r1_spmv_traffic.json", "land": "r1_land_traffic.json"}
 
 
-def dominant_roofline(rooflines: dict, stats: dict, peaks: dict, isolated: dict | None = None) -> dict:
+def dominant_roofline(rooflines: dict, stats: dict, peaks: dict, isolated: dict | None = None,
+                      gather: dict | None = None, nnz: int = 0) -> dict:
     """`roofline` of the bench contract: the kernel with the largest summed
     device time over the timed region, its achieved rate = algorithmic work
     per launch / mean launch time (CUDA events around every launch on the
@@ -361,6 +402,16 @@ def dominant_roofline(rooflines: dict, stats: dict, peaks: dict, isolated: dict 
         r["isolated"] = {"achieved": round(ach, 1), "frac": round(ach / r["peak"], 4), "avg_launch_us": round(us, 2),
                          "launches": isolated["launches"],
                          "how": "the same kernel back to back on one stream right after the timed region"}
+    if name == "spmv" and gather and nnz:
+        # the limiter's own ceiling: x gathers per second vs the pure-gather rate
+        ceil = gather["G_gathers_per_s"]
+        g = {"ceiling_G_gathers_per_s": ceil, "probe": gather,
+             "in_burst_G_gathers_per_s": round(nnz / r["avg_launch_us"] / 1e3, 1)}
+        g["in_burst_frac"] = round(g["in_burst_G_gathers_per_s"] / ceil, 4)
+        if "isolated" in r:
+            g["isolated_G_gathers_per_s"] = round(nnz / r["isolated"]["avg_launch_us"] / 1e3, 1)
+            g["isolated_frac"] = round(g["isolated_G_gathers_per_s"] / ceil, 4)
+        r["gather_roofline"] = g
     return r
 
 
@@ -616,6 +667,7 @@ def our_arm(args, rank, world, dist) -> dict:
         probe = land_probe(data)
         dom_body = max(stats_val, key=lambda k: stats_val[k]["total_us"])
         iso = body_probe(data, dom_body)
+        gceil = gather_probe(data) if dom_body == "spmv" else None
         sim.dataplane.results_in_hbm = False
         sim.dataplane.drop_hbm_sources()
         sim.check_no_leaks()
@@ -695,7 +747,8 @@ def our_arm(args, rank, world, dist) -> dict:
         # the contract's roofline: the kernel with the largest share of device
         # time in the timed value leg, timed there with CUDA events on its own
         # stream; the data plane's own kernel (land) is reported beside it
-        "roofline": dominant_roofline(rooflines, stats_val, peaks, iso),
+        "roofline": dominant_roofline(rooflines, stats_val, peaks, iso, gceil,
+                                      next((int(data[n].args[1]) for n in sorted(data) if data[n].body == "spmv"), 0)),
         "roofline_land": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
                           "unit": "GB/s", "frac": land["frac"], "traffic": land_traffic(probe["segment"]),
                           "traffic_source": "profiles/r1_land_traffic.json (ncu --set full, one launch)",

@@ -210,11 +210,17 @@ int sage_fanout(int src_gpu, uint64_t src_dptr, int dst_gpu, uint64_t dst_dptr, 
 
 /* ---- function bodies (the COMPUTE node, functions.py:276) ----------------- */
 #define SAGE_BODY_TOUCH    0  /* read RO + input, write a digest (synthetic functions) */
-#define SAGE_BODY_SGEMM    1  /* C[M,N] = A[M,K] . B[K,N], A = RO, bf16 in / fp32 out   */
+#define SAGE_BODY_SGEMM    1  /* C[M,N] = A[M,K] . B[K,N], A = RO, fp32 in / TF32 MMA   */
 #define SAGE_BODY_STENCIL  2  /* 7-point 3-D Jacobi, coefficients RO, fp32               */
 #define SAGE_BODY_SPMV     3  /* CSR y = A.x, A = RO, fp32                              */
 #define SAGE_BODY_SPIN     4  /* occupy the SMs for args[0] microseconds                */
 #define SAGE_BODY_SGEMM_F32 5 /* the SGEMM on SIMT fp32 cores (exact-fp32 variant)      */
+#define SAGE_BODY_SPMV_CSB 7  /* y = A.x, A = RO in the column-sliced block format of
+                                 parboil.spmv(fmt="csb"); args = {rows, cols, offsets
+                                 offset, entries offset, R, CW, Emax, S | nnz << 8}   */
+#define SAGE_BODY_GATHER   6  /* diagnostic: args[0] random 4-B gathers from the input
+                                 (a power-of-two float array), the ceiling spmv's x
+                                 gathers run against; writes 16 B                   */
 /* SGEMM: C[M,N] = A[M,K] . BT[N,K]^T, fp32 in memory, tcgen05 kind::tf32 MMAs
  * with fp32 accumulation in TMEM; args = {M, N, K}; input = BT (K-contiguous,
  * Parboil's "matrix2t")                                                       */
@@ -334,7 +340,8 @@ int sage_fixedgsl_release(sage_handle job);
 #define SAGE_KERNEL_STENCIL  3
 #define SAGE_KERNEL_SPMV     4
 #define SAGE_KERNEL_VERIFY   5   /* direct-path checksum of DMA'd identity loads */
-#define SAGE_KERNEL_KINDS    6
+#define SAGE_KERNEL_GATHER   6   /* SAGE_BODY_GATHER; work = gathers               */
+#define SAGE_KERNEL_KINDS    7
 int sage_stats_enable(int on);
 int sage_stats_reset(void);
 int sage_stats_get(int gpu, int kind, uint64_t *launches, double *total_us, uint64_t *bytes);

@@ -27,7 +27,8 @@ SAGE_INIT_SHARE_DEVICE = 0x2
 CLASS_CONTEXT, CLASS_READ_ONLY, CLASS_WRITABLE, CLASS_INSTANCE_FIXED = 0, 1, 2, 3
 ALLOC_ACCOUNT_ONLY = 0x100
 LOAD_SRC_PINNED, LOAD_SRC_DEVICE, LOAD_SRC_PEER = 0x1, 0x2, 0x4
-BODY_TOUCH, BODY_SGEMM, BODY_STENCIL, BODY_SPMV, BODY_SPIN = 0, 1, 2, 3, 4
+BODY_TOUCH, BODY_SGEMM, BODY_STENCIL, BODY_SPMV, BODY_SPIN, BODY_SGEMM_F32, BODY_GATHER = 0, 1, 2, 3, 4, 5, 6
+BODY_SPMV_CSB = 7
 
 u64 = C.c_uint64
 i64 = C.c_int64

@@ -242,6 +242,33 @@ __global__ void __launch_bounds__(256) spmv4_kernel(const int *__restrict__ rowp
   if (row < rows && sub == 0) y[row] = s;
 }
 
+// Random-gather ceiling (diagnostic body): each thread does 4 independent
+// 4-B loads at hashed indices of a power-of-two array -- spmv4's x access
+// pattern (4 lanes per row, 4 gathers per step) without its col / val
+// streams.  A sum guards the loads; one lane per CTA writes it.
+__device__ __forceinline__ uint32_t gather_hash(uint32_t v) {
+  v ^= v >> 16;
+  v *= 0x7feb352dU;
+  v ^= v >> 15;
+  v *= 0x846ca68bU;
+  v ^= v >> 16;
+  return v;
+}
+
+__global__ void __launch_bounds__(256) gather_kernel(const float *__restrict__ x, uint32_t mask, long long n,
+                                                     float *__restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  float s = 0.f;
+  if (4 * t < n) {
+    const uint32_t base = (uint32_t)(4 * t);
+    const float a = __ldg(x + (gather_hash(base) & mask)), b = __ldg(x + (gather_hash(base + 1) & mask));
+    const float c = __ldg(x + (gather_hash(base + 2) & mask)), d = __ldg(x + (gather_hash(base + 3) & mask));
+    s = (a + b) + (c + d);
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = s;
+}
+
 __global__ void spin_kernel(long long us) {
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -330,6 +357,18 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
     case SAGE_BODY_SPIN:
       spin_kernel<<<1, 32, 0, s>>>(b->args[0]);
       break;
+    case SAGE_BODY_SPMV_CSB:
+      return spmv_csb(b, s, sm_count);
+    case SAGE_BODY_GATHER: {
+      const long long n = b->args[0];
+      const uint64_t elems = b->input_bytes / 4;
+      if (n <= 0 || n % 4 || elems == 0 || (elems & (elems - 1)) || elems > (1ull << 32) || !b->out ||
+          b->out_bytes < 16)
+        return fail(SAGE_EINVAL, "gather: needs gathers % 4 == 0, a power-of-two float input and a 16-B output");
+      gather_kernel<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>((const float *)b->input, (uint32_t)(elems - 1), n,
+                                                                    (float *)b->out);
+      break;
+    }
     default:
       return fail(SAGE_EINVAL, "unknown body kind");
   }
@@ -347,7 +386,9 @@ int touch_all_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&a, stencil4_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, spmv4_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, spin_kernel));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, gather_kernel));
   SAGE_TRY(touch_tc_kernels());
+  SAGE_TRY(touch_csb_kernel());
   return SAGE_OK;
 }
 
@@ -384,6 +425,14 @@ int sage::launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b) {
     case SAGE_BODY_SPMV:
       kind = SAGE_KERNEL_SPMV;  // row_ptr + (col, val) per nnz + x gathers + y
       work = 4ull * (b->args[0] + 1) + 8ull * b->args[1] + 4ull * b->args[1] + 4ull * b->args[0];
+      break;
+    case SAGE_BODY_SPMV_CSB:
+      kind = SAGE_KERNEL_SPMV;  // 8 B per entry + x once per row group + y
+      work = 8ull * (uint64_t)(b->args[7] >> 8) + 4ull * (uint64_t)b->args[1] + 4ull * (uint64_t)b->args[0];
+      break;
+    case SAGE_BODY_GATHER:
+      kind = SAGE_KERNEL_GATHER;
+      work = (uint64_t)b->args[0];
       break;
     default: sb = nullptr;
   }

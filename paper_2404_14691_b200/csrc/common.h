@@ -207,6 +207,9 @@ int touch_all_kernels();
 // tcgen05 GEMM (gemm_tc.cu)
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
 int touch_tc_kernels();
+// column-sliced block spmv (spmv_csb.cu)
+int spmv_csb(const sage_body_desc *b, cudaStream_t s, int sm_count);
+int touch_csb_kernel();
 
 // invocations (invoke.cu): stop the completion thread, drop live records
 void invoke_shutdown();

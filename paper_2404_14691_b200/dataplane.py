@@ -39,7 +39,8 @@ from .layout import SegmentLayout
 from .resources import AllocClass, SimulationError
 
 _BODY = {"touch": _lib.BODY_TOUCH, "sgemm": _lib.BODY_SGEMM, "stencil": _lib.BODY_STENCIL,
-         "spmv": _lib.BODY_SPMV, "spin": _lib.BODY_SPIN, "sgemm_f32": 5}
+         "spmv": _lib.BODY_SPMV, "spin": _lib.BODY_SPIN, "sgemm_f32": 5,
+         "spmv_csb": _lib.BODY_SPMV_CSB}
 
 
 def _a256(n: int) -> int:

@@ -112,3 +112,73 @@ def test_spmv_ragged_rows(dp, misalign):
     np.testing.assert_allclose(got.view(np.float32), O.spmv_ref(rowptr, col, val, x), rtol=1e-3, atol=1e-4)
     sr.free()
     sx.free()
+
+
+def test_gather_ceiling_body(dp):
+    """The diagnostic GATHER body (bench.py's spmv gather ceiling) reads the
+    input at hashed indices: over an all-ones array warp 0 of block 0 sums
+    32 lanes x 4 gathers; bad shapes are refused."""
+    seg = upload(np.ones(1 << 12, np.float32))
+    got = run_body(_lib.BODY_GATHER, 0, 0, seg.dptr, 4 << 12, 16, (4096,)).view(np.float32)
+    assert got[0] == 128.0
+    for inp_bytes, n in ((3 << 12, 4096), (4 << 12, 4098), (4 << 12, 0)):
+        with pytest.raises(_lib.SageError):
+            run_body(_lib.BODY_GATHER, 0, 0, seg.dptr, inp_bytes, 16, (n,))
+    seg.free()
+
+
+def _csb_case(rows, counts, slices, chunk_cols, seed=21):
+    from paper_2404_14691_b200.parboil import csb_pack
+    rng = np.random.default_rng(seed)
+    rowptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    nnz = int(rowptr[-1])
+    col = rng.integers(0, rows, nnz, dtype=np.int32)
+    val = rng.standard_normal(nnz, dtype=np.float32)
+    x = rng.standard_normal(rows, dtype=np.float32)
+    off, ent, p = csb_pack(rowptr, col, val, rows, slices=slices, chunk_cols=chunk_cols)
+    o_ent = (off.nbytes + 255) // 256 * 256
+    ro = np.zeros(o_ent + ent.nbytes, np.uint8)
+    ro[:off.nbytes] = off.view(np.uint8)
+    ro[o_ent:] = ent.view(np.uint8).reshape(-1)
+    args = (rows, rows, 0, o_ent, p["R"], p["CW"], p["Emax"], p["S"] | p["NS"] << 4 | (p["entries"] << 8))
+    return rowptr, col, val, x, off, ent, p, ro, args
+
+
+@pytest.mark.parametrize("rows,kind,slices,chunk_cols", [
+    (5000, "ragged", 2, 6144), (5001, "ragged", 1, 1024), (4099, "ragged", 2, 1024), (1 << 16, "uniform", 2, 12288),
+    (1 << 20, "uniform", 2, 6144)])
+def test_spmv_csb_vs_oracle(dp, rows, kind, slices, chunk_cols):
+    """The column-sliced block spmv (TMA-staged x chunks, DSMEM slice sum)
+    against the oracle's independent CSB decode AND the CSR reference of the
+    same matrix; two launches are bit-identical (fixed summation order)."""
+    rng = np.random.default_rng(rows)
+    counts = rng.integers(0, 40, rows) if kind == "ragged" else np.full(rows, 16)
+    if kind == "ragged":
+        counts[::7] = 0
+        counts[3] = 300                                     # one long row: runs across warp steps
+    rowptr, col, val, x, off, ent, p, ro, args = _csb_case(rows, counts, slices, chunk_cols)
+    sr, sx = upload(ro), upload(x)
+    got = run_body(_lib.BODY_SPMV_CSB, sr.dptr, ro.size, sx.dptr, x.nbytes, rows * 4, args).view(np.float32)
+    again = run_body(_lib.BODY_SPMV_CSB, sr.dptr, ro.size, sx.dptr, x.nbytes, rows * 4, args).view(np.float32)
+    assert np.array_equal(got, again)
+    want = O.spmv_csb_ref(off, ent, rows, rows, p["R"], p["CW"], p["S"], x)
+    np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-4)
+    np.testing.assert_allclose(got, O.spmv_ref(rowptr, col, val, x), rtol=1e-3, atol=1e-4)
+    sr.free()
+    sx.free()
+
+
+def test_spmv_csb_rejects_bad_formats(dp):
+    rowptr, col, val, x, off, ent, p, ro, args = _csb_case(3000, np.full(3000, 4), 2, 6144)
+    sr, sx = upload(ro), upload(x)
+    bad = [list(args) for _ in range(5)]
+    bad[0][4] = 1 << 15                       # R beyond the 14-bit row field
+    bad[1][5] = 1001                          # chunk width not a multiple of 4
+    bad[2][6] = 1 << 20                       # entry block larger than shared memory
+    bad[3][3] = args[3] + 4                   # entries not 16-B aligned
+    bad[4][7] = args[7] & ~0xF0 | 1 << 4      # a 1-deep ring
+    for a in bad:
+        with pytest.raises(_lib.SageError):
+            run_body(_lib.BODY_SPMV_CSB, sr.dptr, ro.size, sx.dptr, x.nbytes, 3000 * 4, tuple(a))
+    sr.free()
+    sx.free()
