@@ -219,6 +219,17 @@ void issuer_drain(int gpu);
 
 // sage_segment_load with an optional pre-created END event (land.cu)
 int segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev, sage_handle pre_end);
+// ... in pieces: open validates, creates the events and applies the waits;
+// a load that is not staged through the ring completes inside open (*cur ==
+// nullptr, handles out).  Otherwise each step enqueues chunks until `budget`
+// link bytes moved (piece_ev: recorded after the piece's last H2D) and the
+// last one sets *done and hands out the handles.
+struct LoadCursor;
+int segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCursor **cur, sage_handle *load_out,
+                      sage_handle *end_ev);
+int segment_load_step(LoadCursor *c, uint64_t budget, uint64_t *bytes, sage_handle *piece_ev, bool *done,
+                      sage_handle *load_out, sage_handle *end_ev);
+void segment_load_close(LoadCursor *c);
 
 // layouts (land.cu)
 int layouts_destroy_all();

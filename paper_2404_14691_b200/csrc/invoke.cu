@@ -19,15 +19,22 @@
 // thread instead.  The issuer keeps at most `lookahead` bytes of H2D queued
 // per GPU and, whenever there is room, enqueues the ready invocation (every
 // event it waits on already recorded) with the smallest H2D - D2H balance,
-// FIFO among equals, anything older than `max_defer` first.  Followers of a
+// FIFO among equals, anything older than `max_defer` first: followers of a
 // landed segment (balance ~0: their return traffic overlaps the next loads)
-// thus run between the chunks of the next cold load.  The events handed back
+// go before the next cold load.  Optionally (SAGE_ISSUE_PIECE_MB) a large
+// cold load staged through the ring is enqueued a piece at a time,
+// alternating with those followers.  The events handed back
 // are created at submit and recorded when the invocation is issued; waits on
 // them block until then.  Off the submitting thread, the ~30 us of CUDA
 // enqueue per invocation also overlaps the caller's admission work.
 //   SAGE_ISSUER=0              enqueue inline (admission order)
 //   SAGE_ISSUE_LOOKAHEAD_MB    H2D bytes kept queued per GPU (default 32)
 //   SAGE_ISSUE_MAX_DEFER_US    age that overrides the balance order (3000)
+//   SAGE_ISSUE_PIECE_MB        > 0: a staged (ring) RO load is enqueued in
+//                              pieces of this many MiB, alternating with the
+//                              followers of its GPU (0 = whole loads, default:
+//                              on the cfg-2 e2e burst 8 / 16 / 24 MiB pieces
+//                              measured 22.4 / 18.9 / 19.0 vs 18.6 ms)
 #include "common.h"
 
 namespace sage {
@@ -44,6 +51,12 @@ struct Inv {
   sage_invoke_desc d{};                 // the submitted descriptor (waits -> hold)
   int64_t t_enqueue = 0;
   int64_t h2d = 0, d2h = 0;             // PCIe bytes each way (issue order)
+  // issue state across pieces (the RO load of a cold leader may be enqueued
+  // in pieces, other invocations' copies in between)
+  Gpu *G = nullptr;
+  cudaStream_t s = nullptr;
+  sage_handle last = 0;                 // the stage boundary most recently recorded on s
+  LoadCursor *ro_cur = nullptr;         // staged RO load still being enqueued
   std::atomic<bool> issued{false};
   std::string err;                      // issue failure (reported by collect)
   sage_invoke_info info{};
@@ -244,39 +257,64 @@ static int submit_prepare(Inv *I) {
   return SAGE_OK;
 }
 
-// enqueue the whole Parallel DAG of one invocation (admission order when
-// inline, the issuer's order otherwise)
-static int issue(Inv *I) {
+// Enqueue the Parallel DAG of one invocation in three parts: issue_head
+// (GPU_CTX, open the RO load), issue_ro_piece (enqueue the staged RO load's
+// chunks, all at once or a piece at a time) and issue_tail (input, SYNC_WAIT,
+// COMPUTE, RETURN).  Admission order when inline, the issuer's otherwise.
+// Stage boundaries on the slot stream are shared: the event that ends one
+// stage also begins the next (one record + one time read instead of two).
+static int rec_on(Inv *I, sage_handle *h) {
+  Event *e;
+  SAGE_TRY(event_new(I->d.gpu, h, &e));
+  return event_record(e, I->s);
+}
+static int rec_pre_on(Inv *I, sage_handle pre, sage_handle *h) {
+  SAGE_TRY(event_alias(pre, h));
+  return event_record(event_get(pre), I->s);
+}
+
+// any failure: waiters on this invocation's events must not hang -- record
+// whatever was handed out and never reached (followers then fail their own
+// checks); nothing may still reference I afterwards
+static void issue_abort(Inv *I) {
+  const sage_invoke_desc *d = &I->d;
+  if (I->ro_cur) {
+    segment_load_close(I->ro_cur);
+    I->ro_cur = nullptr;
+  }
+  Gpu *H = I->G ? I->G : gpu_get(d->gpu);
+  cudaSetDevice(dev_of(d->gpu));
+  for (sage_handle h : {I->pre_ro, I->pre_ctx, I->pre_done}) {
+    Event *e = h ? event_get(h) : nullptr;
+    if (e && !e->recorded.load() && H) event_record(e, H->aux);
+  }
+  cudaDeviceSynchronize();
+}
+
+static void issue_release_holds(Inv *I) {
+  for (int i = 0; i < 6; ++i)
+    if (I->hold[i]) { sage_event_release(I->hold[i]); I->hold[i] = 0; }
+  I->issued.store(true, std::memory_order_release);
+}
+
+static int issue_head(Inv *I) {
   const sage_invoke_desc *d = &I->d;
   int rc = sage_ctx_acquire(d->gpu, &I->slot);
-  Gpu *G = nullptr;
-  cudaStream_t s = nullptr;
-  if (rc == SAGE_OK) rc = slot_stream(I->slot, &G, &s);
-  if (rc == SAGE_OK) cudaSetDevice(G->dev);
-  // Stage boundaries on the slot stream are shared: the event that ends one
-  // stage also begins the next (one record + one time read instead of two).
-  auto rec = [&](sage_handle *h) -> int {
-    Event *e;
-    SAGE_TRY(event_new(d->gpu, h, &e));
-    return event_record(e, s);
-  };
-  auto rec_pre = [&](sage_handle pre, sage_handle *h) -> int {
-    SAGE_TRY(event_alias(pre, h));
-    return event_record(event_get(pre), s);
-  };
-  sage_handle last = 0;  // the boundary most recently recorded on s
+  if (rc == SAGE_OK) rc = slot_stream(I->slot, &I->G, &I->s);
+  if (rc == SAGE_OK) cudaSetDevice(I->G->dev);
+  I->last = 0;
   // GPU_CTX: bind the function context on the invocation's pooled stream
   // (zero its 64 KiB header: descriptor table, scratch counters)
   if (rc == SAGE_OK && (d->flags & SAGE_INV_CTX)) {
-    rc = rec(&I->ctx_b);
+    rc = rec_on(I, &I->ctx_b);
     if (rc == SAGE_OK && d->ctx_dptr && d->ctx_bytes) {
-      cudaError_t e = cudaMemsetAsync((void *)d->ctx_dptr, 0, std::min<uint64_t>(d->ctx_bytes, 64 << 10), s);
+      cudaError_t e = cudaMemsetAsync((void *)d->ctx_dptr, 0, std::min<uint64_t>(d->ctx_bytes, 64 << 10), I->s);
       if (e != cudaSuccess) rc = cuda_fail(e, "ctx bind memset");
     }
-    if (rc == SAGE_OK) rc = rec_pre(I->pre_ctx, &I->ctx_e);
-    last = I->ctx_e;
+    if (rc == SAGE_OK) rc = rec_pre_on(I, I->pre_ctx, &I->ctx_e);
+    I->last = I->ctx_e;
   }
-  // CPU_LOAD -> GPU_LOAD: the read-only segment ...
+  // CPU_LOAD -> GPU_LOAD: the read-only segment (a staged load stays open)
   if (rc == SAGE_OK && (d->flags & SAGE_INV_RO)) {
     sage_load_desc L{};
     L.gpu = d->gpu;
@@ -288,10 +326,29 @@ static int issue(Inv *I) {
     L.wait = d->ro_wait;
     L.n_wait = d->n_ro_wait;
     L.src_gpu = d->ro_src_gpu;
-    rc = segment_load(&L, &I->ro_load, &I->ro_end, I->pre_ro);
+    rc = segment_load_open(&L, I->pre_ro, &I->ro_cur, &I->ro_load, &I->ro_end);
   }
+  return rc;
+}
+
+// enqueue up to `budget` bytes of the open RO load; *done once it is complete
+static int issue_ro_piece(Inv *I, uint64_t budget, uint64_t *bytes, sage_handle *piece_ev, bool *done) {
+  int rc = segment_load_step(I->ro_cur, budget, bytes, piece_ev, done, &I->ro_load, &I->ro_end);
+  if (rc != SAGE_OK || *done) {
+    segment_load_close(I->ro_cur);
+    I->ro_cur = nullptr;
+  }
+  return rc;
+}
+
+static int issue_tail(Inv *I) {
+  const sage_invoke_desc *d = &I->d;
+  Gpu *G = I->G;
+  cudaStream_t s = I->s;
+  cudaSetDevice(G->dev);
+  int rc = SAGE_OK;
   // ... and the invocation input (identity layout)
-  if (rc == SAGE_OK && (d->flags & SAGE_INV_INPUT)) {
+  if (d->flags & SAGE_INV_INPUT) {
     sage_load_desc L{};
     L.gpu = d->gpu;
     L.flags = load_flags(d->in_kind);
@@ -308,19 +365,20 @@ static int issue(Inv *I) {
   // leader tokens (SYNC_WAIT) and the compute-gate predecessor: COMPUTE waits
   // on all of them; only a SYNC_WAIT plan node records the stage
   for (int i = 0; i < d->n_wait && i < 4; ++i) deps[nd++] = d->wait[i];
+  sage_handle last = I->last;
   if (rc == SAGE_OK && (d->flags & SAGE_INV_SYNC)) {
-    rc = last ? event_alias(last, &I->sync_b) : rec(&I->sync_b);
+    rc = last ? event_alias(last, &I->sync_b) : rec_on(I, &I->sync_b);
     if (rc == SAGE_OK) rc = wait_events(s, deps, nd);
-    if (rc == SAGE_OK) rc = rec(&I->sync_e);
+    if (rc == SAGE_OK) rc = rec_on(I, &I->sync_e);
     last = I->sync_e;
   } else if (rc == SAGE_OK && nd) {
     rc = wait_events(s, deps, nd);
     last = 0;  // COMPUTE begins when the joins clear, not at the last boundary
   }
   // COMPUTE
-  if (rc == SAGE_OK) rc = last ? event_alias(last, &I->comp_b) : rec(&I->comp_b);
+  if (rc == SAGE_OK) rc = last ? event_alias(last, &I->comp_b) : rec_on(I, &I->comp_b);
   if (rc == SAGE_OK) rc = launch_timed(G, s, &d->body);
-  if (rc == SAGE_OK) rc = rec(&I->comp_e);
+  if (rc == SAGE_OK) rc = rec_on(I, &I->comp_e);
   // RETURN
   if (rc == SAGE_OK) rc = return_enqueue(G, s, I->comp_e, d->ret_src, d->ret_dst, d->ret_bytes,
                                         (d->flags & SAGE_INV_RET_HOST) != 0, &I->ret_b, &I->ret_e, I->pre_done);
@@ -331,20 +389,19 @@ static int issue(Inv *I) {
     cudaError_t e = re ? cudaStreamWaitEvent(s, re->ev, 0) : cudaErrorInvalidResourceHandle;
     if (e != cudaSuccess) rc = cuda_fail(e, "invoke completion wait");
   }
-  if (rc != SAGE_OK) {
-    // waiters on this invocation's events must not hang: record whatever was
-    // handed out and never reached (followers then fail their own checks)
-    Gpu *H = G ? G : gpu_get(d->gpu);
-    cudaSetDevice(dev_of(d->gpu));
-    for (sage_handle h : {I->pre_ro, I->pre_ctx, I->pre_done}) {
-      Event *e = h ? event_get(h) : nullptr;
-      if (e && !e->recorded.load() && H) event_record(e, H->aux);
-    }
-    cudaDeviceSynchronize();  // error path only: nothing may still reference I
+  return rc;
+}
+
+// the whole invocation at once (inline path)
+static int issue(Inv *I) {
+  int rc = issue_head(I);
+  if (rc == SAGE_OK && I->ro_cur) {
+    bool done = false;
+    rc = issue_ro_piece(I, UINT64_MAX, nullptr, nullptr, &done);
   }
-  for (int i = 0; i < 6; ++i)
-    if (I->hold[i]) { sage_event_release(I->hold[i]); I->hold[i] = 0; }
-  I->issued.store(true, std::memory_order_release);
+  if (rc == SAGE_OK) rc = issue_tail(I);
+  if (rc != SAGE_OK) issue_abort(I);
+  issue_release_holds(I);
   return rc;
 }
 
@@ -364,6 +421,7 @@ std::mutex iss_mu;
 std::condition_variable iss_cv;       // work arrived / stop
 std::condition_variable iss_idle_cv;  // something was issued
 std::deque<Inv *> iss_q;              // submitted, not yet issued (submit order)
+std::deque<Inv *> iss_open;           // head issued, staged RO load still being enqueued
 int iss_busy = 0;                     // being issued right now
 bool iss_stop = false;
 std::thread *issuer = nullptr;
@@ -408,14 +466,63 @@ static void complete_failed(Inv *I, int rc, const std::string &msg) {
   fprintf(stderr, "sage: invocation %llu failed at issue: %s\n", (unsigned long long)I->id, msg.c_str());
 }
 
+// add an H2D flight (bytes in the copy queue until `ev` completes)
+static void flight_add(std::deque<Flight> &flights, sage_handle ev_alias_of, int64_t bytes, int gpu) {
+  Flight f{0, bytes, gpu};
+  if (event_alias(ev_alias_of, &f.ev) == SAGE_OK) flights.push_back(f);
+}
+
+// Issue one step of invocation I: a fresh invocation gets its head (and the
+// first piece of a staged RO load); an invocation with an open RO load gets
+// its next piece.  Returns true when I is fully issued (or failed).
+static bool issue_step(Inv *I, int64_t piece, std::deque<Flight> &flights) {
+  const sage_invoke_desc &d = I->d;
+  const bool fresh = I->G == nullptr && !I->ro_cur;
+  int rc = SAGE_OK;
+  if (fresh) {
+    rc = issue_head(I);
+    if (rc == SAGE_OK && !I->ro_cur && I->ro_end && (d.flags & SAGE_INV_RO) && pcie_kind(d.ro_kind))
+      flight_add(flights, I->ro_end, (int64_t)d.ro_src_bytes, I->gpu);
+  }
+  if (rc == SAGE_OK && I->ro_cur) {
+    uint64_t moved = 0;
+    sage_handle pev = 0;
+    bool done = false;
+    rc = issue_ro_piece(I, piece > 0 ? (uint64_t)piece : UINT64_MAX, &moved, &pev, &done);
+    if (pev) {
+      if (moved) {
+        Flight f{pev, (int64_t)moved, I->gpu};
+        flights.push_back(f);
+      } else {
+        sage_event_release(pev);
+      }
+    }
+    if (rc == SAGE_OK && !done) return false;   // more pieces to come
+  }
+  if (rc == SAGE_OK) {
+    rc = issue_tail(I);
+    if (rc == SAGE_OK && I->in_end && (d.flags & SAGE_INV_INPUT) && pcie_kind(d.in_kind))
+      flight_add(flights, I->in_end, (int64_t)d.in_bytes, I->gpu);
+  }
+  if (rc != SAGE_OK) issue_abort(I);
+  issue_release_holds(I);
+  if (rc == SAGE_OK) rc = issue_notify(I);
+  if (rc != SAGE_OK) complete_failed(I, rc, sage_last_error());   // (I may be released from here on)
+  return true;
+}
+
 static void issuer_main() {
   const int64_t lookahead = env_i64("SAGE_ISSUE_LOOKAHEAD_MB", 32) << 20;
   const int64_t max_defer = env_i64("SAGE_ISSUE_MAX_DEFER_US", 3000);
+  const int64_t piece = env_i64("SAGE_ISSUE_PIECE_MB", 0) << 20;
   std::deque<Flight> flights;   // H2D queued by this thread, not yet landed
   std::vector<int64_t> pending;
+  std::vector<char> piece_turn; // per GPU: the next slot goes to an open staged load
+  int rr = 0;                   // GPU the next pick starts looking at
   for (;;) {
     // retire landed H2D (issuer-only state, no lock)
     pending.assign(st.gpus.size() + 1, 0);
+    if (piece_turn.size() < pending.size()) piece_turn.resize(pending.size(), 1);
     for (auto it = flights.begin(); it != flights.end();) {
       if (sage_event_query(it->ev) != SAGE_ENOTREADY) {
         sage_event_release(it->ev);
@@ -428,7 +535,7 @@ static void issuer_main() {
     Inv *pick = nullptr;
     {
       std::unique_lock<std::mutex> lk(iss_mu);
-      if (iss_q.empty()) {
+      if (iss_q.empty() && iss_open.empty()) {
         if (iss_stop) break;
         if (flights.empty()) {
           iss_cv.wait(lk, [] { return iss_stop || !iss_q.empty(); });
@@ -438,40 +545,66 @@ static void issuer_main() {
         continue;
       }
       const int64_t now = host_now_us();
-      auto best = iss_q.end();
-      int64_t best_key = INT64_MAX;
-      for (auto it = iss_q.begin(); it != iss_q.end(); ++it) {
-        Inv *I = *it;
-        if (!inv_ready(I)) continue;
-        if (I->h2d > 0 && pending[I->gpu] > 0 && pending[I->gpu] >= lookahead) continue;   // PCIe queue full
-        if (now - I->t_enqueue >= max_defer) { best = it; break; }                         // overdue: FIFO
-        const int64_t key = I->h2d - I->d2h;
-        if (key < best_key) { best_key = key; best = it; }
+      auto room = [&](int gpu) { return pending[gpu] <= 0 || pending[gpu] < lookahead; };
+      // Per GPU, in rotation: an open staged load alternates with the
+      // followers (ready invocations whose H2D - D2H balance is within one
+      // piece: their returns keep D2H busy while the load crosses H2D);
+      // with no open load, the smallest waiting cold load opens next (its
+      // followers become ready as soon as it is enqueued), else the
+      // follower with the smallest balance (FIFO among equals, overdue first).
+      // SAGE_ISSUE_PIECE_MB=0: whole loads, balance order only.
+      const int ng = (int)pending.size();
+      for (int k = 0; k < ng && !pick; ++k) {
+        const int g = (rr + k) % ng;
+        if (!room(g)) continue;
+        auto open = iss_open.end();
+        for (auto it = iss_open.begin(); it != iss_open.end(); ++it)
+          if ((*it)->gpu == g) { open = it; break; }
+        auto fol = iss_q.end(), cold = iss_q.end();
+        int64_t fol_key = INT64_MAX, cold_key = INT64_MAX;
+        bool fol_overdue = false;
+        for (auto it = iss_q.begin(); it != iss_q.end(); ++it) {
+          Inv *I = *it;
+          if (I->gpu != g || !inv_ready(I)) continue;
+          const int64_t key = I->h2d - I->d2h;
+          if (piece > 0 && key > piece) {
+            if (key < cold_key) { cold_key = key; cold = it; }
+          } else if (!fol_overdue) {
+            if (now - I->t_enqueue >= max_defer) { fol = it; fol_overdue = true; }
+            else if (key < fol_key) { fol_key = key; fol = it; }
+          }
+        }
+        if (open != iss_open.end()) {
+          if (!piece_turn[g] && fol != iss_q.end()) {
+            pick = *fol;
+            iss_q.erase(fol);
+            piece_turn[g] = 1;
+          } else {
+            pick = *open;
+            iss_open.erase(open);
+            piece_turn[g] = 0;
+          }
+        } else if (cold != iss_q.end()) {
+          pick = *cold;
+          iss_q.erase(cold);
+          piece_turn[g] = 0;
+        } else if (fol != iss_q.end()) {
+          pick = *fol;
+          iss_q.erase(fol);
+          piece_turn[g] = 1;
+        }
       }
-      if (best == iss_q.end()) {
+      if (!pick) {
         iss_cv.wait_for(lk, std::chrono::microseconds(20));
         continue;
       }
-      pick = *best;
-      iss_q.erase(best);
+      rr = (pick->gpu + 1) % ng;
       ++iss_busy;
     }
-    int rc = issue(pick);
-    if (rc == SAGE_OK && pick->h2d > 0) {
-      const sage_invoke_desc &d = pick->d;
-      if (pick->ro_end && (d.flags & SAGE_INV_RO) && pcie_kind(d.ro_kind)) {
-        Flight f{0, (int64_t)d.ro_src_bytes, pick->gpu};
-        if (event_alias(pick->ro_end, &f.ev) == SAGE_OK) flights.push_back(f);
-      }
-      if (pick->in_end && (d.flags & SAGE_INV_INPUT) && pcie_kind(d.in_kind)) {
-        Flight f{0, (int64_t)d.in_bytes, pick->gpu};
-        if (event_alias(pick->in_end, &f.ev) == SAGE_OK) flights.push_back(f);
-      }
-    }
-    if (rc == SAGE_OK) rc = issue_notify(pick);
-    if (rc != SAGE_OK) complete_failed(pick, rc, sage_last_error());   // (pick may be released from here on)
+    const bool finished = issue_step(pick, piece, flights);
     {
       std::lock_guard<std::mutex> lk(iss_mu);
+      if (!finished) iss_open.push_back(pick);
       --iss_busy;
     }
     iss_idle_cv.notify_all();
@@ -496,6 +629,8 @@ void issuer_drain(int gpu) {
   iss_idle_cv.wait(lk, [gpu] {
     if (iss_busy) return false;
     for (Inv *I : iss_q)
+      if (gpu < 0 || I->gpu == gpu) return false;
+    for (Inv *I : iss_open)
       if (gpu < 0 || I->gpu == gpu) return false;
     return true;
   });

@@ -400,7 +400,113 @@ int sage_segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handl
 
 }  // extern "C"
 
+// A staged load being enqueued piece by piece (the issuer interleaves other
+// invocations' copies between the pieces of a large cold load).
+struct sage::LoadCursor {
+  Load *L = nullptr;
+  Gpu *G = nullptr;
+  const Plan *P = nullptr;
+  const uint8_t *src = nullptr;
+  uint8_t *dst = nullptr;
+  int gpu = -1;
+  bool pinned = false;
+  size_t next = 0;   // first chunk not yet enqueued
+};
+
+// Register a finished load: END on the land stream, handles out.
+static int load_finish(Load *L, Gpu *G, sage_handle *load_out, sage_handle *end_ev) {
+  if (!L->has_gpu_begin) SAGE_TRY(event_record(L->eb, G->land));
+  SAGE_TRY(event_record(L->ee, G->land));
+  SAGE_TRY(event_alias(L->he, end_ev));
+  uint64_t id = g_load_next++;
+  {
+    std::lock_guard<std::mutex> lk2(g_load_mu);
+    g_loads[id] = L;
+  }
+  *load_out = make_handle(Kind::Load, id);
+  return SAGE_OK;
+}
+
+// Enqueue the ring chunks of a staged (packed / pageable) load from
+// c->next on until at least `budget` bytes crossed the link or the plan is
+// done: CPU_LOAD (pageable only) -> H2D into a ring slot -> land.
+static int cursor_advance(LoadCursor *c, uint64_t budget, uint64_t *enq) {
+  Gpu *G = c->G;
+  Load *L = c->L;
+  const Plan &P = *c->P;
+  const uint64_t slot_bytes = G->chunk + 256;
+  uint64_t moved = 0;
+  int rc = SAGE_OK;
+  for (; c->next < P.chunks.size() && moved < budget; ++c->next) {
+    const size_t k = c->next;
+    const ChunkPlan &C = P.chunks[k];
+    const uint64_t n = C.se - C.sb;
+    const uint32_t r = (uint32_t)(G->chunk_seq++ % G->ring);
+    uint8_t *dslot = G->dstage + r * slot_bytes;
+    uint8_t *pslot = G->pin + r * slot_bytes;
+    const uint8_t *src = c->src + C.sb;
+    if (n) {
+      if (!c->pinned) {
+        // CPU_LOAD: DB record -> pinned staging, once the slot's last H2D is done
+        SAGE_CUDA(cudaStreamWaitEvent(G->host, G->ev_h2d[r], 0));
+        SAGE_CUDA(cudaLaunchHostFunc(G->host, host_copy_fn, new HostCopyArg{L, pslot, src, (size_t)n}));
+        SAGE_CUDA(cudaEventRecord(G->ev_cpu[r], G->host));
+        SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_cpu[r], 0));
+        L->host_bytes += n;
+      }
+      // GPU_LOAD: H2D into the device slot once its last land is done
+      SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_land[r], 0));
+      if (!L->has_gpu_begin) { SAGE_TRY(event_record(L->eb, G->copy)); L->has_gpu_begin = true; }
+      SAGE_CUDA(cudaMemcpyAsync(dslot, c->pinned ? src : pslot, n, cudaMemcpyHostToDevice, G->copy));
+      SAGE_CUDA(cudaEventRecord(G->ev_h2d[r], G->copy));
+      SAGE_CUDA(cudaStreamWaitEvent(G->land, G->ev_h2d[r], 0));
+      L->link_bytes += n;
+      moved += n;
+    } else if (!L->has_gpu_begin) {
+      SAGE_TRY(event_record(L->eb, G->land));
+      L->has_gpu_begin = true;
+    }
+    if ((rc = enqueue_land(G, P, C, c->gpu, dslot, c->dst, L->acc_idx, k + 1 == P.chunks.size())) != SAGE_OK)
+      return rc;
+    SAGE_CUDA(cudaEventRecord(G->ev_land[r], G->land));
+  }
+  if (enq) *enq = moved;
+  return SAGE_OK;
+}
+
+int sage::segment_load_step(LoadCursor *c, uint64_t budget, uint64_t *bytes, sage_handle *piece_ev, bool *done,
+                            sage_handle *load_out, sage_handle *end_ev) {
+  Gpu *G = c->G;
+  cudaSetDevice(G->dev);
+  std::lock_guard<std::mutex> lk(G->load_mu);   // ring order == enqueue order
+  uint64_t moved = 0;
+  SAGE_TRY(cursor_advance(c, budget, &moved));
+  if (bytes) *bytes = moved;
+  if (piece_ev) {   // marks the end of this piece's H2D (lookahead accounting)
+    Event *e;
+    SAGE_TRY(event_new(c->gpu, piece_ev, &e));
+    SAGE_TRY(event_record(e, G->copy));
+  }
+  *done = c->next >= c->P->chunks.size();
+  if (*done) SAGE_TRY(load_finish(c->L, G, load_out, end_ev));
+  return SAGE_OK;
+}
+
+void sage::segment_load_close(LoadCursor *c) { delete c; }
+
 int sage::segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev, sage_handle pre_end) {
+  LoadCursor *c = nullptr;
+  SAGE_TRY(segment_load_open(d, pre_end, &c, load_out, end_ev));
+  if (!c) return SAGE_OK;
+  bool done = false;
+  int rc = segment_load_step(c, UINT64_MAX, nullptr, nullptr, &done, load_out, end_ev);
+  segment_load_close(c);
+  return rc;
+}
+
+int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCursor **cur, sage_handle *load_out,
+                            sage_handle *end_ev) {
+  *cur = nullptr;
   SAGE_TRY(require_up());
   if (!d || !load_out || !end_ev) return fail(SAGE_EINVAL, "segment_load: null argument");
   Gpu *G = gpu_get(d->gpu);
@@ -513,54 +619,22 @@ int sage::segment_load(const sage_load_desc *d, sage_handle *load_out, sage_hand
       if (rc != SAGE_OK) return rc;
     }
   } else {
-    const Plan &P = lay->chunked;
     const bool pinned = (d->flags & SAGE_LOAD_SRC_PINNED) != 0;
-    const uint64_t slot_bytes = G->chunk + 256;
     if ((rc = wait_list(G->copy, d->wait, d->n_wait)) != SAGE_OK) return rc;
     if (!pinned && (rc = wait_list(G->host, d->wait, d->n_wait)) != SAGE_OK) return rc;
-    L->chunks = (uint32_t)P.chunks.size();
-    for (size_t k = 0; k < P.chunks.size(); ++k) {
-      const ChunkPlan &C = P.chunks[k];
-      const uint64_t n = C.se - C.sb;
-      const uint32_t r = (uint32_t)(G->chunk_seq++ % G->ring);
-      uint8_t *dslot = G->dstage + r * slot_bytes;
-      uint8_t *pslot = G->pin + r * slot_bytes;
-      const uint8_t *src = static_cast<const uint8_t *>(d->src) + C.sb;
-      if (n) {
-        if (!pinned) {
-          // CPU_LOAD: DB record -> pinned staging, once the slot's last H2D is done
-          SAGE_CUDA(cudaStreamWaitEvent(G->host, G->ev_h2d[r], 0));
-          SAGE_CUDA(cudaLaunchHostFunc(G->host, host_copy_fn, new HostCopyArg{L, pslot, src, (size_t)n}));
-          SAGE_CUDA(cudaEventRecord(G->ev_cpu[r], G->host));
-          SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_cpu[r], 0));
-          L->host_bytes += n;
-        }
-        // GPU_LOAD: H2D into the device slot once its last land is done
-        SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_land[r], 0));
-        if (!L->has_gpu_begin) { SAGE_TRY(event_record(Eb, G->copy)); L->has_gpu_begin = true; }
-        SAGE_CUDA(cudaMemcpyAsync(dslot, pinned ? src : pslot, n, cudaMemcpyHostToDevice, G->copy));
-        SAGE_CUDA(cudaEventRecord(G->ev_h2d[r], G->copy));
-        SAGE_CUDA(cudaStreamWaitEvent(G->land, G->ev_h2d[r], 0));
-        L->link_bytes += n;
-      } else if (!L->has_gpu_begin) {
-        SAGE_TRY(event_record(Eb, G->land));
-        L->has_gpu_begin = true;
-      }
-      if ((rc = enqueue_land(G, P, C, d->gpu, dslot, dst, L->acc_idx, k + 1 == P.chunks.size())) != SAGE_OK)
-        return rc;
-      SAGE_CUDA(cudaEventRecord(G->ev_land[r], G->land));
-    }
+    L->chunks = (uint32_t)lay->chunked.chunks.size();
+    auto *c = new LoadCursor();
+    c->L = L;
+    c->G = G;
+    c->P = &lay->chunked;
+    c->src = static_cast<const uint8_t *>(d->src);
+    c->dst = dst;
+    c->gpu = d->gpu;
+    c->pinned = pinned;
+    *cur = c;   // the chunks are enqueued by segment_load_step
+    return SAGE_OK;
   }
-  if (!L->has_gpu_begin) SAGE_TRY(event_record(Eb, G->land));
-  SAGE_TRY(event_record(Ee, G->land));
-  SAGE_TRY(event_alias(L->he, end_ev));
-  uint64_t id = g_load_next++;
-  {
-    std::lock_guard<std::mutex> lk2(g_load_mu);
-    g_loads[id] = L;
-  }
-  *load_out = make_handle(Kind::Load, id);
-  return SAGE_OK;
+  return load_finish(L, G, load_out, end_ev);
 }
 
 extern "C" {

@@ -58,10 +58,10 @@ print("RESULT " + json.dumps(out))
 """
 
 
-def run_child(issuer: str, tmp):
+def run_child(issuer: str, tmp, piece_mb: str = "0"):
     import numpy as np
-    env = dict(os.environ, SAGE_ISSUER=issuer)
-    npz = str(tmp / f"issuer{issuer}.npz")
+    env = dict(os.environ, SAGE_ISSUER=issuer, SAGE_ISSUE_PIECE_MB=piece_mb)
+    npz = str(tmp / f"issuer{issuer}_p{piece_mb}.npz")
     res = subprocess.run([sys.executable, "-c", CHILD, str(ROOT), npz], capture_output=True, text=True, env=env,
                          timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
@@ -83,6 +83,26 @@ def test_issuer_changes_order_not_results(built, tmp_path):
     assert len(off) == len(on) == 48
     assert off == on
     for meta, a, b in zip(off, r_off, r_on):
+        if meta[0] == "sgemm":
+            np.testing.assert_allclose(a.view(np.float32), b.view(np.float32), rtol=1e-5, atol=1e-4)
+        else:
+            assert np.array_equal(a, b), meta
+
+
+def test_piecewise_cold_loads_change_order_not_results(built, tmp_path):
+    """SAGE_ISSUE_PIECE_MB=1: every staged cold load is enqueued one ring
+    chunk at a time, alternating with the followers of landed segments; the
+    same metadata, checksums and results as enqueueing at admission, and
+    followers still compute after their leader's segment landed (checked in
+    the child)."""
+    import numpy as np
+    from conftest import gpu_available
+    if not gpu_available():
+        pytest.fail("gpu test run without a visible CUDA device")
+    off, r_off = run_child("0", tmp_path)
+    pc, r_pc = run_child("1", tmp_path, piece_mb="1")
+    assert off == pc
+    for meta, a, b in zip(off, r_off, r_pc):
         if meta[0] == "sgemm":
             np.testing.assert_allclose(a.view(np.float32), b.view(np.float32), rtol=1e-5, atol=1e-4)
         else:

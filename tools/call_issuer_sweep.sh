@@ -1,6 +1,10 @@
 #!/bin/bash
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
-for cfg in "SAGE_ISSUE_LOOKAHEAD_MB=32 SAGE_ISSUE_MAX_DEFER_US=3000" "SAGE_ISSUE_LOOKAHEAD_MB=16 SAGE_ISSUE_MAX_DEFER_US=3000" "SAGE_ISSUE_LOOKAHEAD_MB=64 SAGE_ISSUE_MAX_DEFER_US=3000" "SAGE_ISSUE_LOOKAHEAD_MB=32 SAGE_ISSUE_MAX_DEFER_US=1000" "SAGE_ISSUE_LOOKAHEAD_MB=32 SAGE_ISSUE_MAX_DEFER_US=10000" "SAGE_ISSUE_LOOKAHEAD_MB=32 SAGE_ISSUE_MAX_DEFER_US=3000"; do
-  env $cfg timeout 300 python bench.py --no-cfg1 --no-cpu-baseline --steps 10 > gpurun_out/sw.json 2>/dev/null
-  python -c "import json,sys; d=json.load(open('gpurun_out/sw.json')); e=d['e2e']; print(sys.argv[1], e['value'], e['ms_per_step'], e['setup_p50_ms'], e['roofline']['frac'])" "$cfg"
+# e2e burst length (tools/e2e_timeline.py, 6 bursts) across issuer knobs
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+mkdir -p gpurun_out/sweep
+for d in 3000 6000 20000; do
+  for la in 16 32 64; do
+    SAGE_ISSUE_MAX_DEFER_US=$d SAGE_ISSUE_LOOKAHEAD_MB=$la timeout 300 python tools/e2e_timeline.py > gpurun_out/sweep/d${d}_l${la}.jsonl 2>&1
+    echo "defer $d lookahead $la $(grep bursts_us gpurun_out/sweep/d${d}_l${la}.jsonl)"
+  done
 done

@@ -23,11 +23,19 @@ for n in names:
     pls.append(pb)
 sim.dataplane.pin_host_store()
 out = []
+spans = []                                     # (first H2D begin, last return end) per burst
+walls = []
+import time  # noqa: E402
 for rep in range(6):
     for r in list(sim.sharing.residents.values()):
         sim.sharing._evict(r)
+    t_sub = time.perf_counter()
     invs = sim.submit_many(names, payloads=pls)
+    t_done = time.perf_counter()
     sim.drain()
+    t_drained = time.perf_counter()
+    walls.append([round((t_done - t_sub) * 1e6), round((t_drained - t_sub) * 1e6)])
+    spans.append([min(i.stages[Stage.GPU_LOAD][0] for i in invs), max(i.stages[Stage.RETURN][1] for i in invs)])
     if rep == 5:
         t0 = min(i.arrival_us for i in invs)
         for i in invs:
@@ -37,6 +45,9 @@ for rep in range(6):
 for o in out:
     print(json.dumps(o))
 end = max(o["stages"]["return"][1] for o in out)
+print(json.dumps({"bursts_us": [round(b - a) for a, b in spans],
+                  "gaps_between_bursts_us": [round(spans[k + 1][0] - spans[k][1]) for k in range(len(spans) - 1)],
+                  "submit_and_drain_wall_us": walls}))
 print(json.dumps({"burst_us": end,
                   "last_gpu_load_end": max(o["stages"]["gpu_load"][1] for o in out),
                   "first_return_begin": min(o["stages"]["return"][0] for o in out),
