@@ -25,7 +25,8 @@
 // Per CTA: 1 producer warp (one elected lane issues the bulk copies of the
 // x chunk and the bucket's entries onto a full barrier) + W = 16 consumer
 // warps (wait full, gather from the staged x, add into the CTA's y partial
-// in shared memory, arrive on empty).  A warp's rows are its own and one
+// in shared memory; every consumer thread fences the async proxy and arrives
+// on empty -- racecheck-clean, profiles/r1_spmv_csb_sanitizer.txt).  A warp's rows are its own and one
 // row's entries inside a 32-entry window are merged in lane order, so every
 // sum has a fixed order (sm_100 has no native shared fp32 atomic add: it
 // would be a CAS loop); slices are summed in rank order.  Repeated launches
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kCsbThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < sh.NS; ++i) {
       mb_init(&full[i], 1);
-      mb_init(&empty[i], kCsbWarps);
+      mb_init(&empty[i], kCsbWarps * 32);   // every consumer thread releases its own reads
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -240,8 +241,10 @@ __global__ void __launch_bounds__(kCsbThreads, 1)
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mb_arrive(&empty[st]);
+      // the stage's next fill is an async-proxy (bulk copy) write: order this
+      // thread's generic-proxy reads of it before its release
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mb_arrive(&empty[st]);
       if (++st == sh.NS) {
         st = 0;
         ph ^= 1;
