@@ -494,6 +494,15 @@ def max_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
+def min_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=_reduce_device(dist))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t.item())
+
+
 def sum_over_ranks(dist, v: float) -> float:
     if dist is None:
         return v
@@ -612,6 +621,7 @@ def our_arm(args, rank, world, dist) -> dict:
     sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=1, function_data=data,
                      copy_results=False)
     box = None
+    fanout_note = None
     if world > 1 and args.fanout != "none":
         # PCIe once per box: each function's home rank loads its segment over
         # PCIe; the other ranks land it from the home's pages peer to peer
@@ -620,6 +630,13 @@ def our_arm(args, rank, world, dist) -> dict:
         if args.fanout == "p2p":
             job = f"{os.environ.get('MASTER_PORT', '0')}-{os.getppid()}"
             box = PeerFanout(rank, world, table, job=job, barrier=dist.barrier)
+            # check the exchange end to end on this box before relying on it;
+            # any rank failing -> every rank loads over its own PCIe instead
+            ok = box.selftest(0) and os.environ.get("SAGE_FANOUT_SELFTEST_FAIL", "-1") != str(rank)
+            if min_over_ranks(dist, 1.0 if ok else 0.0) < 1.0:
+                box.close()
+                box = None
+                fanout_note = "peer fan-out selftest failed on a rank: every rank loaded over its own PCIe"
         else:
             box = BoxFanout(rank, world, table)
         sim.dataplane.box = box
@@ -761,7 +778,7 @@ def our_arm(args, rank, world, dist) -> dict:
         "rooflines": rooflines,
         "kernels_e2e": stats_e2e,
         "gpu_launches": gpu_launches,
-        "fanout": None if box is None else {
+        "fanout": ({"fallback": fanout_note} if fanout_note else None) if box is None else {
             "how": ("home rank loads each RO segment over PCIe; the other ranks land it from the home's pages "
                     "peer to peer (one land + checksum, interprocess event)" if box.kind == "peer" else
                     "home rank loads each RO segment over PCIe; ncclBroadcast to the other ranks, then "

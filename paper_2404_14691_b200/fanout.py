@@ -159,6 +159,7 @@ class PeerFanout(BoxFanout):
         self._lsock.bind(path)
         self._lsock.listen(max(1, world))
         self._lsock.settimeout(timeout_s)
+        self._barrier = barrier
         if barrier:
             barrier()                                 # everyone listens
         self.to_home: dict[int, socket.socket] = {}
@@ -215,7 +216,10 @@ class PeerFanout(BoxFanout):
     def fetch(self, gpu: int, name: str, nbytes: int, scratch=None):
         """Receiver: map the home's segment and open its landed event.
         Returns ("peer", device address, event to wait on)."""
-        msg, fds = self._message_for(self.home(name), name)
+        return self._fetch_from(self.home(name), gpu, name, nbytes)
+
+    def _fetch_from(self, home: int, gpu: int, name: str, nbytes: int):
+        msg, fds = self._message_for(home, name)
         if msg["bytes"] != nbytes:
             raise RuntimeError(f"{name}: home sent {msg['bytes']} B, expected {nbytes} B")
         L = _lib.lib()
@@ -233,6 +237,57 @@ class PeerFanout(BoxFanout):
         self.received += 1
         self.bytes_in += nbytes
         return "peer", dptr.value, D.Event(ev.value)
+
+    def selftest(self, gpu: int, nbytes: int = 1 << 20) -> bool:
+        """Collective check of the whole exchange before any function uses
+        it: every rank lands a rank-specific byte pattern and publishes the
+        pages; every rank then lands each peer's pages peer to peer (export /
+        import / interprocess event / `land` reading the peer) and compares the
+        checksum with a local land of the same pattern.  Returns whether this
+        rank's checks passed; the caller agrees across ranks and falls back
+        when any failed.  `barrier` must be set (peers read this rank's pages
+        until every rank is done)."""
+        import numpy as np
+
+        def pattern(r: int) -> np.ndarray:
+            return np.random.Generator(np.random.PCG64(1000 + r)).integers(0, 256, nbytes, dtype=np.uint8)
+
+        mine = D.pool_alloc(gpu, nbytes, _lib.CLASS_READ_ONLY, unaccounted=True)
+        tmp = D.pool_alloc(gpu, nbytes, _lib.CLASS_WRITABLE, unaccounted=True)
+        sent, ok = None, True
+        stats = (self.sent, self.received, self.bytes_out, self.bytes_in)
+        try:
+            op = D.load(gpu, mine.dptr, pattern(self.rank))
+            op.wait()
+            sent = self.publish(gpu, mine.dptr, nbytes, op.end, seg_handle=mine.h, name=f"__selftest_{self.rank}")
+            op.release()
+            for h in range(self.world):
+                if h == self.rank:
+                    continue
+                _, src, ev = self._fetch_from(h, gpu, f"__selftest_{h}", nbytes)
+                got = D.load(gpu, tmp.dptr, None, None, device_src=src, device_src_bytes=nbytes, peer_gpu=gpu,
+                             wait=[ev])
+                want = D.load(gpu, tmp.dptr, pattern(h), wait=[got.end])
+                a, b = got.wait().checksum, want.wait().checksum
+                got.release()
+                want.release()
+                ok = ok and a == b and a != 0
+        except Exception as e:   # noqa: BLE001 -- any failure means "do not use this exchange"
+            print(f"sage fanout selftest (rank {self.rank}): {e}", flush=True)
+            ok = False
+        finally:
+            if self._barrier:
+                self._barrier()                  # peers are done reading `mine`
+            try:
+                self.reap()
+            except Exception:   # noqa: BLE001
+                ok = False
+            if sent is not None:
+                sent.release()
+            mine.free()
+            tmp.free()
+            self.sent, self.received, self.bytes_out, self.bytes_in = stats
+        return ok
 
     def reap(self) -> None:
         """Unmap every received segment; call when no device work reads them
