@@ -48,14 +48,20 @@ def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real", dtype: 
     """(FunctionSpec, FunctionData) for ResNet-50 inference on a batch of
     224x224 images; the DB record packs the state dict back to back.
     dtype "fp32": 102.4 MB of weights, fp32 input; "bf16": the weights and
-    the input in bfloat16 (51.2 MB, half the PCIe bytes), logits returned in
-    fp32 (BASELINE.json: BF16 outputs within rtol 1e-2)."""
+    the input in bfloat16 (51.2 MB, half the PCIe bytes), packed
+    channels-last (filters OHWI, input NHWC: meta["layout"] == "nhwc"),
+    logits returned in fp32 (BASELINE.json: BF16 outputs within rtol 1e-2)."""
     if dtype not in ("fp32", "bf16"):
         raise ValueError(f"resnet50: dtype must be fp32 or bf16, not {dtype!r}")
     names, arrays = _state(seed)
+    shapes = [a.shape for a in arrays]            # logical (NCHW / OIHW) shapes
     dtypes = [a.dtype.str for a in arrays]
     if dtype == "bf16":
-        arrays = [_bf16_bits(a) if a.dtype == np.float32 else a for a in arrays]
+        # channels-last record: conv filters stored OHWI, the input NHWC, so
+        # the zero-copy views feed cuDNN's NHWC tensor-core kernels (a batch-8
+        # graph replay: 1.12 ms vs 1.38 ms NCHW, profiles/r1_resnet50_body_formats.jsonl)
+        arrays = [_bf16_bits(a.transpose(0, 2, 3, 1) if a.ndim == 4 else a) if a.dtype == np.float32 else a
+                  for a in arrays]
         dtypes = ["bf16" if d.endswith("f4") else d for d in dtypes]
     sizes = [a.nbytes for a in arrays]
     layout = SegmentLayout.packed(sizes, align=256, names=tuple(names))
@@ -63,15 +69,31 @@ def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real", dtype: 
     rng = np.random.Generator(np.random.PCG64(seed + 1))
     x = rng.standard_normal((batch, 3, 224, 224), dtype=np.float32)
     if dtype == "bf16":
-        x = _bf16_bits(x)
+        x = _bf16_bits(x.transpose(0, 2, 3, 1))
     out_bytes = batch * 1000 * 4
     data = FunctionData(layout, db, body="resnet50", args=(batch,), input=x.reshape(-1).view(np.uint8),
                         out_bytes=out_bytes)
-    data.meta = {"shapes": [a.shape for a in arrays], "dtypes": dtypes, "names": names, "compute": dtype}
+    data.meta = {"shapes": shapes, "dtypes": dtypes, "names": names, "compute": dtype,
+                 "layout": "nhwc" if dtype == "bf16" else "nchw"}
     spec = FunctionSpec(name=name, ro_mem_mb=_mb(layout.seg_bytes),
                         writable_mem_mb=_mb(x.nbytes + out_bytes + 4096), compute_ms=24.3,
                         input_bytes_host_mb=_mb(x.nbytes), input_bytes_pcie_mb=_mb(x.nbytes), body="resnet50")
     return spec, data
+
+
+def _as_logical(t, shp, fd: FunctionData):
+    """A flat parameter view shaped to its logical (PyTorch) shape; 4-D
+    filters of a channels-last record become OIHW views with NHWC strides."""
+    if len(shp) == 4 and fd.meta.get("layout") == "nhwc":
+        o, i, h, w = shp
+        return t.view(o, h, w, i).permute(0, 3, 1, 2)
+    return t.view(shp) if len(shp) else t.view(())
+
+
+def _input_view(t, batch: int, fd: FunctionData):
+    if fd.meta.get("layout") == "nhwc":
+        return t.view(batch, 224, 224, 3).permute(0, 3, 1, 2)
+    return t.view(batch, 3, 224, 224)
 
 
 def _torch_dtype(tag: str):
@@ -122,8 +144,7 @@ def _params(fd: FunctionData, ro_ptr: int, dev, plane: int):
         seg = view(ro_ptr, lay.seg_bytes, dev)
         params = {}
         for n, off, ln, shp, dt in zip(meta["names"], lay.dst_off, lay.length, meta["shapes"], meta["dtypes"]):
-            t = seg[off:off + ln].view(_torch_dtype(dt))
-            params[n] = t.view(shp) if len(shp) else t.view(())
+            params[n] = _as_logical(seg[off:off + ln].view(_torch_dtype(dt)), shp, fd)
         for k in [k for k in _PARAMS if k[0] == key[0] and k[2] == key[2]]:
             del _PARAMS[k]         # the function's segment moved on this GPU
         _PARAMS[key] = params
@@ -174,10 +195,10 @@ def prewarm(fd: FunctionData, device_index: int) -> None:
     params = {}
     for n, off, ln, shp, dt in zip(meta["names"], lay.src_off, lay.length, meta["shapes"], meta["dtypes"]):
         raw = torch.from_numpy(fd.db[off:off + ln].copy()).view(_torch_dtype(dt))
-        params[n] = raw.view(shp).to(dev) if len(shp) else raw.view(()).to(dev)
+        params[n] = _as_logical(raw, shp, fd).to(dev)
     model = _skeleton()
     side = torch.cuda.Stream(device=dev)
-    x = torch.zeros((fd.args[0], 3, 224, 224), device=dev, dtype=_compute_dtype(fd))
+    x = _static_input(fd.args[0], dev, fd)
     with torch.cuda.stream(side), torch.inference_mode():
         for _ in range(2):
             torch.func.functional_call(model, params, (x,))
@@ -195,7 +216,13 @@ def _graphs_enabled() -> bool:
     return os.environ.get("SAGE_DNN_GRAPHS", "1") != "0"
 
 
-def _capture(model, params, batch: int, dev, ext, dtype=None) -> _GraphEntry:
+def _static_input(batch: int, dev, fd: FunctionData):
+    import torch
+    x = torch.zeros((batch, 3, 224, 224), device=dev, dtype=_compute_dtype(fd))
+    return x.contiguous(memory_format=torch.channels_last) if fd.meta.get("layout") == "nhwc" else x
+
+
+def _capture(model, params, batch: int, dev, ext, fd: FunctionData) -> _GraphEntry:
     """Warm up (cuDNN algorithm choice, allocations) and capture one forward
     on a side stream ordered after the invocation's stream (the segment has
     landed there).  Capture is thread-local: the library's issuer and
@@ -203,7 +230,7 @@ def _capture(model, params, batch: int, dev, ext, dtype=None) -> _GraphEntry:
     import torch
     side = torch.cuda.Stream(device=dev)
     side.wait_stream(ext)
-    x = torch.zeros((batch, 3, 224, 224), device=dev, dtype=dtype or torch.float32)
+    x = _static_input(batch, dev, fd)
     with torch.cuda.stream(side), torch.inference_mode():
         for _ in range(2):
             torch.func.functional_call(model, params, (x,))
@@ -227,7 +254,7 @@ def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, strea
     dev = torch.device("cuda", device_index)
     params = _params(fd, ro_ptr, dev, plane)
     batch = fd.args[0]
-    x = view(in_ptr, fd.input_bytes, dev).view(_compute_dtype(fd)).view(batch, 3, 224, 224)
+    x = _input_view(view(in_ptr, fd.input_bytes, dev).view(_compute_dtype(fd)), batch, fd)
     out = view(out_ptr, fd.out_bytes, dev).view(torch.float32).view(batch, 1000)
     model = _skeleton()
     ext = torch.cuda.ExternalStream(stream_ptr, device=dev)
@@ -244,7 +271,7 @@ def run_resnet50(fd: FunctionData, ro_ptr: int, in_ptr: int, out_ptr: int, strea
     if len(pool.entries) < GRAPHS_PER_SEGMENT:
         import time
         t0 = time.perf_counter()
-        pool.entries.append(_capture(model, params, batch, dev, ext, _compute_dtype(fd)))
+        pool.entries.append(_capture(model, params, batch, dev, ext, fd))
         CAPTURES["count"] += 1
         CAPTURES["seconds"] += time.perf_counter() - t0
     entry = pool.entries[pool.next % len(pool.entries)]

@@ -87,7 +87,9 @@ def test_resnet50_bf16_function_within_rtol(built):
         assert [i.warmth.label() for i in invs] == ["Cold"] + ["Stage1Hot"] * 4
         torch.manual_seed(0)
         ref = torchvision.models.resnet50(weights=None).eval().cuda()
-        x = torch.from_numpy(data.input.copy()).view(torch.bfloat16).float().view(8, 3, 224, 224).cuda()
+        assert data.meta["layout"] == "nhwc"                   # the record is packed channels-last
+        x = torch.from_numpy(data.input.copy()).view(torch.bfloat16).float().view(8, 224, 224, 3)
+        x = x.permute(0, 3, 1, 2).contiguous().cuda()
         with torch.inference_mode():
             want = ref(x).float().cpu().numpy()
         for inv in invs:
