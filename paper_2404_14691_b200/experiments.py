@@ -197,9 +197,9 @@ def cfg5(ns=(1, 2, 4, 8, 16, 32, 64, 128, 256, 512), reps: int = 3, gpus_list=(1
 
 def _workload(kind: str):
     """(spec table, function data) of a named workload."""
-    if kind == "cfg3":
+    if kind in ("cfg3", "cfg3_bf16"):
         from .dnn import resnet50
-        spec, data = resnet50()
+        spec, data = resnet50(dtype="bf16" if kind == "cfg3_bf16" else "fp32")
         return {spec.name: spec}, {spec.name: data}
     from .parboil import cfg2_functions
     return cfg2_functions()
@@ -277,7 +277,8 @@ def main(argv=None):
     ap.add_argument("--out", default=None)
     ap.add_argument("--rate", type=float, default=None, help="cfg3: Poisson rate (/s)")
     ap.add_argument("--gpus", default=None, help="cfg3: comma-separated logical GPU counts")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"], help="peak / trace: function set")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg3_bf16"],
+                    help="peak / trace: function set")
     ap.add_argument("--trace", default=None, help="trace: flat trace CSV (timestamp_ms,function)")
     ap.add_argument("--time-scale", type=float, default=1.0)
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"], help="cfg3: ResNet-50 weights / input")
