@@ -171,7 +171,8 @@ class _GraphPool:
         self.next = 0
 
 
-GRAPHS_PER_SEGMENT = 4
+import os as _os
+GRAPHS_PER_SEGMENT = int(_os.environ.get("SAGE_DNN_GRAPHS_PER_SEGMENT", "4"))
 _GRAPHS: dict = {}
 CAPTURES = {"count": 0, "seconds": 0.0}   # graph captures so far (reported by experiments.cfg3)
 
