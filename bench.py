@@ -642,7 +642,9 @@ def our_arm(args, rank, world, dist) -> dict:
         sim.dataplane.box = box
     L = _lib.lib()
     try:
-        _lib.check(L.sage_stats_enable(1), "stats_enable")
+        # the e2e legs are timed without per-kernel events (they cost ~3% of a
+        # PCIe-bound burst: tools/e2e_timeline.py, SAGE_TIMELINE_STATS)
+        _lib.check(L.sage_stats_enable(0), "stats_enable")
         # ---- e2e: host buffers through the public API -------------------------
         # request payloads arrive in pinned host buffers (as from a NIC); the
         # functions' DB records stay pageable: cold loads pay CPU_LOAD
@@ -662,10 +664,16 @@ def our_arm(args, rank, world, dist) -> dict:
         e2e_steps = timed.step_ms
         e2e_box_bytes = timed.box_bytes
         clocks_e2e = clocks.stop()
+        # per-kernel breakdown of the e2e path: one more (untimed) step with
+        # CUDA events around every launch; the value leg keeps them on (its
+        # dominant kernel is the contract roofline)
+        _lib.check(L.sage_stats_enable(1), "stats_enable")
+        _lib.check(L.sage_stats_reset(), "stats_reset")
+        run_steps(sim, names, 1, payloads)
+        stats_e2e = kernel_stats()
         sim.dataplane.unpin_host_store()
         for pb in payloads:
             pb.free()
-        stats_e2e = kernel_stats()
         per_step = len(names)
         pcie = pcie_probe(0)
         h2d = sum(i.measured.get("pcie_bytes", 0) for i in invs_e2e) / args.steps
@@ -777,6 +785,8 @@ def our_arm(args, rank, world, dist) -> dict:
                                  f"events on the land stream (in-burst launches: rooflines.land)"},
         "rooflines": rooflines,
         "kernels_e2e": stats_e2e,
+        "kernels_e2e_how": "one untimed e2e step with CUDA events around every launch (the timed e2e legs run "
+                           "without them)",
         "gpu_launches": gpu_launches,
         "fanout": ({"fallback": fanout_note} if fanout_note else None) if box is None else {
             "how": ("home rank loads each RO segment over PCIe; the other ranks land it from the home's pages "

@@ -22,6 +22,9 @@ for n in names:
     pb.view()[:] = data[n].input
     pls.append(pb)
 sim.dataplane.pin_host_store()
+import os  # noqa: E402
+from paper_2404_14691_b200 import _lib  # noqa: E402
+_lib.check(_lib.lib().sage_stats_enable(int(os.environ.get("SAGE_TIMELINE_STATS", "0"))), "stats_enable")
 out = []
 spans = []                                     # (first H2D begin, last return end) per burst
 walls = []
