@@ -745,10 +745,7 @@ def our_arm(args, rank, world, dist) -> dict:
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(val_us / 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (bodies) / u8 (land)", "data": "synthetic",
-        "config": {"workload": f"cfg2: burst of {per_step} concurrent invocations (sgemm/stencil/spmv uniform "
-                               f"mix, shared RO segments, cold start per burst) per GPU",
-                   "policy": "SAGE", "burst": per_step, "gpus": world,
-                   "l2": "inputs larger than L2 (212 MiB RO + 504 MiB inputs per step)"},
+        "config": workload_config(per_step, world),
         "setup_p50_ms": round(percentile(setups_val, 50) / 1e3, 3),
         "setup_p99_ms": round(percentile(setups_val, 99) / 1e3, 3),
         "step_ms": val_steps,
@@ -805,6 +802,15 @@ def our_arm(args, rank, world, dist) -> dict:
     return line
 
 
+def workload_config(burst: int, world: int) -> dict:
+    """The `config` both arms report (the reference arm times a bounded
+    sample of the same workload, described in its cpu_baseline.sample)."""
+    return {"workload": f"cfg2: burst of {burst} concurrent invocations (sgemm/stencil/spmv uniform "
+                        f"mix, shared RO segments, cold start per burst) per GPU",
+            "policy": "SAGE", "burst": burst, "gpus": world,
+            "l2": "inputs larger than L2 (212 MiB RO + 504 MiB inputs per step)"}
+
+
 def reference_arm(args, rank, world) -> dict:
     """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
     steps, warmup = args.steps, args.warmup
@@ -823,10 +829,11 @@ def reference_arm(args, rank, world) -> dict:
     return {"metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
             "ms_per_step": round(dt * 1e3 / steps, 1), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32 (bodies) / u8 (load)", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "cfg2 mix, host-only loading path + numpy bodies (bounded sample: 3 "
-                                   "invocations per step, one per function)"},
+            "config": workload_config(args.burst, world),
             "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{done} invocations over {steps} steps"},
+                             "sample": f"{done} invocations over {steps} steps: each step 3 invocations (one per "
+                                       f"function) of the cfg-2 burst through the reference's host-only path "
+                                       f"(oracle port: load + unpack + checksum on all host threads, numpy bodies)"},
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
