@@ -44,14 +44,20 @@ UNIT = "invocations/s"
 
 
 def _rank_env():
+    """One process per GPU: every device stays visible (peers' exported pages
+    then map over NVLink like NCCL's own), this rank's library planes start
+    at device LOCAL_RANK (SAGE_DEVICE_OFFSET)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not _shared_gpu():
-        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-        ids = vis.split(",") if vis else [str(i) for i in range(64)]
-        os.environ["CUDA_VISIBLE_DEVICES"] = ids[local]
+        os.environ["SAGE_DEVICE_OFFSET"] = str(local)
     return rank, world, local
+
+
+def _my_device() -> int:
+    """Physical device index of this rank (torch / NVML numbering)."""
+    return int(os.environ.get("SAGE_DEVICE_OFFSET", "0"))
 
 
 def _shared_gpu() -> bool:
@@ -659,7 +665,7 @@ def our_arm(args, rank, world, dist) -> dict:
         # (b) the daemon's host store pinned at registration (outside the timed
         #     region): cold loads DMA straight from it -- the headline e2e
         sim.dataplane.pin_host_store()
-        clocks = ClockSampler(0).start()
+        clocks = ClockSampler(_my_device()).start()
         e2e_us, invs_e2e = timed(sim, names, args.steps, args.warmup, dist, payloads)
         e2e_steps = timed.step_ms
         e2e_box_bytes = timed.box_bytes
@@ -675,14 +681,14 @@ def our_arm(args, rank, world, dist) -> dict:
         for pb in payloads:
             pb.free()
         per_step = len(names)
-        pcie = pcie_probe(0)
+        pcie = pcie_probe(_my_device())
         h2d = sum(i.measured.get("pcie_bytes", 0) for i in invs_e2e) / args.steps
         d2h = sum(data[n].out_bytes for n in names)
         setups_e2e = [i.setup_us for i in invs_e2e]
         # ---- value: HBM-resident sources ----------------------------------------
         sim.dataplane.stage_sources_in_hbm(0)
         sim.dataplane.results_in_hbm = True
-        clocks = ClockSampler(0).start()
+        clocks = ClockSampler(_my_device()).start()
         val_us, invs_val = timed(sim, names, args.steps, args.warmup, dist)
         val_steps = timed.step_ms
         clocks_val = clocks.stop()
@@ -861,7 +867,7 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(_my_device())
         tdist.init_process_group("gloo" if _shared_gpu() else "nccl")
         dist = tdist
     from paper_2404_14691_b200 import _lib

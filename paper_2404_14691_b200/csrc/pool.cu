@@ -181,7 +181,11 @@ static void unmap_segment(Pool *P, Alloc *A) {
 int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chunk) {
   Gpu *G = st.gpus[id].get();
   G->id = id;
-  G->dev = id % std::max(1, st.n_devices);
+  // SAGE_DEVICE_OFFSET: logical GPU 0 is physical device `offset` (one
+  // process per GPU with every device visible -- bench.py under torchrun --
+  // so peers' exported pages map over NVLink)
+  static const int offset = [] { const char *e = getenv("SAGE_DEVICE_OFFSET"); return e ? atoi(e) : 0; }();
+  G->dev = (id + std::max(0, offset)) % std::max(1, st.n_devices);
   SAGE_CUDA(cudaSetDevice(G->dev));
   SAGE_CUDA(cudaFree(0));  // create/retain the primary context up front (the pre-created ctx)
   SAGE_CUDA(cudaDeviceGetAttribute(&G->sm_count, cudaDevAttrMultiProcessorCount, G->dev));

@@ -40,7 +40,7 @@ def _worker(rank, world, port, q):
         homes = BoxFanout(rank, world, ["spmv", "sgemm", "stencil"]).homes
         same = bench.ro_checksums_agree(dist, {"a": _FD(0xFEDCBA9876543210), "b": _FD(7)})
         differ = bench.ro_checksums_agree(dist, {"a": _FD(0xFEDCBA9876543210 + rank), "b": _FD(7)})
-        q.put((r, w, local, os.environ.get("CUDA_VISIBLE_DEVICES"), mx, sm, sorted(homes.items()), same, differ))
+        q.put((r, w, local, os.environ.get("SAGE_DEVICE_OFFSET"), mx, sm, sorted(homes.items()), same, differ))
     finally:
         dist.destroy_process_group()
 
@@ -58,7 +58,7 @@ def test_two_rank_max_and_sum_over_gloo():
         assert p.exitcode == 0
     assert [o[0] for o in out] == [0, 1]
     assert all(o[1] == 2 for o in out)
-    assert [o[3] for o in out] == ["0", "1"]                  # one GPU per rank
+    assert [o[3] for o in out] == ["0", "1"]                  # one GPU per rank (library planes start there)
     assert all(o[4] == 11.0 for o in out)                      # max over ranks
     assert all(o[5] == 128.0 for o in out)                     # whole-job invocations
     assert out[0][6] == out[1][6] == [("sgemm", 0), ("spmv", 1), ("stencil", 0)]   # same homes on every rank
