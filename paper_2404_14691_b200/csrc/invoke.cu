@@ -556,16 +556,20 @@ static void issuer_main() {
       const int ng = (int)pending.size();
       for (int k = 0; k < ng && !pick; ++k) {
         const int g = (rr + k) % ng;
-        if (!room(g)) continue;
+        // a full PCIe queue holds back everything that adds H2D bytes;
+        // invocations without H2D (HBM-resident sources) still go
+        const bool has_room = room(g);
         auto open = iss_open.end();
-        for (auto it = iss_open.begin(); it != iss_open.end(); ++it)
-          if ((*it)->gpu == g) { open = it; break; }
+        if (has_room)
+          for (auto it = iss_open.begin(); it != iss_open.end(); ++it)
+            if ((*it)->gpu == g) { open = it; break; }
         auto fol = iss_q.end(), cold = iss_q.end();
         int64_t fol_key = INT64_MAX, cold_key = INT64_MAX;
         bool fol_overdue = false;
         for (auto it = iss_q.begin(); it != iss_q.end(); ++it) {
           Inv *I = *it;
           if (I->gpu != g || !inv_ready(I)) continue;
+          if (I->h2d > 0 && !has_room) continue;
           const int64_t key = I->h2d - I->d2h;
           if (piece > 0 && key > piece) {
             if (key < cold_key) { cold_key = key; cold = it; }
