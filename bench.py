@@ -184,7 +184,7 @@ def run_steps(sim, names, steps: int, payloads=None, marks=None):
     for _ in range(steps):
         if sim.sharing is not None:   # start every burst cold (no resident segment)
             for r in list(sim.sharing.residents.values()):
-                sim.sharing._evict(r)
+                sim.sharing.evict(r)
         invs = sim.submit_many(names, payloads=payloads)
         sim.drain()
         box = getattr(sim.dataplane, "box", None)
@@ -560,7 +560,7 @@ def cfg1_compare(n: int = 16) -> dict:
             for rep in range(reps):
                 if sim.sharing is not None:
                     for r in list(sim.sharing.residents.values()):
-                        sim.sharing._evict(r)
+                        sim.sharing.evict(r)
                 invs = sim.submit_many([spec.name] * n)
                 sim.drain()
                 if rep >= (1 if reps > 1 else 0):   # first SAGE burst is warm-up

@@ -85,6 +85,9 @@ int sage_pool_free(sage_handle h);
 /* ledger release now (the reference frees at once, sharing.py:217-229), the
  * physical pages once `ev` completes (a D2H / kernel may still read them)   */
 int sage_pool_free_after(sage_handle h, sage_handle ev);
+/* ... after every event in evs (e.g. the cache D2H and peer lands reading the
+ * segment over NVLink from other GPUs)                                       */
+int sage_pool_free_after_n(sage_handle h, const sage_handle *evs, int n);
 int sage_pool_effective(int gpu, uint64_t bytes, uint64_t *effective);
 int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total,
                     uint64_t *physical_total, uint64_t *capacity);
@@ -135,6 +138,9 @@ int sage_event_query(sage_handle ev);                  /* SAGE_OK or SAGE_ENOTRE
 int sage_event_sync(sage_handle ev);
 int sage_event_time(sage_handle ev, int64_t *t_us);    /* completion time, library clock */
 int sage_event_release(sage_handle ev);
+/* a second, independently released handle on the same event (keep a stage
+ * END alive past the invocation that owns it: peer readers of a segment)   */
+int sage_event_alias(sage_handle ev, sage_handle *out);
 /* poll n events; done[i] = 1 when complete.  Blocks up to timeout_us until at
  * least one is complete.  Returns the number complete (>= 0) or an error.    */
 int sage_event_poll(const sage_handle *evs, int n, uint8_t *done, int64_t timeout_us);
@@ -350,6 +356,100 @@ int sage_device_sync(int gpu);
 int sage_mark(int gpu, sage_handle *ev);
 /* elapsed µs between two completed events of the same GPU (device clock) */
 int sage_event_elapsed(sage_handle a, sage_handle b, double *us);
+
+/* ---- sharing manager: the native resident table ----------------------------
+ * Replaces SharingManager's resident dict and its state machine
+ * (sharing.py:103-335): warmth classification (:115-125), delta sizes
+ * (:126-134), leader election by allocation (:136-177), the refcounted
+ * release (:181-196), the four-stage timed decay (:217-246), eviction
+ * (:248-263), victim choice under pressure (:271-298) and the invariant sweep
+ * (:305-335); plus a content index for deduplicating identical RO records.
+ * Host code: usable without a GPU.  The caller owns the ledger allocations and
+ * the engine timers and executes each returned step (sharing.py).           */
+#define SAGE_SHARE_RO           0x1u   /* ro_sharing (policies.py:29)                  */
+#define SAGE_SHARE_CTX          0x2u   /* ctx_sharing                                   */
+#define SAGE_SHARE_MULTI_STAGE  0x4u   /* multi_stage_exit                              */
+#define SAGE_FN_HAS_RO          0x1u   /* fn_flags: ro_mem_mb > 0                        */
+#define SAGE_WARMTH_COLD        0      /* WarmthClass order (functions.py:23-41)        */
+#define SAGE_WARMTH_STAGE4      1
+#define SAGE_WARMTH_STAGE3      2
+#define SAGE_WARMTH_STAGE2      3
+#define SAGE_WARMTH_STAGE1_HOT  4
+#define SAGE_RES_ACTIVE         0      /* ResidentState (sharing.py:30-36)              */
+#define SAGE_RES_STAGE1         1
+#define SAGE_RES_STAGE2         2
+#define SAGE_RES_STAGE3         3
+#define SAGE_RES_STAGE4         4
+#define SAGE_TOKEN_RO           0
+#define SAGE_TOKEN_CTX          1
+typedef struct {
+  int32_t warmth;
+  uint8_t shared_ro, shared_ctx, wait_ro, wait_ctx;
+  uint8_t leader_ro, leader_ctx;     /* this admission allocates the shared segment   */
+  uint8_t timer_cancelled;           /* a decay timer was pending: cancel the engine's */
+  uint8_t new_resident;
+  uint64_t alloc_ro, alloc_ctx;      /* bytes of new shared segments to allocate      */
+  uint64_t resident;                 /* resident id (0 in a preview of none)          */
+} sage_share_grant;
+/* step actions, executed by the caller in this order */
+#define SAGE_STEP_CACHE_RO     0x01u  /* allocate the host RO cache (+ D2H of the held segment) */
+#define SAGE_STEP_FREE_RO      0x02u  /* free the GPU RO segment (after the cache D2H / readers) */
+#define SAGE_STEP_FREE_CTX     0x04u
+#define SAGE_STEP_DROP_CACHE   0x08u
+#define SAGE_STEP_EVICT        0x10u  /* the resident is gone                          */
+#define SAGE_STEP_GPU_FREED    0x20u  /* wake the GPU's queue (policies.on_memory_freed) */
+#define SAGE_STEP_ARM          0x40u  /* schedule the decay timer (deadline_us, timer_gen) */
+typedef struct {
+  uint32_t actions;
+  int32_t state_before, state_after;
+  uint32_t timer_gen;
+  uint8_t timer_cancelled, _pad[7];
+  int64_t deadline_us;
+  uint64_t resident;
+} sage_share_step;
+#define SAGE_HOLD_RO         0x1u
+#define SAGE_HOLD_CTX        0x2u
+#define SAGE_HOLD_CACHE      0x4u
+#define SAGE_HOLD_CPU_CTX    0x8u
+#define SAGE_HOLD_CONTAINER  0x10u
+typedef struct {
+  uint64_t resident;
+  int32_t fn, gpu, state;
+  uint32_t active, holds, timer_gen;
+  uint64_t ro_bytes, ctx_bytes;
+  int64_t last_activity_us, deadline_us;
+  uint32_t has_checksum, _pad;
+  uint64_t checksum;
+} sage_resident_info;
+int sage_share_create(int n_gpus, uint32_t flags, int64_t keep_alive_us, const int64_t intervals_us[4],
+                      sage_handle *tab);
+int sage_share_destroy(sage_handle tab);
+int sage_share_preview(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
+                       uint32_t fn_flags, sage_share_grant *g);                /* sharing.py:108-134 */
+int sage_share_admit(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
+                     uint32_t fn_flags, int64_t now_us, sage_share_grant *g);  /* sharing.py:136-177 */
+/* attach the leader's stage END event to a token (ev != 0) or mark it ready  */
+int sage_share_token(sage_handle tab, uint64_t resident, int kind, sage_handle ev);
+int sage_share_token_ready(sage_handle tab, uint64_t resident, int kind, int *ready);
+int sage_share_release(sage_handle tab, int32_t fn, int gpu, int64_t now_us,
+                       sage_share_step *out);                                  /* sharing.py:181-196 */
+/* the decay timer (resident, timer_gen) fired                                */
+int sage_share_expire(sage_handle tab, uint64_t resident, uint32_t timer_gen, int64_t now_us,
+                      sage_share_step *out);                                   /* sharing.py:203-246 */
+int sage_share_victim(sage_handle tab, int gpu, int32_t exclude_fn, uint64_t *resident); /* :288-298 */
+int sage_share_demote(sage_handle tab, uint64_t resident, int64_t now_us,
+                      sage_share_step *out);                                   /* sharing.py:271-286 */
+int sage_share_evict(sage_handle tab, uint64_t resident, sage_share_step *out); /* sharing.py:248-263 */
+int sage_share_info(sage_handle tab, uint64_t resident, sage_resident_info *out);
+int sage_share_lookup(sage_handle tab, int32_t fn, int gpu, uint64_t *resident);
+int sage_share_list(sage_handle tab, uint64_t *ids, int cap, int *n);
+int sage_share_ro_loads(sage_handle tab, int32_t fn, int gpu, uint32_t *n);  /* sharing.py:174-175 */
+/* content index: a landed RO segment's checksum; lookup of another function's
+ * resident segment with the same content on a GPU (token ready)             */
+int sage_share_set_checksum(sage_handle tab, uint64_t resident, uint64_t checksum);
+int sage_share_find_content(sage_handle tab, int gpu, uint64_t checksum, int32_t exclude_fn,
+                            uint64_t *resident);
+int sage_share_check(sage_handle tab);                                         /* sharing.py:305-335 */
 
 /* ---- test support (never on the product path) ------------------------------
  * Runs the chunk planner and the land byte semantics on the host so the

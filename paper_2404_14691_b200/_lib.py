@@ -87,6 +87,34 @@ class FixedGSLInfo(C.Structure):
                 ("pad_", C.c_int32)]
 
 
+SHARE_RO, SHARE_CTX, SHARE_MULTI_STAGE = 0x1, 0x2, 0x4
+FN_HAS_RO = 0x1
+TOKEN_RO, TOKEN_CTX = 0, 1
+STEP_CACHE_RO, STEP_FREE_RO, STEP_FREE_CTX, STEP_DROP_CACHE = 0x01, 0x02, 0x04, 0x08
+STEP_EVICT, STEP_GPU_FREED, STEP_ARM = 0x10, 0x20, 0x40
+HOLD_RO, HOLD_CTX, HOLD_CACHE, HOLD_CPU_CTX, HOLD_CONTAINER = 0x1, 0x2, 0x4, 0x8, 0x10
+
+
+class ShareGrant(C.Structure):
+    _fields_ = [("warmth", C.c_int32), ("shared_ro", C.c_uint8), ("shared_ctx", C.c_uint8),
+                ("wait_ro", C.c_uint8), ("wait_ctx", C.c_uint8), ("leader_ro", C.c_uint8),
+                ("leader_ctx", C.c_uint8), ("timer_cancelled", C.c_uint8), ("new_resident", C.c_uint8),
+                ("alloc_ro", u64), ("alloc_ctx", u64), ("resident", u64)]
+
+
+class ShareStep(C.Structure):
+    _fields_ = [("actions", C.c_uint32), ("state_before", C.c_int32), ("state_after", C.c_int32),
+                ("timer_gen", C.c_uint32), ("timer_cancelled", C.c_uint8), ("pad_", C.c_uint8 * 7),
+                ("deadline_us", i64), ("resident", u64)]
+
+
+class ResidentInfo(C.Structure):
+    _fields_ = [("resident", u64), ("fn", C.c_int32), ("gpu", C.c_int32), ("state", C.c_int32),
+                ("active", C.c_uint32), ("holds", C.c_uint32), ("timer_gen", C.c_uint32),
+                ("ro_bytes", u64), ("ctx_bytes", u64), ("last_activity_us", i64), ("deadline_us", i64),
+                ("has_checksum", C.c_uint32), ("pad_", C.c_uint32), ("checksum", u64)]
+
+
 _SIGS = {
     "sage_init": (C.c_int, [C.c_int, u64, u64, u64, C.c_uint32]),
     "sage_shutdown": (C.c_int, []),
@@ -99,6 +127,7 @@ _SIGS = {
     "sage_pool_alloc": (C.c_int, [C.c_int, u64, C.c_int, C.POINTER(H), C.POINTER(u64), C.POINTER(u64)]),
     "sage_pool_free": (C.c_int, [H]),
     "sage_pool_free_after": (C.c_int, [H, H]),
+    "sage_pool_free_after_n": (C.c_int, [H, C.POINTER(H), C.c_int]),
     "sage_pool_effective": (C.c_int, [C.c_int, u64, C.POINTER(u64)]),
     "sage_pool_usage": (C.c_int, [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "sage_pool_dptr": (C.c_int, [H, C.POINTER(u64), C.POINTER(u64)]),
@@ -114,6 +143,7 @@ _SIGS = {
     "sage_event_sync": (C.c_int, [H]),
     "sage_event_time": (C.c_int, [H, C.POINTER(i64)]),
     "sage_event_release": (C.c_int, [H]),
+    "sage_event_alias": (C.c_int, [H, C.POINTER(H)]),
     "sage_event_poll": (C.c_int, [C.POINTER(H), C.c_int, C.POINTER(C.c_uint8), i64]),
     "sage_ctx_acquire": (C.c_int, [C.c_int, C.POINTER(H)]),
     "sage_ctx_release": (C.c_int, [H]),
@@ -152,6 +182,24 @@ _SIGS = {
     "sage_device_sync": (C.c_int, [C.c_int]),
     "sage_mark": (C.c_int, [C.c_int, C.POINTER(H)]),
     "sage_event_elapsed": (C.c_int, [H, H, C.POINTER(C.c_double)]),
+    "sage_share_create": (C.c_int, [C.c_int, C.c_uint32, i64, C.POINTER(i64), C.POINTER(H)]),
+    "sage_share_destroy": (C.c_int, [H]),
+    "sage_share_preview": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, C.POINTER(ShareGrant)]),
+    "sage_share_admit": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, i64, C.POINTER(ShareGrant)]),
+    "sage_share_token": (C.c_int, [H, u64, C.c_int, H]),
+    "sage_share_token_ready": (C.c_int, [H, u64, C.c_int, C.POINTER(C.c_int)]),
+    "sage_share_release": (C.c_int, [H, C.c_int32, C.c_int, i64, C.POINTER(ShareStep)]),
+    "sage_share_expire": (C.c_int, [H, u64, C.c_uint32, i64, C.POINTER(ShareStep)]),
+    "sage_share_victim": (C.c_int, [H, C.c_int, C.c_int32, C.POINTER(u64)]),
+    "sage_share_demote": (C.c_int, [H, u64, i64, C.POINTER(ShareStep)]),
+    "sage_share_evict": (C.c_int, [H, u64, C.POINTER(ShareStep)]),
+    "sage_share_info": (C.c_int, [H, u64, C.POINTER(ResidentInfo)]),
+    "sage_share_lookup": (C.c_int, [H, C.c_int32, C.c_int, C.POINTER(u64)]),
+    "sage_share_list": (C.c_int, [H, C.POINTER(u64), C.c_int, C.POINTER(C.c_int)]),
+    "sage_share_ro_loads": (C.c_int, [H, C.c_int32, C.c_int, C.POINTER(C.c_uint32)]),
+    "sage_share_set_checksum": (C.c_int, [H, u64, u64]),
+    "sage_share_find_content": (C.c_int, [H, C.c_int, u64, C.c_int32, C.POINTER(u64)]),
+    "sage_share_check": (C.c_int, [H]),
     "sage_debug_emulate_land": (C.c_int, [H, C.c_void_p, u64, C.c_void_p, u64, C.POINTER(u64)]),
 }
 

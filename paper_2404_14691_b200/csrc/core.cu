@@ -541,6 +541,10 @@ int sage_shutdown(void) {
 }
 
 // ------------------------------------------------------------- events -------
+int sage_event_alias(sage_handle h, sage_handle *out) {
+  if (!out) return fail(SAGE_EINVAL, "event_alias: null out");
+  return event_alias(h, out);
+}
 int sage_event_query(sage_handle h) {
   Event *e = event_get(h);
   if (!e) return fail(SAGE_ESTATE, "unknown event handle");

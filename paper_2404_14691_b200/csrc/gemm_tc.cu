@@ -22,6 +22,23 @@
 // Operands use the canonical K-major SWIZZLE_128B layout: 8-row x 128-B
 // core groups 1024 B apart (SBO = 64 x 16 B), start address advanced by
 // 32 B per K = 8 step inside the swizzle atom.
+//
+// FP32 accuracy (3xTF32, the default): a TF32 operand keeps 10 of fp32's 23
+// mantissa bits, so one pass has a relative error of ~2^-11 per product --
+// far outside rtol 1e-3 on a K = 4096 dot product near cancellation.  Each
+// operand x is split as x = hi + lo with hi = x with its low 13 mantissa
+// bits cleared (exactly a TF32 value) and lo = x - hi (exact in fp32, |lo| <
+// 2^-10 |x|), and the tile product is accumulated as
+//     A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi
+// (the dropped A_lo.B_lo term is < 2^-20 relative; lo's own TF32 reading
+// adds < 2^-21).  The split happens in shared memory: the epilogue warps,
+// idle during the K loop, convert each landed stage (lo into a second
+// buffer of the same swizzled layout; the transform is elementwise, so the
+// swizzle needs no decoding) and release it to the MMA issuer through a
+// second mbarrier.  X3 = 1 keeps the landed x as "hi": valid because the
+// tensor core reads a TF32 operand with the low 13 bits ignored
+// (tools/tf32_probe.cu measures this); X3 = 2 also rewrites hi in place
+// (one more shared-memory store per element, correct under any reading).
 #include "common.h"
 
 #include <cudaTypedefs.h>
@@ -48,13 +65,15 @@ template <int BN>
 constexpr int tc_stages() { return BN >= 256 ? 4 : BN >= 128 ? 6 : 8; }
 constexpr int TC_THREADS = 192;
 
-template <int BN>
+template <int BN, int X3 = 0>
 struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 4;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = tc_stages<BN>();
+  static constexpr int RAW = A_BYTES + B_BYTES;
+  static constexpr int STAGE = X3 ? 2 * RAW : RAW;     // 3xTF32: + lo copies of both tiles
+  static constexpr int STAGES = X3 ? (192 * 1024) / STAGE : tc_stages<BN>();
   static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(STAGES >= 2, "smem ring needs two stages");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -114,19 +133,53 @@ __device__ __forceinline__ uint32_t tf32_idesc() {
          | ((uint32_t)(TC_BM >> 4) << 24);
 }
 
-template <int BN, bool MC = false, bool CR = false>
+// hi = x with the low 13 mantissa bits cleared (a TF32 value); lo = x - hi exactly
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// 3xTF32 split of one landed stage (X3 > 0): 128 epilogue threads, float4 granularity
+template <int X3>
+__device__ __forceinline__ void split_tile(uint8_t *raw, uint8_t *lo, int bytes, int t) {
+  float4 *r4 = reinterpret_cast<float4 *>(raw), *l4 = reinterpret_cast<float4 *>(lo);
+  constexpr int U = 4;
+  for (int i0 = t; i0 < bytes / 16; i0 += 128 * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * 128 < bytes / 16) v[u] = r4[i0 + u * 128];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + u * 128 >= bytes / 16) break;
+      const float4 h = make_float4(tf32_hi(v[u].x), tf32_hi(v[u].y), tf32_hi(v[u].z), tf32_hi(v[u].w));
+      l4[i0 + u * 128] = make_float4(v[u].x - h.x, v[u].y - h.y, v[u].z - h.z, v[u].w - h.w);
+      if constexpr (X3 == 2) r4[i0 + u * 128] = h;
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int BN, bool MC = false, bool CR = false, int X3 = 0>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
                       int M, int N, int K) {
-  using S = TcSmem<BN>;
+  using S = TcSmem<BN, X3>;
   constexpr int TC_STAGES = S::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *sA = smem;                                  // STAGES x A_BYTES
   uint8_t *sB = smem + TC_STAGES * S::A_BYTES;         // STAGES x B_BYTES
+  uint8_t *sAl = smem + TC_STAGES * S::RAW;            // X3: STAGES x A_BYTES (lo parts)
+  uint8_t *sBl = sAl + TC_STAGES * S::A_BYTES;         // X3: STAGES x B_BYTES
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * S::STAGE);
   uint64_t *empty = full + TC_STAGES;
-  uint64_t *tmem_full = empty + TC_STAGES;
+  uint64_t *conv = empty + TC_STAGES;                  // X3: stage split, 4 converter warps
+  uint64_t *tmem_full = conv + TC_STAGES;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,6 +202,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int s = 0; s < TC_STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], MC ? 2 : 1);   // MC: both CTAs' MMAs must release a slot
+        mbar_init(&conv[s], 4);
       }
       mbar_init(tmem_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -187,22 +241,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t idesc = tf32_idesc<BN>();
       for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % TC_STAGES, round = kb / TC_STAGES;
-        mbar_wait(&full[s], round & 1);
+        mbar_wait(X3 ? &conv[s] : &full[s], round & 1);
         if (kb == 0) gemm_mark(2);
         if (kb == kblocks / 2) gemm_mark(3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint64_t da = kmajor_sw128_desc(smem_u32(sA + s * S::A_BYTES));
         const uint64_t db = kmajor_sw128_desc(smem_u32(sB + s * S::B_BYTES));
+        const uint64_t dal = kmajor_sw128_desc(smem_u32(sAl + s * S::A_BYTES));
+        const uint64_t dbl = kmajor_sw128_desc(smem_u32(sBl + s * S::B_BYTES));
 #pragma unroll
         for (int k = 0; k < TC_BK / 8; ++k) {
           // advance 32 B (8 tf32) along K inside the 128-B swizzle row: +2 in 16-B units
           const uint64_t a = da + (uint64_t)(2 * k), b = db + (uint64_t)(2 * k);
           const uint32_t acc = (kb | k) ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t"
-              "setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(a), "l"(b), "r"(idesc), "r"(acc));
+          if constexpr (X3) {
+            // correction terms first (smallest magnitudes), then hi.hi
+            mma_tf32(tmem, dal + (uint64_t)(2 * k), b, idesc, acc);
+            mma_tf32(tmem, a, dbl + (uint64_t)(2 * k), idesc, 1u);
+            mma_tf32(tmem, a, b, idesc, 1u);
+          } else {
+            mma_tf32(tmem, a, b, idesc, acc);
+          }
         }
         // free the smem slot once these MMAs have read it (MC: in both CTAs,
         // whose producers both write into it)
@@ -223,6 +282,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    : "memory");
     }
   } else {
+    if constexpr (X3 > 0) {
+      // ---- 3xTF32 split: warps 2..5 convert each landed stage ----
+      const int t = threadIdx.x - 64;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % TC_STAGES, round = kb / TC_STAGES;
+        mbar_wait(&full[s], round & 1);
+        split_tile<X3>(sA + s * S::A_BYTES, sAl + s * S::A_BYTES, S::A_BYTES, t);
+        split_tile<X3>(sB + s * S::B_BYTES, sBl + s * S::B_BYTES, S::B_BYTES, t);
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+      }
+    }
     // ---- epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) ----
     mbar_wait(tmem_full, 0);
     if (warp == 2 && lane == 0) gemm_mark(5);
@@ -378,17 +451,17 @@ static bool sgemm_mc_enabled() {
   return on;
 }
 
-template <int BN, bool MC, bool CR = false>
+template <int BN, bool MC, bool CR, int X3>
 static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float *C, int M, int N, int K, int split,
                             cudaStream_t s) {
   // the smem opt-in is per device and context (FixedGSL instances launch from
   // fresh contexts): cheap, so set it on every launch
-  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN, MC, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TcSmem<BN>::TOTAL));
+  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN, MC, CR, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TcSmem<BN, X3>::TOTAL));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(N / BN, M / TC_BM, split);
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = TcSmem<BN>::TOTAL;
+  cfg.dynamicSmemBytes = TcSmem<BN, X3>::TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   if (MC || CR) {
@@ -399,11 +472,11 @@ static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  SAGE_CUDA(cudaLaunchKernelEx(&cfg, sgemm_tf32_kernel<BN, MC, CR>, ma, mb, C, M, N, K));
+  SAGE_CUDA(cudaLaunchKernelEx(&cfg, sgemm_tf32_kernel<BN, MC, CR, X3>, ma, mb, C, M, N, K));
   return SAGE_OK;
 }
 
-template <int BN>
+template <int BN, int X3>
 static int launch_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
   // 2-CTA clusters along M when the M tiles pair up
   const bool mc = sgemm_mc_enabled() && (M / TC_BM) % 2 == 0;
@@ -423,12 +496,32 @@ static int launch_tc(const float *A, const float *BT, float *C, int M, int N, in
   static const bool cr_on = [] { const char *e = getenv("SAGE_SGEMM_CR"); return !(e && atoi(e) == 0); }();
   const bool cr = cr_on && !mc && split > 1 && split <= 8 && TC_BM % split == 0;
   if (split > 1 && !cr) SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
-  const int rc = mc ? launch_tc_kernel<BN, true>(ma, mb, C, M, N, K, split, s)
-                 : cr ? launch_tc_kernel<BN, false, true>(ma, mb, C, M, N, K, split, s)
-                      : launch_tc_kernel<BN, false>(ma, mb, C, M, N, K, split, s);
+  const int rc = mc ? launch_tc_kernel<BN, true, false, X3>(ma, mb, C, M, N, K, split, s)
+                 : cr ? launch_tc_kernel<BN, false, true, X3>(ma, mb, C, M, N, K, split, s)
+                      : launch_tc_kernel<BN, false, false, X3>(ma, mb, C, M, N, K, split, s);
   if (rc != SAGE_OK) return rc;
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
+}
+
+// SAGE_SGEMM_PASSES: 3 (default) = 3xTF32, FP32-accurate, with the landed x
+// used as hi (X3 = 1); 4 = 3xTF32 with hi rewritten in place (X3 = 2);
+// 1 = single-pass TF32 (diagnostics: the round-1 kernel)
+int sgemm_passes() {
+  static const int v = [] { const char *e = getenv("SAGE_SGEMM_PASSES"); return e ? atoi(e) : 3; }();
+  return v;
+}
+
+template <int X3>
+static int sgemm_tc_x(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
+  // widest N tile that divides N: A (the shared weights, the dominant
+  // operand of these skinny GEMMs) is then streamed through smem once
+  static const int force_bn = [] { const char *e = getenv("SAGE_SGEMM_BN"); return e ? atoi(e) : 0; }();
+  if (force_bn == 64) return launch_tc<64, X3>(A, BT, C, M, N, K, s);       // diagnostics: tile sweep
+  if (force_bn == 128 && N % 128 == 0) return launch_tc<128, X3>(A, BT, C, M, N, K, s);
+  if (N % 256 == 0) return launch_tc<256, X3>(A, BT, C, M, N, K, s);
+  if (N % 128 == 0) return launch_tc<128, X3>(A, BT, C, M, N, K, s);
+  return launch_tc<64, X3>(A, BT, C, M, N, K, s);
 }
 
 // M % 128 == 0, N % 64 == 0, K % 32 == 0, 16-B aligned operands
@@ -437,28 +530,26 @@ int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cud
     return fail(SAGE_EINVAL, "sgemm (tcgen05): M % 128, N % 64 and K % 32 must be 0");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(BT) | reinterpret_cast<uintptr_t>(C)) & 15)
     return fail(SAGE_EINVAL, "sgemm (tcgen05): operands must be 16-byte aligned");
-  // widest N tile that divides N: A (the shared weights, the dominant
-  // operand of these skinny GEMMs) is then streamed through smem once
-  static const int force_bn = [] { const char *e = getenv("SAGE_SGEMM_BN"); return e ? atoi(e) : 0; }();
-  if (force_bn == 64) return launch_tc<64>(A, BT, C, M, N, K, s);       // diagnostics: tile sweep
-  if (force_bn == 128 && N % 128 == 0) return launch_tc<128>(A, BT, C, M, N, K, s);
-  if (N % 256 == 0) return launch_tc<256>(A, BT, C, M, N, K, s);
-  if (N % 128 == 0) return launch_tc<128>(A, BT, C, M, N, K, s);
-  return launch_tc<64>(A, BT, C, M, N, K, s);
+  const int p = sgemm_passes();
+  if (p == 1) return sgemm_tc_x<0>(A, BT, C, M, N, K, s);
+  if (p == 4) return sgemm_tc_x<2>(A, BT, C, M, N, K, s);
+  return sgemm_tc_x<1>(A, BT, C, M, N, K, s);
 }
 
-int touch_tc_kernels() {
+// module-load the sgemm kernels of the configured precision (a fresh
+// FixedGSL context loads only what its body needs)
+template <int X3>
+static int touch_x() {
   cudaFuncAttributes a;
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64, true>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, true>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, true>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64, false, true>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, false, true>));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, true>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, true, X3>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, false, X3>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, false, true, X3>));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<64, false, true, X3>));
   return SAGE_OK;
+}
+int touch_tc_kernels() {
+  const int p = sgemm_passes();
+  return p == 1 ? touch_x<0>() : p == 4 ? touch_x<2>() : touch_x<1>();
 }
 
 }  // namespace sage

@@ -387,11 +387,18 @@ int sage_pool_free(sage_handle h) {
   return SAGE_OK;
 }
 
-int sage_pool_free_after(sage_handle h, sage_handle evh) {
+int sage_pool_free_after_n(sage_handle h, const sage_handle *evs, int n) {
   if (handle_kind(h) != Kind::Alloc) return fail(SAGE_EINVAL, "not a pool handle");
-  Event *E = event_get(evh);
-  if (!E || !E->ev) return fail(SAGE_ESTATE, "free_after: unknown event");
-  SAGE_TRY(event_await_recorded(E));
+  if (n < 0 || (n > 0 && !evs)) return fail(SAGE_EINVAL, "free_after: bad event list");
+  std::vector<Event *> E;
+  for (int i = 0; i < n; ++i) {
+    if (!evs[i]) continue;
+    Event *e = event_get(evs[i]);
+    if (!e || !e->ev) return fail(SAGE_ESTATE, "free_after: unknown event");
+    SAGE_TRY(event_await_recorded(e));
+    E.push_back(e);
+  }
+  if (E.empty()) return sage_pool_free(h);
   Alloc *A = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_alloc_mu);
@@ -409,12 +416,18 @@ int sage_pool_free_after(sage_handle h, sage_handle evh) {
   cudaSetDevice(dev_of(A->gpu));
   cudaEvent_t ev;
   SAGE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  // chain: our private event completes when the caller's event does
-  SAGE_CUDA(cudaStreamWaitEvent(G->aux, E->ev, 0));
+  // chain: our private event completes when every reader's event has (the
+  // readers may run on other GPUs: a peer land over NVLink)
+  for (Event *e : E) SAGE_CUDA(cudaStreamWaitEvent(G->aux, e->ev, 0));
   SAGE_CUDA(cudaEventRecord(ev, G->aux));
   P->zombies.emplace_back(A, ev);
   reap(P, false);
   return SAGE_OK;
+}
+
+int sage_pool_free_after(sage_handle h, sage_handle evh) {
+  if (!evh) return fail(SAGE_ESTATE, "free_after: unknown event");
+  return sage_pool_free_after_n(h, &evh, 1);
 }
 
 int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total, uint64_t *physical_total,

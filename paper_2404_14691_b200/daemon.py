@@ -114,7 +114,7 @@ class MemoryDaemon:
                 fd.ro_checksum = res.checksum
             elif fd.ro_checksum != res.checksum:
                 raise SimulationError(f"{name}: landed checksum {res.checksum:016x} != {fd.ro_checksum:016x}")
-            r.ro_checksum = res.checksum
+            sim.sharing.record_checksum(r, res.checksum)
             r.ro_token.set_ready(sim.engine.tick())
             self.loads += 1
         elif r.ro_token is not None and not r.ro_token.ready and r.ro_token.event is not None:

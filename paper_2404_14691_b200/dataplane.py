@@ -206,6 +206,24 @@ _STAGES = [Stage.CONTAINER, Stage.CPU_CTX, Stage.CPU_LOAD, Stage.GPU_CTX, Stage.
            Stage.COMPUTE, Stage.RETURN]
 
 
+def _add_reader(resident, ev_h: int) -> None:
+    """A land on another GPU reads `resident`'s RO segment over NVLink: keep
+    an alias of its END event so freeing the segment waits for it (finished
+    readers are dropped as new ones arrive)."""
+    if not ev_h:
+        return
+    alias = _lib.H(0)
+    _lib.check(_lib.lib().sage_event_alias(ev_h, _lib.C.byref(alias)), "sage_event_alias")
+    live = []
+    for e in resident.readers:
+        if _lib.lib().sage_event_query(e.h) == _lib.SAGE_OK:
+            e.release()
+        else:
+            live.append(e)
+    live.append(D.Event(alias.value))
+    resident.readers = live
+
+
 class _Borrowed(D.Event):
     """An event owned by a native invocation: released with it, never alone."""
 
@@ -439,6 +457,7 @@ class DataPlane:
             d.ctx_dptr, d.ctx_bytes = self._ctx_dst(run)
         box = self.box
         publish = False
+        peer = None
         ro = 0
         if fd.layout.seg_bytes:
             if resident is not None and resident.gpu_ro is not None:
@@ -546,6 +565,8 @@ class DataPlane:
         run.invh = h.value
         run.end = _Borrowed(done.value)
         self._gate_push(run)
+        if run.ro_source == "nvlink" and peer is not None:
+            _add_reader(peer, ro_end.value or done.value)
         if publish:
             # home rank: send the landed segment to the other ranks; eviction
             # waits for the send (sharing._evict)
@@ -631,8 +652,8 @@ class DataPlane:
             if a.cls is AllocClass.CONTEXT:
                 return a.dptr, a.requested
         slot = getattr(inv, "ctx_slot", None)
-        if slot is not None and slot.alloc is not None:
-            return slot.alloc.dptr, slot.alloc.requested
+        if slot is not None and slot.seg is not None:
+            return slot.seg.dptr, slot.seg.requested
         return 0, 0
 
     def _peer_source(self, run: _Run):
@@ -791,6 +812,7 @@ class DataPlane:
                 op = D.load(gpu, dst, None, None, device_src=peer.gpu_ro.dptr,
                             device_src_bytes=fd.layout.seg_bytes, peer_gpu=peer.gpu, wait=w)
                 run.ro_source = "nvlink"
+                _add_reader(peer, op.end.h)
             elif fd.db_dev is not None:
                 op = D.load(gpu, dst, None, fd.layout, device_src=fd.db_dev.dptr,
                             device_src_bytes=fd.layout.packed_bytes, wait=wait)
@@ -921,8 +943,8 @@ class DataPlane:
         elif fd.ro_checksum != checksum:
             raise SimulationError(f"{inv}: landed read-only segment checksum {checksum:016x} != "
                                   f"{fd.ro_checksum:016x} (source {run.ro_source})")
-        if r is not None:
-            r.ro_checksum = checksum
+        if r is not None and grant.leader_ro and r.gpu_ro is not None and r.ro_checksum is None:
+            self.sim.sharing.record_checksum(r, checksum)    # the content index of the native table
 
     def _release(self, run: _Run) -> None:
         if run.invh:

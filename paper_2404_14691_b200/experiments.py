@@ -32,7 +32,7 @@ from .workload import OpenLoopSource, PoissonOpenSpec, generate_arrivals
 def _evict_all(sim) -> None:
     if sim.sharing is not None:
         for r in list(sim.sharing.residents.values()):
-            sim.sharing._evict(r)
+            sim.sharing.evict(r)
 
 
 def _round(d):

@@ -94,9 +94,13 @@ class DevicePool:
             raise MemoryError(exc.shortfall) from exc
 
     def free(self, seg, after=None) -> None:
-        if after is not None and after.h:
+        """`after`: a device Event or a list of them (the pages outlive the
+        ledger entry until every one completed)."""
+        evs = [e.h for e in (after if isinstance(after, (list, tuple)) else [after]) if e is not None and e.h]
+        if evs:
             from . import _lib
-            _lib.check(_lib.lib().sage_pool_free_after(seg.h, after.h), "sage_pool_free_after")
+            _lib.check(_lib.lib().sage_pool_free_after_n(seg.h, (_lib.H * len(evs))(*evs), len(evs)),
+                       "sage_pool_free_after_n")
             seg.h = 0
         else:
             seg.free()
@@ -164,8 +168,9 @@ class MemoryLedger:
         return alloc
 
     def free(self, alloc: Allocation, after=None) -> None:
-        """Release now; with `after` (a device Event) the physical pages are
-        returned only once that event completes (a D2H may still read them)."""
+        """Release now; with `after` (a device Event, or a list) the physical
+        pages are returned only once it completes (a D2H or a peer land may
+        still read them)."""
         if self._allocs.get(alloc.id) is not alloc:
             raise SimulationError(f"ledger {self.name}: double or unknown free (id={alloc.id})")
         del self._allocs[alloc.id]

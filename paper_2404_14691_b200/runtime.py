@@ -284,9 +284,9 @@ class Simulation:
                         persistent += alloc.effective
         if isinstance(self.policy, PoolPolicy):
             for pool in self.policy.pools.values():
-                for slot in pool.slots:
-                    if slot.alloc is not None:
-                        persistent += slot.alloc.effective
+                for slot in pool.contexts:
+                    if slot.seg is not None:
+                        persistent += slot.seg.effective
         actual = sum(l.usage for l in self.gpu_ledgers)
         if actual != persistent:
             raise SimulationError(f"GPU memory leak: {actual} B held vs {persistent} B persistent")
@@ -296,14 +296,13 @@ class Simulation:
     def close(self) -> None:
         """Free everything and shut the device plane down."""
         if self.sharing is not None:
-            for r in list(self.sharing.residents.values()):
-                self.sharing._evict(r)
+            self.sharing.close()
         if isinstance(self.policy, PoolPolicy):
             for (name, gpu), pool in self.policy.pools.items():
-                for slot in pool.slots:
-                    if slot.alloc is not None:
-                        self.gpu_ledgers[gpu].free(slot.alloc)
-                        slot.alloc = None
+                for slot in pool.contexts:
+                    if slot.seg is not None:
+                        self.gpu_ledgers[gpu].free(slot.seg)
+                        slot.seg = None
         self.dataplane.close()
         if self._owns_device:
             _lib.shutdown()

@@ -1,6 +1,7 @@
 """Function bodies called directly through the C-ABI (sage_launch) against
-numpy references: the tcgen05 TF32 GEMM over several shapes, the SIMT fp32
-GEMM at strict fp32 tolerance, stencil and spmv edge shapes."""
+numpy references: the tcgen05 3xTF32 GEMM over several shapes at the FP32
+contract (rtol 1e-3, atol 1e-4 * max|C|), the SIMT fp32 GEMM, stencil and
+spmv edge shapes."""
 import numpy as np
 import pytest
 
@@ -36,7 +37,7 @@ def run_body(kind, ro, ro_bytes, inp, inp_bytes, out_bytes, args):
 
 @pytest.mark.parametrize("m,n,k", [(128, 64, 32), (256, 128, 256), (512, 256, 4096), (4096, 256, 4096),
                                    (1024, 192, 96)])
-def test_sgemm_tcgen05_tf32(dp, m, n, k):
+def test_sgemm_tcgen05_fp32(dp, m, n, k):
     rng = np.random.default_rng(m + n + k)
     A = rng.standard_normal((m, k), dtype=np.float32)
     BT = rng.standard_normal((n, k), dtype=np.float32)
@@ -44,10 +45,13 @@ def test_sgemm_tcgen05_tf32(dp, m, n, k):
     got = run_body(_lib.BODY_SGEMM, sa.dptr, A.nbytes, sb.dptr, BT.nbytes, m * n * 4, (m, n, k))
     got = got.view(np.float32).reshape(m, n)
     want = O.sgemm_ref(A, BT.T)
-    # TF32 MMA inputs (10-bit mantissa), fp32 accumulation: 4-sigma rounding bound
-    np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
-    # and it is really TF32, not garbage that happens to be small
-    assert np.abs(got - want).max() < 0.05 * np.abs(want).max()
+    # FP32 contract (north_star): rtol 1e-3 with atol 1e-4 * max|C|.  A
+    # single TF32 pass misses it (error ~2^-11 * sqrt(K) per element); the
+    # 3xTF32 split is ~2^-21
+    np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-4 * np.abs(want).max())
+    # and well inside it: the residual is at fp32 level, not TF32 level
+    err = np.abs(got.astype(np.float64) - want).max() / np.abs(want).max()
+    assert err < 1e-5, err   # one TF32 pass: ~1e-4
     sa.free()
     sb.free()
 

@@ -147,8 +147,8 @@ def test_parboil_bodies_match_oracle(built_lib):
                 m, n, k = fd.args
                 want = O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(n, k).T)
                 got = inv.result.view(np.float32).reshape(m, n)
-                # TF32 MMA inputs (10-bit mantissa): 4-sigma bound of the rounding error
-                np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
+                # FP32 contract (3xTF32 tcgen05): rtol 1e-3, atol 1e-4 * max|C|
+                np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-4 * np.abs(want).max())
             elif fd.body == "stencil":
                 nx, ny, nz, bits = fd.args
                 beta = float(np.int32(bits).view(np.float32))
@@ -197,7 +197,7 @@ def test_full_size_cfg2_burst(built_lib):
                 rows = np.arange(0, m, 97)
                 want = (A[rows].astype(np.float64) @ BT.T.astype(np.float64)).astype(np.float32)
                 got = inv.result.view(np.float32).reshape(m, n)[rows]
-                np.testing.assert_allclose(got, want, rtol=1e-3, atol=4 * 2.0 ** -10 * np.sqrt(k))
+                np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-4 * np.abs(want).max())
         sim.check_no_leaks()
     finally:
         sim.close()

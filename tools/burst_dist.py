@@ -26,7 +26,7 @@ if "pre" in sys.argv:   # the bench order: e2e bursts (pinned payloads / store) 
             sim.dataplane.pin_host_store()
         for rep in range(13):
             for r in list(sim.sharing.residents.values()):
-                sim.sharing._evict(r)
+                sim.sharing.evict(r)
             sim.submit_many(names, payloads=pls)
             sim.drain()
     sim.dataplane.unpin_host_store()
@@ -38,7 +38,7 @@ _lib.lib().sage_stats_enable(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 rows = []
 for rep in range(45):
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     t0 = time.perf_counter()
     sim.submit_many(names)
     t1 = time.perf_counter()

@@ -31,7 +31,7 @@ walls = []
 import time  # noqa: E402
 for rep in range(6):
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     t_sub = time.perf_counter()
     invs = sim.submit_many(names, payloads=pls)
     t_done = time.perf_counter()

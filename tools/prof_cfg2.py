@@ -30,7 +30,7 @@ elif mode == "e2e":
 
 def burst():
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     t0 = time.perf_counter()
     invs = sim.submit_many(names, payloads=payloads)
     t1 = time.perf_counter()

@@ -1,4 +1,4 @@
-"""ncu driver: the cfg-2 sgemm shape (4096 x 256 x 4096, TF32 tcgen05) launched
+"""ncu driver: the cfg-2 sgemm shape (4096 x 256 x 4096, tcgen05; SAGE_SGEMM_PASSES picks 3xTF32 or TF32) launched
 back to back.  ncu -k regex:sgemm_tf32 -c 2 python tools/prof_gemm.py"""
 import sys
 import time
@@ -35,5 +35,6 @@ for b, e in evs[2:]:
     d = D.C.c_double()
     _lib.check(_lib.lib().sage_event_elapsed(b.h, e.h, D.C.byref(d)), "elapsed")
     us.append(d.value)
-print(f"sgemm tf32 {m}x{n}x{k}: median {np.median(us):.1f} us = {2*m*n*k/np.median(us)/1e6:.1f} TFLOP/s")
+import json, os  # noqa: E402
+print(json.dumps({"sgemm": f"{m}x{n}x{k}", "passes": os.environ.get("SAGE_SGEMM_PASSES", "3"), "bn": os.environ.get("SAGE_SGEMM_BN", "auto"), "median_us": round(float(np.median(us)), 2), "tflops_alg": round(2 * m * n * k / np.median(us) / 1e6, 1)}))
 _lib.shutdown()

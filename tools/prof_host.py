@@ -52,7 +52,7 @@ for rep in range(25):
         cnt.clear()
         t0 = time.perf_counter()
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     sim.submit_many(names)
     sim.drain()
 wall = time.perf_counter() - t0

@@ -16,14 +16,14 @@ for rep in range(3):
     invs = sim.submit_many(["fn100"] * 64)
     sim.drain()
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
 pr = cProfile.Profile()
 pr.enable()
 for rep in range(5):
     invs = sim.submit_many(["fn100"] * 64)
     sim.drain()
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
 pr.disable()
 print(summarize_setup(invs))
 pstats.Stats(pr).sort_stats("tottime").print_stats(25)

@@ -32,7 +32,7 @@ for stats in (0, 1):
     L.sage_stats_enable(stats)
     for rep in range(8):
         for r in list(sim.sharing.residents.values()):
-            sim.sharing._evict(r)
+            sim.sharing.evict(r)
         acc["invoke"] = 0.0
         acc["n"] = 0
         t0 = time.perf_counter()
@@ -54,13 +54,13 @@ sim.dataplane.results_in_hbm = True
 L.sage_stats_enable(0)
 for rep in range(3):
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     sim.submit_many(names)
     sim.drain()
 pr = cProfile.Profile()
 for rep in range(4):
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     pr.enable()
     sim.submit_many(names)
     sim.drain()

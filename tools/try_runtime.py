@@ -40,7 +40,7 @@ for pol in pols:
             out[f"{pol}_rep{rep}"] = s
             if sim.sharing is not None:   # force a cold start next rep
                 for r in list(sim.sharing.residents.values()):
-                    sim.sharing._evict(r)
+                    sim.sharing.evict(r)
         sim.check_no_leaks()
     finally:
         sim.close()
