@@ -18,10 +18,11 @@ Both are whole-job aggregates over all ranks (max-over-ranks device time).
 Extra keys: p50/p99 setup latency (compute_begin - arrival), the cfg-1
 SAGE-vs-FixedGSL setup comparison (16 concurrent 100 MiB cold starts,
 `--cfg1`), per-kernel rooflines measured live with CUDA events, and the CPU
-baseline (the oracle's host-only loading path + numpy bodies, bounded sample).
+baseline (oracle/cpu_path.py: the same burst served on the host cores, each
+invocation's copy + unpack + checksum and fp32 body on its own core).
 
-`--impl reference` times the reference's CPU path instead (the oracle port:
-host-only loading + CPU bodies on all host cores) and prints its own line.
+`--impl reference` times that host-only serving path as the reference arm
+(full bursts, all cores) and prints its own line.
 """
 from __future__ import annotations
 
@@ -549,11 +550,19 @@ def cfg1_compare(n: int = 16) -> dict:
     out = {}
     # SAGE_pinned_store: the memory daemon keeps the function's DB record in
     # pinned host memory (registered once, as SAGE's daemon caches function
-    # data on the host); SAGE and FixedGSL read it pageable per cold start
-    for pol, reps in (("SAGE", 6), ("SAGE_pinned_store", 6), ("FixedGSL", 1)):
-        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol.split("_pinned")[0]), {spec.name: spec}, seed=1,
+    # data on the host); the others read it pageable per cold start.
+    # FixedGSL rows: a fresh CUDA context per instance, on a library thread of
+    # this process ("thread") or in its own OS process ("process": what a
+    # container per function pays), alone (N=1) and 16 at once.  DGSF: four
+    # pre-created contexts (registration time), serial data loading.
+    rows = (("SAGE", "SAGE", "thread", n, 6), ("SAGE_pinned_store", "SAGE", "thread", n, 6),
+            ("DGSF", "DGSF", "thread", n, 3),
+            ("FixedGSL_thread_n1", "FixedGSL", "thread", 1, 3), ("FixedGSL_thread", "FixedGSL", "thread", n, 1),
+            ("FixedGSL_process_n1", "FixedGSL", "process", 1, 3), ("FixedGSL_process", "FixedGSL", "process", n, 1))
+    for row, pol, mode, burst, reps in rows:
+        sim = Simulation(ClusterSpec(gpus=1, instance_mode=mode), policy_preset(pol), {spec.name: spec}, seed=1,
                          function_data={spec.name: data})
-        if pol.endswith("pinned_store"):
+        if row.endswith("pinned_store"):
             sim.dataplane.pin_host_store()
         try:
             samples = []
@@ -561,59 +570,45 @@ def cfg1_compare(n: int = 16) -> dict:
                 if sim.sharing is not None:
                     for r in list(sim.sharing.residents.values()):
                         sim.sharing.evict(r)
-                invs = sim.submit_many([spec.name] * n)
+                invs = sim.submit_many([spec.name] * burst)
                 sim.drain()
-                if rep >= (1 if reps > 1 else 0):   # first SAGE burst is warm-up
+                if rep >= (1 if reps > 1 else 0):   # the first burst is a warm-up
                     samples += invs
             s = summarize_setup(samples)
             s["bursts"] = reps - (1 if reps > 1 else 0)
-            out[pol] = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in s.items()}
+            s["concurrent"] = burst
+            out[row] = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in s.items()}
         finally:
             sim.close()
-    out["p50_setup_ratio_fixedgsl_over_sage"] = round(out["FixedGSL"]["setup_p50_ms"] / out["SAGE"]["setup_p50_ms"], 1)
+    sage = out["SAGE"]["setup_p50_ms"]
+    out["p50_setup_ratio_fixedgsl_over_sage"] = round(out["FixedGSL_thread"]["setup_p50_ms"] / sage, 1)
+    out["p50_setup_ratio_fixedgsl_process_over_sage"] = round(out["FixedGSL_process"]["setup_p50_ms"] / sage, 1)
+    out["p50_setup_ratio_dgsf_over_sage"] = round(out["DGSF"]["setup_p50_ms"] / sage, 1)
     out["workload"] = f"{n} concurrent cold starts, 100 MiB RO (64 ragged tensors), 10 MiB writable, 1 MiB input"
     return out
 
 
-def cpu_baseline(budget_s: float = 15.0, max_inv: int = 9) -> dict:
-    """The oracle's host-only path on this box's host cores: per invocation,
-    DB record -> private buffer -> unpack -> checksum, the input copy, and the
-    function body in numpy (BLAS sgemm / vectorised stencil / spmv)."""
-    import numpy as np
-
-    from oracle import oracle as O
+def cpu_baseline(burst: int = 64, bursts: int = 3) -> dict:
+    """The host-only serving path on this box's cores (oracle/cpu_path.py):
+    the same cfg-2 burst, every invocation loaded (copy + unpack + checksum)
+    and computed (fp32 torch-CPU body) on its own core, all cores busy."""
+    from oracle.cpu_path import CpuServer, host_info
     from paper_2404_14691_b200.parboil import cfg2_functions
     table, data = cfg2_functions()
-    names = burst_names(table, max_inv)
-    cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    done = 0
-    for name in names:
-        fd = data[name]
-        lay = fd.layout
-        sums = O.hostpath_c(fd.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes, 1, cores)
-        seg, _ = O.land_c(fd.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
-        x = fd.input.copy()
-        if fd.body == "sgemm":
-            m, n, k = fd.args
-            O.sgemm_ref(seg[:m * k * 4].view(np.float32).reshape(m, k), x.view(np.float32).reshape(n, k).T)
-        elif fd.body == "stencil":
-            nx, ny, nz, bits = fd.args
-            beta = float(np.int32(bits).view(np.float32))
-            O.stencil_ref(seg.view(np.float32)[:nx * ny * nz].reshape(nz, ny, nx),
-                          x.view(np.float32).reshape(nz, ny, nx), beta)
-        else:
-            rows, nnz, o_rp, o_col, o_val = fd.args
-            O.spmv_ref(seg[o_rp:o_rp + 4 * (rows + 1)].view(np.int32), seg[o_col:o_col + 4 * nnz].view(np.int32),
-                       seg[o_val:o_val + 4 * nnz].view(np.float32), x.view(np.float32))
-        done += 1
-        assert int(sums[0]) != 0
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": round(done / dt, 3), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{done} invocations of the cfg-2 mix (host-only load+unpack+checksum, numpy body), "
-                      f"{dt:.1f} s"}
+    names = burst_names(table, burst)
+    srv = CpuServer(data, workers=min(os.cpu_count() or 1, burst))
+    try:
+        srv.burst(names[:srv.workers])            # warm (threads, allocator, torch kernels)
+        dts = [srv.burst(names) for _ in range(bursts)]
+        lp = srv.load_path_rates()
+    finally:
+        srv.close()
+    v = burst * len(dts) / sum(dts)
+    return {"value": round(v, 2), "unit": UNIT, "cores": srv.workers, "kind": "port",
+            "sample": f"{len(dts)} full bursts of {burst} cfg-2 invocations, {sum(dts):.2f} s: per invocation "
+                      f"host copy + unpack + checksum (C) and the fp32 body (torch-CPU, 1 thread), "
+                      f"{srv.workers} invocations at a time on {srv.workers} threads",
+            "host": host_info(), "load_path": lp}
 
 
 def our_arm(args, rank, world, dist) -> dict:
@@ -818,29 +813,35 @@ def workload_config(burst: int, world: int) -> dict:
 
 
 def reference_arm(args, rank, world) -> dict:
-    """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
-    steps, warmup = args.steps, args.warmup
-    for _ in range(warmup):
-        cpu_baseline(budget_s=2.0, max_inv=1)
-    vals = []
-    t0 = time.perf_counter()
-    done = 0
-    for _ in range(steps):
-        b = cpu_baseline(budget_s=8.0, max_inv=3)
-        vals.append(b["value"])
-        done += 3
-    dt = time.perf_counter() - t0
-    v = done / dt
-    cores = os.cpu_count() or 1
-    return {"metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
-            "ms_per_step": round(dt * 1e3 / steps, 1), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32 (bodies) / u8 (load)", "data": "synthetic", "impl": "reference",
-            "config": workload_config(args.burst, world),
-            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{done} invocations over {steps} steps: each step 3 invocations (one per "
-                                       f"function) of the cfg-2 burst through the reference's host-only path "
-                                       f"(oracle port: load + unpack + checksum on all host threads, numpy bodies)"},
-            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    """--impl reference: the reference's CPU path on this box's host cores
+    (the host-only serving path of oracle/cpu_path.py; the reference itself
+    is a simulator with nothing to time), rank 0 only.  One step = one full
+    cfg-2 burst of `--burst` invocations, the same workload our arm serves."""
+    from oracle.cpu_path import CpuServer, host_info
+    from paper_2404_14691_b200.parboil import cfg2_functions
+    table, data = cfg2_functions()
+    names = burst_names(table, args.burst)
+    srv = CpuServer(data, workers=min(os.cpu_count() or 1, args.burst))
+    try:
+        for _ in range(args.warmup):
+            srv.burst(names)
+        dts = [srv.burst(names) for _ in range(args.steps)]
+        lp = srv.load_path_rates()
+    finally:
+        srv.close()
+    total = sum(dts)
+    v = args.burst * args.steps / total
+    return {"metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total * 1e3 / args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (bodies) / u8 (load)", "data": "synthetic",
+            "impl": "reference", "config": workload_config(args.burst, world),
+            "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": srv.workers, "kind": "port",
+                             "sample": f"{args.steps} full bursts of {args.burst} cfg-2 invocations after "
+                                       f"{args.warmup} warm-up bursts: per invocation host copy + unpack + "
+                                       f"checksum (C) and the fp32 body (torch-CPU, 1 thread), {srv.workers} "
+                                       f"invocations at a time on {srv.workers} threads",
+                             "host": host_info(), "load_path": lp},
+            "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():

@@ -312,15 +312,19 @@ int sage_invoke_release(sage_handle inv);
  * One invocation = fresh cuCtxCreate + cudaMalloc + pageable synchronous
  * per-tensor cudaMemcpy + body + D2H + context teardown, run on a library
  * worker thread; completion is polled through its end event.                 */
+#define SAGE_INSTANCE_THREAD   0  /* a fresh context on a library worker thread        */
+#define SAGE_INSTANCE_PROCESS  1  /* a fresh OS process per instance (sage_instance_worker) */
+#define SAGE_INSTANCE_POOLED   2  /* DGSF: run in a pre-created context (no GPU_CTX)    */
 typedef struct {
   int32_t gpu;
-  int32_t pad_;
+  int32_t mode;                  /* SAGE_INSTANCE_*                                  */
   sage_handle layout;            /* RO layout (0 = identity)                         */
   const void *ro_src; uint64_t ro_src_bytes;
   const void *input;  uint64_t input_bytes;
   uint64_t alloc_bytes;          /* device bytes the instance reserves (1 GiB-rounded) */
   sage_body_desc body;           /* ro/input/out pointers are filled in by the worker */
   void *result; uint64_t result_bytes;
+  sage_handle ctx;               /* SAGE_INSTANCE_POOLED: from sage_instance_ctx_create */
 } sage_fixedgsl_desc;
 typedef struct {
   int64_t t[16];                 /* begin/end per reference Stage (functions.py:164-176
@@ -334,6 +338,13 @@ typedef struct {
 int sage_fixedgsl_submit(const sage_fixedgsl_desc *d, sage_handle *job, sage_handle *end_ev);
 int sage_fixedgsl_info_get(sage_handle job, sage_fixedgsl_info *out);
 int sage_fixedgsl_release(sage_handle job);
+/* DGSF's pre-created contexts (policies.py:163-179): a real cuCtxCreate made at
+ * registration with the body's kernels loaded; one job at a time runs in it  */
+int sage_instance_ctx_create(int gpu, int body, sage_handle *ctx);
+int sage_instance_ctx_destroy(sage_handle ctx);
+/* the entry of an instance process (SAGE_INSTANCE_PROCESS): sage_instance_worker
+ * calls it with the memfd of its region; not for other callers               */
+int sage_instance_child(int fd);
 
 /* ---- measurement ------------------------------------------------------------
  * Live kernel timing for the roofline: when enabled, every land / body launch

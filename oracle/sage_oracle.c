@@ -48,12 +48,15 @@ static inline uint64_t pair_term(uint32_t lo, uint32_t hi, uint64_t p) {
 
 /* checksum of `bytes` (multiple of 8) starting at 64-bit word index word_base */
 uint64_t oracle_checksum(const uint8_t *p, uint64_t bytes, uint64_t word_base) {
+  /* one 64-bit load per word: this form vectorises (AVX2 vpmuludq) */
   uint64_t s = 0, n = bytes / 8;
   for (uint64_t i = 0; i < n; ++i) {
-    uint32_t lo, hi;
-    memcpy(&lo, p + 8 * i, 4);
-    memcpy(&hi, p + 8 * i + 4, 4);
-    s += pair_term(lo, hi, word_base + i);
+    uint64_t w;
+    memcpy(&w, p + 8 * i, 8);
+    const uint64_t q = word_base + i;
+    const uint32_t k = (uint32_t)q * 0x9E3779B1u ^ (uint32_t)(q >> 32) * 0x85EBCA77u;
+    const uint32_t a = (uint32_t)w ^ k, b = (uint32_t)(w >> 32) ^ (k + 0x7F4A7C15u);
+    s += (uint64_t)a * b + (((uint64_t)b << 32) | a);
   }
   return s;
 }
@@ -145,4 +148,71 @@ out:
   if (J.scratch) for (int t = 0; t < threads; ++t) free(J.scratch[t]);
   free(J.scratch); free(th); free(args);
   return rc;
+}
+
+/* ---- the host-only path as a CPU serving process would run it ------------
+ * One invocation on one core: CPU_LOAD (DB record -> the invocation's private
+ * host buffer), then unpack + checksum fused window by window so the
+ * checksum reads the bytes while they are still in cache (one pass over the
+ * segment instead of two).  Same bytes and checksum as oracle_land.          */
+uint64_t oracle_load_into(const uint8_t *db, const uint64_t *src_off, const uint64_t *dst_off,
+                          const uint64_t *len, uint32_t n, uint64_t packed_bytes, uint8_t *priv, uint8_t *seg,
+                          uint64_t seg_bytes) {
+  memcpy(priv, db, packed_bytes);
+  const uint64_t W = 256 << 10;
+  uint64_t s = 0;
+  uint32_t t = 0;
+  for (uint64_t w0 = 0; w0 < seg_bytes; w0 += W) {
+    const uint64_t w1 = w0 + W < seg_bytes ? w0 + W : seg_bytes;
+    uint64_t cur = w0;
+    while (t < n && dst_off[t] + len[t] <= w0) ++t;          /* tensors ending before the window */
+    for (uint32_t i = t; i < n && dst_off[i] < w1; ++i) {
+      const uint64_t a = dst_off[i] > w0 ? dst_off[i] : w0;
+      const uint64_t e = dst_off[i] + len[i] < w1 ? dst_off[i] + len[i] : w1;
+      if (a > cur) memset(seg + cur, 0, a - cur);
+      if (e > a) memcpy(seg + a, priv + src_off[i] + (a - dst_off[i]), e - a);
+      if (e > cur) cur = e;
+    }
+    if (w1 > cur) memset(seg + cur, 0, w1 - cur);
+    s += oracle_checksum(seg + w0, w1 - w0, w0 / 8);
+  }
+  return s;
+}
+
+/* aggregate memcpy rate (GB/s, read + write bytes) of `threads` threads each
+ * copying its own `bytes` buffer `reps` times: the host memory roofline    */
+typedef struct { uint8_t *a, *b; uint64_t bytes; int reps; } memcpy_arg;
+static void *memcpy_worker(void *p) {
+  memcpy_arg *m = (memcpy_arg *)p;
+  for (int r = 0; r < m->reps; ++r) memcpy(m->b, m->a, m->bytes);
+  return NULL;
+}
+#include <time.h>
+double oracle_memcpy_rate(uint64_t bytes, int threads, int reps) {
+  if (threads < 1) threads = 1;
+  memcpy_arg *args = (memcpy_arg *)calloc((size_t)threads, sizeof(memcpy_arg));
+  pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+  double gbs = -1;
+  int ok = args && th;
+  for (int t = 0; ok && t < threads; ++t) {
+    args[t].a = (uint8_t *)malloc(bytes);
+    args[t].b = (uint8_t *)malloc(bytes);
+    if (!args[t].a || !args[t].b) { ok = 0; break; }
+    memset(args[t].a, 1, bytes);
+    memset(args[t].b, 0, bytes);
+    args[t].bytes = bytes;
+    args[t].reps = reps;
+  }
+  if (ok) {
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, memcpy_worker, &args[t]);
+    for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    const double s = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
+    gbs = 2.0 * (double)bytes * reps * threads / s / 1e9;
+  }
+  for (int t = 0; args && t < threads; ++t) { free(args[t].a); free(args[t].b); }
+  free(args); free(th);
+  return gbs;
 }

@@ -16,6 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 LIB = PKG / "libsagedp.so"
+WORKER = PKG / "sage_instance_worker"      # one FixedGSL instance process (SAGE_INSTANCE_PROCESS)
 ORACLE_SRC = ROOT / "oracle" / "sage_oracle.c"
 ORACLE_LIB = ROOT / "oracle" / "liboracle.so"
 
@@ -61,6 +62,9 @@ def build_lib(force: bool = False) -> Path:
         list(ex.map(compile_one, jobs))
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+    wsrc = CSRC / "instance_worker.cpp"
+    if force or _stale(WORKER, [wsrc, LIB]):
+        _run(["g++", "-O2", "-o", str(WORKER), str(wsrc), f"-L{PKG}", "-lsagedp", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

@@ -58,10 +58,13 @@ class BodyDesc(C.Structure):
                 ("ro_bytes", u64), ("input_bytes", u64), ("out_bytes", u64), ("args", i64 * 8)]
 
 
+INSTANCE_THREAD, INSTANCE_PROCESS, INSTANCE_POOLED = 0, 1, 2
+
+
 class FixedGSLDesc(C.Structure):
-    _fields_ = [("gpu", C.c_int32), ("pad_", C.c_int32), ("layout", H), ("ro_src", C.c_void_p),
+    _fields_ = [("gpu", C.c_int32), ("mode", C.c_int32), ("layout", H), ("ro_src", C.c_void_p),
                 ("ro_src_bytes", u64), ("input", C.c_void_p), ("input_bytes", u64), ("alloc_bytes", u64),
-                ("body", BodyDesc), ("result", C.c_void_p), ("result_bytes", u64)]
+                ("body", BodyDesc), ("result", C.c_void_p), ("result_bytes", u64), ("ctx", H)]
 
 
 INV_CTX, INV_RO, INV_INPUT, INV_SYNC, INV_RET_HOST = 0x1, 0x2, 0x4, 0x8, 0x10
@@ -176,6 +179,9 @@ _SIGS = {
     "sage_fixedgsl_submit": (C.c_int, [C.POINTER(FixedGSLDesc), C.POINTER(H), C.POINTER(H)]),
     "sage_fixedgsl_info_get": (C.c_int, [H, C.POINTER(FixedGSLInfo)]),
     "sage_fixedgsl_release": (C.c_int, [H]),
+    "sage_instance_ctx_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(H)]),
+    "sage_instance_ctx_destroy": (C.c_int, [H]),
+    "sage_instance_child": (C.c_int, [C.c_int]),
     "sage_stats_enable": (C.c_int, [C.c_int]),
     "sage_stats_reset": (C.c_int, []),
     "sage_stats_get": (C.c_int, [C.c_int, C.c_int, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(u64)]),

@@ -376,19 +376,27 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
   return SAGE_OK;
 }
 
-// the lazily-loaded module must exist in every context that launches bodies
-int touch_all_kernels() {
+// load (lazily loaded modules) only the kernels of one body into the current
+// context: what a function instance's own context pays for its code, no more
+int touch_body_kernels(int body) {
   cudaFuncAttributes a;
-  SAGE_CUDA(cudaFuncGetAttributes(&a, touch_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, stencil_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, spmv_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, stencil4_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, spmv4_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, spin_kernel));
-  SAGE_CUDA(cudaFuncGetAttributes(&a, gather_kernel));
-  SAGE_TRY(touch_tc_kernels());
-  SAGE_TRY(touch_csb_kernel());
+  switch (body) {
+    case SAGE_BODY_TOUCH: SAGE_CUDA(cudaFuncGetAttributes(&a, touch_kernel)); break;
+    case SAGE_BODY_SGEMM: SAGE_TRY(touch_tc_kernels()); break;
+    case SAGE_BODY_SGEMM_F32: SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_kernel)); break;
+    case SAGE_BODY_STENCIL:
+      SAGE_CUDA(cudaFuncGetAttributes(&a, stencil4_kernel));
+      SAGE_CUDA(cudaFuncGetAttributes(&a, stencil_kernel));
+      break;
+    case SAGE_BODY_SPMV:
+      SAGE_CUDA(cudaFuncGetAttributes(&a, spmv4_kernel));
+      SAGE_CUDA(cudaFuncGetAttributes(&a, spmv_kernel));
+      break;
+    case SAGE_BODY_SPIN: SAGE_CUDA(cudaFuncGetAttributes(&a, spin_kernel)); break;
+    case SAGE_BODY_SPMV_CSB: SAGE_TRY(touch_csb_kernel()); break;
+    case SAGE_BODY_GATHER: SAGE_CUDA(cudaFuncGetAttributes(&a, gather_kernel)); break;
+    default: return fail(SAGE_EINVAL, "touch_body_kernels: unknown body");
+  }
   return SAGE_OK;
 }
 

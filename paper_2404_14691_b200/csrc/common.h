@@ -203,7 +203,9 @@ int launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b);   // + live k
 // gets an alias of it)
 int return_enqueue(Gpu *G, cudaStream_t s, sage_handle prev, uint64_t src, void *dst, uint64_t bytes,
                    bool host_dst, sage_handle *begin_ev, sage_handle *end_ev, sage_handle pre_end = 0);
-int touch_all_kernels();
+int touch_body_kernels(int body);   // module-load one body's kernels into the current context
+int64_t host_epoch_us();            // CLOCK_MONOTONIC µs of the library epoch (sage_init)
+int64_t mono_us();                  // CLOCK_MONOTONIC µs (absolute)
 // tcgen05 GEMM (gemm_tc.cu)
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
 int touch_tc_kernels();

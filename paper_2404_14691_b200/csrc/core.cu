@@ -40,6 +40,8 @@ static int64_t mono_ns() {
   return (int64_t)ts.tv_sec * 1000000000ll + ts.tv_nsec;
 }
 int64_t host_now_us() { return (mono_ns() - g_epoch_ns) / 1000; }
+int64_t host_epoch_us() { return g_epoch_ns / 1000; }
+int64_t mono_us() { return mono_ns() / 1000; }
 
 // ------------------------------------------------------- driver entry pts ---
 template <class F>

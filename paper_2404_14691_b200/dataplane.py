@@ -272,6 +272,7 @@ class DataPlane:
         self.pinned = _PinnedPool()
         self.data: dict[str, FunctionData] = {}
         self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
+        self._contexts: set = set()     # DGSF pre-created CUDA contexts
         self._free_slots: dict[int, list] = {}
         self._fast = _FastCompletions(self)
         self._scratch: dict[tuple[int, int], list] = {}
@@ -398,15 +399,18 @@ class DataPlane:
             self.pinned.put(buf)
             r.cpu_ro_cache.segment = None
 
-    def precreate_context(self, gpu: int, alloc) -> Optional[D.Event]:
-        """DGSF: bind a pre-created context segment once, at registration."""
-        slot = D.Slot(gpu)
-        b, e = slot.bind_ctx(alloc.dptr, alloc.requested)
-        e.sync()
-        b.release()
-        e.release()
-        slot.release()
-        return None
+    def precreate_context(self, gpu: int, alloc, spec: Optional[FunctionSpec] = None) -> int:
+        """DGSF registration: a real CUDA context (cuCtxCreate) with the
+        function's body kernels loaded; its invocations run in it."""
+        body = self.data_for(spec).body if spec is not None else "touch"
+        h = D.instance_ctx_create(gpu, _BODY.get(body, _lib.BODY_TOUCH))
+        self._contexts.add(h)
+        return h
+
+    def release_context(self, h: int) -> None:
+        if h in self._contexts:
+            self._contexts.discard(h)
+            D.instance_ctx_destroy(h)
 
     # -------------------------------------------------------------- start -----
     def start(self, inv, plan: StagePlan, wait_tokens=(), hooks=None, fresh_context: bool = False) -> None:
@@ -415,8 +419,11 @@ class DataPlane:
         run = _Run(inv=inv, plan=plan, gpu=inv.gpu, hooks=dict(hooks or {}), fd=fd)
         run.t_enqueue = self.sim.engine.tick()
         inv.run = run
-        if fresh_context:
-            self._start_fixedgsl(run, fd)
+        slot = getattr(inv, "ctx_slot", None)
+        if fresh_context or slot is not None:
+            # FixedGSL instance, or DGSF: in the slot's pre-created context (a
+            # slot whose context expired re-creates one inside its own plan)
+            self._start_fixedgsl(run, fd, ctx=slot.handle if slot is not None and slot.handle else 0)
             return
         try:
             if fd.body != "resnet50" and self._fast_ok(plan):
@@ -836,16 +843,24 @@ class DataPlane:
                            out=out_dst, out_bytes=max(16, fd.out_bytes), args=fd.args)
 
     # ----------------------------------------------------------- FixedGSL -----
-    def _start_fixedgsl(self, run: _Run, fd: FunctionData) -> None:
+    def _start_fixedgsl(self, run: _Run, fd: FunctionData, ctx: int = 0) -> None:
+        """An instance job: FixedGSL (a fresh context, on a library thread or
+        -- ClusterSpec.instance_mode "process" -- in its own OS process), or
+        DGSF in a pre-created context `ctx` (data reserved per invocation)."""
         inv = run.inv
         spec = inv.spec
         run.result = self.pinned.get(max(16, fd.out_bytes))
         run.out_bytes = fd.out_bytes
-        alloc = inv.allocations[0].effective if inv.allocations else 0
+        if ctx:
+            mode, reserve = _lib.INSTANCE_POOLED, sum(a.effective for a in inv.allocations)
+        else:
+            mode = _lib.INSTANCE_PROCESS if self.sim.cluster.instance_mode == "process" else _lib.INSTANCE_THREAD
+            alloc = inv.allocations[0].effective if inv.allocations else 0
+            reserve = max(0, alloc - spec.context_bytes)
         body = D.body_desc(_BODY[fd.body], out_bytes=max(16, fd.out_bytes), args=fd.args)
         run.job = D.fixedgsl_submit(run.gpu, fd.layout if fd.layout.n else None,
                                     fd.db if fd.layout.packed_bytes else None, self._payload(inv, fd),
-                                    max(0, alloc - spec.context_bytes), body, run.result, fd.out_bytes)
+                                    reserve, body, run.result, fd.out_bytes, mode=mode, ctx=ctx)
         run.end = run.job.end
         run.ro_source = "pcie"
         self.sim.engine.watch(run.end, self._on_done, run)
@@ -986,4 +1001,6 @@ class DataPlane:
             for s in lst:
                 s.release()
         self._free_slots.clear()
+        for h in list(self._contexts):
+            self.release_context(h)
         self.pinned.close()

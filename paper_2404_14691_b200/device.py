@@ -339,9 +339,14 @@ class FixedGSLJob:
 
 
 def fixedgsl_submit(gpu: int, layout, ro_src, inp, alloc_bytes: int, body: "_lib.BodyDesc",
-                    result: Optional[PinnedBuffer], result_bytes: int) -> FixedGSLJob:
+                    result: Optional[PinnedBuffer], result_bytes: int, mode: int = 0, ctx: int = 0) -> FixedGSLJob:
+    """One instance-per-invocation job: mode INSTANCE_THREAD (fresh context
+    on a library thread), INSTANCE_PROCESS (fresh OS process) or
+    INSTANCE_POOLED (DGSF: in the pre-created context `ctx`)."""
     d = _lib.FixedGSLDesc()
     d.gpu = gpu
+    d.mode = mode
+    d.ctx = ctx
     d.layout = layout.handle() if layout is not None else 0
     keep = []
     if ro_src is not None:
@@ -359,3 +364,14 @@ def fixedgsl_submit(gpu: int, layout, ro_src, inp, alloc_bytes: int, body: "_lib
     jh, eh = H(), H()
     check(lib().sage_fixedgsl_submit(C.byref(d), C.byref(jh), C.byref(eh)), "sage_fixedgsl_submit")
     return FixedGSLJob(jh.value, Event(eh.value), keep)
+
+
+def instance_ctx_create(gpu: int, body: int) -> int:
+    """A real pre-created CUDA context with `body`'s kernels loaded (DGSF)."""
+    h = H()
+    check(lib().sage_instance_ctx_create(gpu, body, C.byref(h)), "sage_instance_ctx_create")
+    return h.value
+
+
+def instance_ctx_destroy(h: int) -> None:
+    check(lib().sage_instance_ctx_destroy(h), "sage_instance_ctx_destroy")

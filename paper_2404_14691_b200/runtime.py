@@ -52,10 +52,15 @@ class ClusterSpec:
     chunk_mb: float = 8.0
     staging_mb: float = 64.0
     host_threads: Optional[int] = None
+    # FixedGSL instances: "thread" (a fresh context on a library thread) or
+    # "process" (a fresh OS process per instance, the container-per-function shape)
+    instance_mode: str = "thread"
 
     def __post_init__(self):
         if self.gpus < 1:
             raise ValueError("cluster needs at least one GPU")
+        if self.instance_mode not in ("thread", "process"):
+            raise ValueError(f"instance_mode must be 'thread' or 'process', not {self.instance_mode!r}")
         if self.gpu_mem_mb <= 0 or self.pcie_bw_mbps <= 0 or self.host_bw_mbps <= 0:
             raise ValueError("cluster capacities and bandwidths must be positive")
 
