@@ -368,6 +368,24 @@ int sage_mark(int gpu, sage_handle *ev);
 /* elapsed µs between two completed events of the same GPU (device clock) */
 int sage_event_elapsed(sage_handle a, sage_handle b, double *us);
 
+/* ---- ResNet-50 convolution (tcgen05 implicit GEMM, BF16) -------------------
+ * One convolution of NHWC bf16 activations with OHWI bf16 filters read in
+ * place, fp32 accumulation in TMEM, epilogue y = acc * scale + bias
+ * (+ residual) (ReLU), bf16 NHWC out; scale / bias fold batch-norm from its
+ * bf16 parameters (scale = gamma * rsqrt(var + eps), bias = beta - mean *
+ * scale; gamma == 0 pointer: identity).  SAGE_CONV_C4: the input is NHWC with
+ * 4 channels (conv1's 3 padded) and the filter is [Cout][ceil(R*S/16)*64].
+ * Replaces the COMPUTE delay of the resnet50 record (functions.py:154, :276). */
+#define SAGE_CONV_NHWC  0
+#define SAGE_CONV_C4    1
+typedef struct {
+  uint64_t x, w, out, residual;             /* device pointers (residual 0 = none) */
+  uint64_t bn_gamma, bn_beta, bn_mean, bn_var;
+  float bn_eps;
+  int32_t n, h, w_, cin, cout, r, s, stride, pad, relu, mode, pad_;
+} sage_conv_desc;
+int sage_conv(sage_handle slot, const sage_conv_desc *d);
+
 /* ---- sharing manager: the native resident table ----------------------------
  * Replaces SharingManager's resident dict and its state machine
  * (sharing.py:103-335): warmth classification (:115-125), delta sizes

@@ -118,6 +118,17 @@ class ResidentInfo(C.Structure):
                 ("has_checksum", C.c_uint32), ("pad_", C.c_uint32), ("checksum", u64)]
 
 
+CONV_NHWC, CONV_C4 = 0, 1
+
+
+class ConvDesc(C.Structure):
+    _fields_ = [("x", u64), ("w", u64), ("out", u64), ("residual", u64), ("bn_gamma", u64), ("bn_beta", u64),
+                ("bn_mean", u64), ("bn_var", u64), ("bn_eps", C.c_float), ("n", C.c_int32), ("h", C.c_int32),
+                ("w_", C.c_int32), ("cin", C.c_int32), ("cout", C.c_int32), ("r", C.c_int32), ("s", C.c_int32),
+                ("stride", C.c_int32), ("pad", C.c_int32), ("relu", C.c_int32), ("mode", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
 _SIGS = {
     "sage_init": (C.c_int, [C.c_int, u64, u64, u64, C.c_uint32]),
     "sage_shutdown": (C.c_int, []),
@@ -188,6 +199,7 @@ _SIGS = {
     "sage_device_sync": (C.c_int, [C.c_int]),
     "sage_mark": (C.c_int, [C.c_int, C.POINTER(H)]),
     "sage_event_elapsed": (C.c_int, [H, H, C.POINTER(C.c_double)]),
+    "sage_conv": (C.c_int, [H, C.POINTER(ConvDesc)]),
     "sage_share_create": (C.c_int, [C.c_int, C.c_uint32, i64, C.POINTER(i64), C.POINTER(H)]),
     "sage_share_destroy": (C.c_int, [H]),
     "sage_share_preview": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, C.POINTER(ShareGrant)]),

@@ -209,6 +209,9 @@ int64_t mono_us();                  // CLOCK_MONOTONIC µs (absolute)
 // tcgen05 GEMM (gemm_tc.cu)
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
 int touch_tc_kernels();
+// tcgen05 implicit-GEMM convolution (conv_tc.cu)
+int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms);
+int touch_conv_kernels();
 // column-sliced block spmv (spmv_csb.cu)
 int spmv_csb(const sage_body_desc *b, cudaStream_t s, int sm_count);
 int touch_csb_kernel();

@@ -1,0 +1,385 @@
+// conv_tc.cu — ResNet-50 convolutions as tcgen05 implicit GEMMs (BF16 in,
+// FP32 accumulate in TMEM), reading the landed OHWI filters in place, with
+// batch-norm folded into the epilogue together with the residual add and ReLU.
+//
+// GEMM view of one convolution (NHWC activations, OHWI filters):
+//   M = N*P*Q output pixels, N = Cout, K = R*S*Cin (K-major on both sides:
+//   an OHWI filter row IS a K row, an NHWC pixel's channels are contiguous).
+// One CTA computes a 128-pixel x BN-channel tile (6 warps):
+//   warp 0     TMA producer of the filter tile: 64 bf16 of K (one 128-B
+//              SWIZZLE_128B row) x BN output channels per K-block
+//   warp 1     TMEM allocator + single-thread MMA issuer: 4 x
+//              tcgen05.mma.kind::f16 (K = 16 each) per K-block
+//   warps 2-5  im2col gatherers: thread t owns output pixel m0 + t and fills
+//              its 128-B row of the A tile per K-block with cp.async (16 B
+//              per 8 channels; zero-fill for padding and rows past M), then
+//              -- when its copies have landed -- a proxy fence and an arrive
+//              on the stage's barrier; after the K loop the same warps are
+//              the epilogue: tcgen05.ld 32 channels at a time, y = acc * scale
+//              + bias (+ residual), ReLU, bf16, 64-B stores (NHWC)
+// K-block order: filter tap (r, s) outer, 64-channel slice inner, so every
+// K-block is one shifted NHWC window: (kb / (Cin/64)) -> (r, s).
+// conv1 (Cin = 3) runs in the C4 mode: the input padded to 4 channels (8 B
+// per pixel) and the filter to [Cout][256] (16 taps x 4 channels per K-block,
+// 49 taps, zero tail), both prepared by small kernels (resnet.cu).
+// Batch-norm: scale = gamma * rsqrt(var + eps), bias = beta - mean * scale,
+// computed per CTA from the landed bf16 parameters (no folded copy).
+#include "common.h"
+
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+namespace sage {
+
+constexpr int CV_BM = 128;       // output pixels per CTA (UMMA M)
+constexpr int CV_BK = 64;        // bf16 per K-block = one 128-B row
+constexpr int CV_THREADS = 192;
+constexpr int CV_LAG = 2;        // cp.async groups a gatherer keeps in flight
+
+template <int BN>
+struct CvSmem {
+  static constexpr int A_BYTES = CV_BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN >= 256 ? 4 : 6);
+  static constexpr int TOTAL = STAGES * STAGE + 1024 + 256 + 2 * 256 * 4;
+};
+
+__device__ __forceinline__ uint32_t cv_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cv_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra W_%=;\n\t}" ::"r"(cv_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t cv_desc(uint32_t saddr) {   // K-major SWIZZLE_128B, SBO 1024
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+template <int BN>
+__device__ __forceinline__ uint32_t bf16_idesc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(CV_BM >> 4) << 24);
+}
+
+struct ConvArgs {
+  const __nv_bfloat16 *x;        // NHWC (C4 mode: NHWC4)
+  const __nv_bfloat16 *res;      // NHWC [M, Cout] or null
+  __nv_bfloat16 *out;            // NHWC [M, Cout]
+  const __nv_bfloat16 *gamma, *beta, *mean, *var;   // [Cout] (null: identity)
+  float eps;
+  int N, H, W, C, P, Q, R, S, stride, pad, Cout, M, KB, relu;
+};
+
+template <int BN, int C4>
+__global__ void __launch_bounds__(CV_THREADS, 1)
+    conv_bf16_kernel(const __grid_constant__ CUtensorMap mapW, const ConvArgs a) {
+  using Sm = CvSmem<BN>;
+  constexpr int ST = Sm::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *sA = smem;                    // ST x A_BYTES
+  uint8_t *sB = smem + ST * Sm::A_BYTES; // ST x B_BYTES
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * Sm::STAGE);
+  uint64_t *empty = full + ST;
+  uint64_t *tmem_full = empty + ST;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+  float *s_scale = reinterpret_cast<float *>(smem + ST * Sm::STAGE + 256);
+  float *s_bias = s_scale + 256;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * CV_BM, n0 = blockIdx.y * BN;
+
+  if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapW)) : "memory");
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < ST; ++s) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(&full[s])), "r"(129));  // 128 gatherers + TMA
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(&empty[s])), "r"(1));
+      }
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(tmem_full)), "r"(1));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cv_smem(tmem_slot)),
+                 "r"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp >= 2) {
+    // folded batch-norm of this CTA's channels
+    for (int c = threadIdx.x - 64; c < BN; c += 128) {
+      float sc = 1.f, bi = 0.f;
+      if (a.gamma) {
+        const int ch = n0 + c;
+        sc = __bfloat162float(a.gamma[ch]) * rsqrtf(__bfloat162float(a.var[ch]) + a.eps);
+        bi = __bfloat162float(a.beta[ch]) - __bfloat162float(a.mean[ch]) * sc;
+      }
+      s_scale[c] = sc;
+      s_bias[c] = bi;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int KB = a.KB;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- filter tiles by TMA ----
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % ST, round = kb / ST;
+        cv_wait(&empty[s], (round & 1) ^ 1);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cv_smem(&full[s])),
+                     "r"(Sm::B_BYTES)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                cv_smem(sB + s * Sm::B_BYTES)),
+            "l"(reinterpret_cast<uint64_t>(&mapW)), "r"(cv_smem(&full[s])), "r"(kb * CV_BK), "r"(n0)
+            : "memory");
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer ----
+      const uint32_t idesc = bf16_idesc<BN>();
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % ST, round = kb / ST;
+        cv_wait(&full[s], round & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = cv_desc(cv_smem(sA + s * Sm::A_BYTES)), db = cv_desc(cv_smem(sB + s * Sm::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < CV_BK / 16; ++k) {   // K = 16 bf16 = 32 B per MMA: +2 in 16-B units
+          const uint32_t acc = (kb | k) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         cv_smem(&empty[s]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       cv_smem(tmem_full))
+                   : "memory");
+    }
+  } else {
+    // ---- im2col gather: this thread's output pixel ----
+    const int row = threadIdx.x - 64;
+    const int m = m0 + row;
+    const bool live = m < a.M;
+    int n = 0, p = 0, q = 0;
+    if (live) {
+      q = m % a.Q;
+      const int t = m / a.Q;
+      p = t % a.P;
+      n = t / a.P;
+    }
+    const int ih0 = p * a.stride - a.pad, iw0 = q * a.stride - a.pad;
+    const int cslices = C4 ? 1 : a.C / CV_BK;
+    const uint32_t rbase = (uint32_t)row * 128u, rsw = (uint32_t)(row & 7);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % ST, round = kb / ST;
+      cv_wait(&empty[s], (round & 1) ^ 1);
+      const uint32_t dst = cv_smem(sA + s * Sm::A_BYTES) + rbase;
+      if constexpr (!C4) {
+        const int tap = kb / cslices, c0 = (kb - tap * cslices) * CV_BK;
+        const int r = tap / a.S, sx = tap - r * a.S;
+        const int ih = ih0 + r, iw = iw0 + sx;
+        const bool ok = live && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+        const __nv_bfloat16 *src = ok ? a.x + ((size_t)(n * a.H + ih) * a.W + iw) * a.C + c0 : a.x;
+        const uint32_t bytes = ok ? 16u : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + ((j ^ rsw) << 4)),
+                       "l"(src + 8 * j), "r"(bytes)
+                       : "memory");
+      } else {
+        // 16 taps x 4 channels (8 B) per K-block over the NHWC4 input
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int tap = kb * 16 + j;
+          const int r = tap / a.S, sx = tap - r * a.S;
+          const int ih = ih0 + r, iw = iw0 + sx;
+          const bool ok = live && tap < a.R * a.S && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+          const __nv_bfloat16 *src = ok ? a.x + ((size_t)(n * a.H + ih) * a.W + iw) * 4 : a.x;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + (((j >> 1) ^ rsw) << 4) +
+                                                                            ((j & 1) << 3)),
+                       "l"(src), "r"(ok ? 8u : 0u)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (kb >= CV_LAG) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(CV_LAG) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cv_smem(&full[(kb - CV_LAG) % ST])) : "memory");
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int kb = KB > CV_LAG ? KB - CV_LAG : 0; kb < KB; ++kb)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cv_smem(&full[kb % ST])) : "memory");
+
+    // ---- epilogue: TMEM lane quadrant (warp % 4) = 32 output pixels ----
+    cv_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quad = warp & 3;
+    const int orow = m0 + quad * 32 + lane;
+    const bool olive = orow < a.M;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (!olive) continue;
+      const size_t base = (size_t)orow * a.Cout + n0 + c;
+      float y[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]) * s_scale[c + j] + s_bias[c + j];
+      if (a.res) {
+        const uint4 *rp = reinterpret_cast<const uint4 *>(a.res + base);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w = rp[u];
+          const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&w);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            y[8 * u + 2 * e] += f.x;
+            y[8 * u + 2 * e + 1] += f.y;
+          }
+        }
+      }
+      if (a.relu) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = fmaxf(y[j], 0.f);
+      }
+      uint4 *op = reinterpret_cast<uint4 *>(a.out + base);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint4 w;
+        __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(y[8 * u + 2 * e], y[8 * u + 2 * e + 1]);
+        op[u] = w;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+  }
+}
+
+// --------------------------------------------------------------- host side ---
+static PFN_cuTensorMapEncodeTiled_v12000 g_cv_encode = nullptr;
+
+static int encode_filter(CUtensorMap *map, const void *w, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  if (!g_cv_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return fail(SAGE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    g_cv_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {k * 2};
+  cuuint32_t box[2] = {CV_BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_cv_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(w), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled (filter)");
+  return SAGE_OK;
+}
+
+template <int BN, int C4>
+static int launch_conv(const CUtensorMap &map, const ConvArgs &a, cudaStream_t s) {
+  SAGE_CUDA(cudaFuncSetAttribute(conv_bf16_kernel<BN, C4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 CvSmem<BN>::TOTAL));
+  dim3 grid((a.M + CV_BM - 1) / CV_BM, a.Cout / BN);
+  conv_bf16_kernel<BN, C4><<<grid, CV_THREADS, CvSmem<BN>::TOTAL, s>>>(map, a);
+  SAGE_CUDA(cudaGetLastError());
+  return SAGE_OK;
+}
+
+// output-channel tile: the widest that divides Cout and still gives the
+// grid about two waves of the 148 SMs
+static int pick_bn(int m_tiles, int cout, int sms) {
+  int bn = cout % 256 == 0 ? 256 : cout % 128 == 0 ? 128 : 64;
+  while (bn > 64 && (long long)m_tiles * (cout / bn) < 2ll * sms) bn /= 2;
+  return bn;
+}
+
+int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms) {
+  if (!d || !d->x || !d->w || !d->out) return fail(SAGE_EINVAL, "conv: null tensor");
+  const bool c4 = d->mode == SAGE_CONV_C4;
+  if (d->n <= 0 || d->h <= 0 || d->w_ <= 0 || d->cout % 64 || d->r <= 0 || d->s <= 0 || d->stride <= 0 ||
+      d->pad < 0 || (!c4 && d->cin % 64) || (c4 && d->cin != 4))
+    return fail(SAGE_EINVAL, "conv: Cout and Cin must be multiples of 64 (C4 mode: Cin == 4)");
+  if (((d->x | d->w | d->out | d->residual) & 15))
+    return fail(SAGE_EINVAL, "conv: tensors must be 16-byte aligned");
+  ConvArgs a{};
+  a.x = (const __nv_bfloat16 *)d->x;
+  a.res = (const __nv_bfloat16 *)d->residual;
+  a.out = (__nv_bfloat16 *)d->out;
+  a.gamma = (const __nv_bfloat16 *)d->bn_gamma;
+  a.beta = (const __nv_bfloat16 *)d->bn_beta;
+  a.mean = (const __nv_bfloat16 *)d->bn_mean;
+  a.var = (const __nv_bfloat16 *)d->bn_var;
+  if (a.gamma && (!a.beta || !a.mean || !a.var)) return fail(SAGE_EINVAL, "conv: partial batch-norm parameters");
+  a.eps = d->bn_eps;
+  a.N = d->n; a.H = d->h; a.W = d->w_; a.C = d->cin;
+  a.R = d->r; a.S = d->s; a.stride = d->stride; a.pad = d->pad; a.Cout = d->cout;
+  a.P = (d->h + 2 * d->pad - d->r) / d->stride + 1;
+  a.Q = (d->w_ + 2 * d->pad - d->s) / d->stride + 1;
+  a.M = a.N * a.P * a.Q;
+  a.relu = d->relu;
+  const uint64_t ktot = c4 ? (uint64_t)((d->r * d->s + 15) / 16) * CV_BK : (uint64_t)d->r * d->s * d->cin;
+  a.KB = (int)(ktot / CV_BK);
+  const int bn = pick_bn((a.M + CV_BM - 1) / CV_BM, a.Cout, sms);
+  CUtensorMap map;
+  SAGE_TRY(encode_filter(&map, (const void *)d->w, (uint64_t)d->cout, ktot, (uint32_t)bn));
+  if (c4) return bn == 64 ? launch_conv<64, 1>(map, a, s) : launch_conv<128, 1>(map, a, s);
+  if (bn == 256) return launch_conv<256, 0>(map, a, s);
+  if (bn == 128) return launch_conv<128, 0>(map, a, s);
+  return launch_conv<64, 0>(map, a, s);
+}
+
+int touch_conv_kernels() {
+  cudaFuncAttributes at;
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 0>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 0>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 1>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 1>));
+  return SAGE_OK;
+}
+
+}  // namespace sage
+
+using namespace sage;
+
+extern "C" int sage_conv(sage_handle slot, const sage_conv_desc *d) {
+  Gpu *G;
+  cudaStream_t s;
+  SAGE_TRY(slot_stream(slot, &G, &s));
+  cudaSetDevice(G->dev);
+  return conv_bf16(d, s, G->sm_count);
+}

@@ -288,7 +288,7 @@ static int run_in_process(Job *J, int64_t *t) {
   int status = H->status;
   if (!WIFEXITED(wst) && status == SAGE_ENOTREADY) status = fail(SAGE_ESTATE, "instance process died");
   else if (status != SAGE_OK) status = fail(status, std::string("instance process: ") + H->err);
-  for (int i = 2; i < 16; ++i) t[i] = H->t[i];
+  for (int i = 2 * ST_CPU_LOAD; i < 16; ++i) t[i] = H->t[i];
   t[2 * ST_CPU_CTX + 1] = H->t[2 * ST_CPU_CTX + 1];
   J->info.checksum = H->checksum;
   J->info.teardown_us = H->teardown_us;

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % TC_STAGES, round = kb / TC_STAGES;
         mbar_wait(&empty[s], (round & 1) ^ 1);
-        mbar_expect_tx(&full[s], S::STAGE);
+        mbar_expect_tx(&full[s], S::RAW);   // the TMA bytes (3xTF32 lo buffers are written by the converter)
         tma_load_2d(sA + s * S::A_BYTES, &mapA, &full[s], (kb0 + kb) * TC_BK, m0);
         if constexpr (MC)   // this CTA's half of B, into both CTAs (same smem offset)
           tma_load_2d_mc(sB + s * S::B_BYTES + crank * (S::B_BYTES / 2), &mapB, &full[s], (kb0 + kb) * TC_BK,
