@@ -224,6 +224,8 @@ int sage_fanout(int src_gpu, uint64_t src_dptr, int dst_gpu, uint64_t dst_dptr, 
 #define SAGE_BODY_SPMV_CSB 7  /* y = A.x, A = RO in the column-sliced block format of
                                  parboil.spmv(fmt="csb"); args = {rows, cols, offsets
                                  offset, entries offset, R, CW, Emax, S | nnz << 8}   */
+#define SAGE_BODY_RESNET50 8  /* the registered ResNet-50 program (args[0] = sage_net_create
+                                 handle); out = logits then the workspace              */
 #define SAGE_BODY_GATHER   6  /* diagnostic: args[0] random 4-B gathers from the input
                                  (a power-of-two float array), the ceiling spmv's x
                                  gathers run against; writes 16 B                   */
@@ -385,6 +387,29 @@ typedef struct {
   int32_t n, h, w_, cin, cout, r, s, stride, pad, relu, mode, pad_;
 } sage_conv_desc;
 int sage_conv(sage_handle slot, const sage_conv_desc *d);
+
+/* ---- ResNet-50 body: a registered program of native kernels --------------
+ * Ops address the landed RO segment by offset (filters OHWI bf16, batch-norm
+ * bf16, classifier) and buffers by id: SAGE_NET_BUF_INPUT (the request image,
+ * NHWC bf16), SAGE_NET_BUF_OUT (the fp32 logits), SAGE_NET_BUF_WS0 + i (the
+ * invocation's workspace, laid out after the logits in its writable segment).
+ * Launched as body SAGE_BODY_RESNET50 with args[0] = the network handle.   */
+#define SAGE_NET_PAD_INPUT  1   /* NHWC3 -> NHWC4 (the stem's C4 gather)       */
+#define SAGE_NET_CONV       2   /* sage_conv on (src, filter, BN, res) -> dst  */
+#define SAGE_NET_MAXPOOL    3   /* 3x3 stride 2 pad 1                           */
+#define SAGE_NET_POOL_FC    4   /* avg pool into buffer `res` + classifier -> dst (fp32) */
+#define SAGE_NET_BUF_INPUT  0
+#define SAGE_NET_BUF_OUT    1
+#define SAGE_NET_BUF_WS0    2
+typedef struct {
+  int32_t kind, src, dst, res;               /* buffer ids (res -1: none)        */
+  uint64_t w_off, g_off, b_off, m_off, v_off; /* RO offsets (g_off = ~0: no BN)   */
+  float eps;
+  int32_t n, h, w, cin, cout, r, s, stride, pad, relu, mode;
+} sage_net_op;
+int sage_net_create(const sage_net_op *ops, int n_ops, const uint64_t *buf_bytes, int n_bufs, sage_handle *net,
+                    uint64_t *workspace_bytes);
+int sage_net_destroy(sage_handle net);
 
 /* ---- sharing manager: the native resident table ----------------------------
  * Replaces SharingManager's resident dict and its state machine

@@ -119,6 +119,17 @@ class ResidentInfo(C.Structure):
 
 
 CONV_NHWC, CONV_C4 = 0, 1
+BODY_RESNET50 = 8
+NET_PAD_INPUT, NET_CONV, NET_MAXPOOL, NET_POOL_FC = 1, 2, 3, 4
+NET_BUF_INPUT, NET_BUF_OUT, NET_BUF_WS0 = 0, 1, 2
+
+
+class NetOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("src", C.c_int32), ("dst", C.c_int32), ("res", C.c_int32),
+                ("w_off", u64), ("g_off", u64), ("b_off", u64), ("m_off", u64), ("v_off", u64),
+                ("eps", C.c_float), ("n", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("cin", C.c_int32),
+                ("cout", C.c_int32), ("r", C.c_int32), ("s", C.c_int32), ("stride", C.c_int32),
+                ("pad", C.c_int32), ("relu", C.c_int32), ("mode", C.c_int32)]
 
 
 class ConvDesc(C.Structure):
@@ -200,6 +211,8 @@ _SIGS = {
     "sage_mark": (C.c_int, [C.c_int, C.POINTER(H)]),
     "sage_event_elapsed": (C.c_int, [H, H, C.POINTER(C.c_double)]),
     "sage_conv": (C.c_int, [H, C.POINTER(ConvDesc)]),
+    "sage_net_create": (C.c_int, [C.POINTER(NetOp), C.c_int, C.POINTER(u64), C.c_int, C.POINTER(H), C.POINTER(u64)]),
+    "sage_net_destroy": (C.c_int, [H]),
     "sage_share_create": (C.c_int, [C.c_int, C.c_uint32, i64, C.POINTER(i64), C.POINTER(H)]),
     "sage_share_destroy": (C.c_int, [H]),
     "sage_share_preview": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, C.POINTER(ShareGrant)]),

@@ -359,6 +359,8 @@ int launch_body(const sage_body_desc *b, cudaStream_t s, int sm_count) {
       break;
     case SAGE_BODY_SPMV_CSB:
       return spmv_csb(b, s, sm_count);
+    case SAGE_BODY_RESNET50:
+      return net_run(b, s, sm_count);
     case SAGE_BODY_GATHER: {
       const long long n = b->args[0];
       const uint64_t elems = b->input_bytes / 4;
@@ -395,6 +397,7 @@ int touch_body_kernels(int body) {
     case SAGE_BODY_SPIN: SAGE_CUDA(cudaFuncGetAttributes(&a, spin_kernel)); break;
     case SAGE_BODY_SPMV_CSB: SAGE_TRY(touch_csb_kernel()); break;
     case SAGE_BODY_GATHER: SAGE_CUDA(cudaFuncGetAttributes(&a, gather_kernel)); break;
+    case SAGE_BODY_RESNET50: SAGE_TRY(touch_net_kernels()); break;
     default: return fail(SAGE_EINVAL, "touch_body_kernels: unknown body");
   }
   return SAGE_OK;

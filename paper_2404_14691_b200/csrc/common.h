@@ -212,6 +212,9 @@ int touch_tc_kernels();
 // tcgen05 implicit-GEMM convolution (conv_tc.cu)
 int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms);
 int touch_conv_kernels();
+// the ResNet-50 program body (resnet.cu)
+int net_run(const sage_body_desc *b, cudaStream_t s, int sms);
+int touch_net_kernels();
 // column-sliced block spmv (spmv_csb.cu)
 int spmv_csb(const sage_body_desc *b, cudaStream_t s, int sm_count);
 int touch_csb_kernel();

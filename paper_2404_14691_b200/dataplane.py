@@ -40,7 +40,7 @@ from .resources import AllocClass, SimulationError
 
 _BODY = {"touch": _lib.BODY_TOUCH, "sgemm": _lib.BODY_SGEMM, "stencil": _lib.BODY_STENCIL,
          "spmv": _lib.BODY_SPMV, "spin": _lib.BODY_SPIN, "sgemm_f32": 5,
-         "spmv_csb": _lib.BODY_SPMV_CSB}
+         "spmv_csb": _lib.BODY_SPMV_CSB, "resnet50_native": _lib.BODY_RESNET50}
 
 
 def _a256(n: int) -> int:
@@ -82,6 +82,9 @@ class FunctionData:
     input_dev: Optional[D.Segment] = None
     # the DB record is pinned (registered host store): cold loads DMA from it
     db_pinned: bool = False
+    # per-invocation device workspace after the output (the native ResNet
+    # program's activations), inside the invocation's writable segment
+    scratch_bytes: int = 0
 
     @property
     def input_bytes(self) -> int:
@@ -173,6 +176,9 @@ def _body_template(fd: "FunctionData") -> "_lib.BodyDesc":
     """The function's COMPUTE descriptor without pointers, built once."""
     b = fd.__dict__.get("_body_tmpl")
     if b is None:
+        if fd.body == "resnet50_native":
+            from . import dnn
+            dnn.native_handle(fd)       # args[0] = the registered program
         b = D.body_desc(_BODY[fd.body], ro_bytes=fd.layout.seg_bytes, inp_bytes=(fd.input_bytes + 15) // 16 * 16,
                         out_bytes=max(16, fd.out_bytes), args=fd.args)
         fd.__dict__["_body_tmpl"] = b
@@ -627,7 +633,7 @@ class DataPlane:
         """(input dptr, out dptr) inside the private writable allocation, or an
         unaccounted scratch segment when writable is too small."""
         inv = run.inv
-        need = _a256(fd.input_bytes + 16) + _a256(fd.out_bytes)
+        need = _a256(fd.input_bytes + 16) + _a256(fd.out_bytes) + fd.scratch_bytes
         wr = inv.private.get(AllocClass.WRITABLE) if inv.private else None
         if wr is None:
             wr = next((a for a in inv.allocations if a.cls is AllocClass.WRITABLE), None)

@@ -44,15 +44,24 @@ def _bf16_bits(a: np.ndarray) -> np.ndarray:
     return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).view(torch.int16).numpy()
 
 
-def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real", dtype: str = "fp32"):
+def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real", dtype: str = "fp32",
+             engine: str | None = None):
     """(FunctionSpec, FunctionData) for ResNet-50 inference on a batch of
     224x224 images; the DB record packs the state dict back to back.
     dtype "fp32": 102.4 MB of weights, fp32 input; "bf16": the weights and
     the input in bfloat16 (51.2 MB, half the PCIe bytes), packed
     channels-last (filters OHWI, input NHWC: meta["layout"] == "nhwc"),
-    logits returned in fp32 (BASELINE.json: BF16 outputs within rtol 1e-2)."""
+    logits returned in fp32 (BASELINE.json: BF16 outputs within rtol 1e-2).
+    engine: "native" (BF16 default) runs the body as the registered program of
+    tcgen05 convolutions (csrc/resnet.cu, csrc/conv_tc.cu); "torch" (FP32
+    default) runs PyTorch / cuDNN over zero-copy views, with TF32 off."""
     if dtype not in ("fp32", "bf16"):
         raise ValueError(f"resnet50: dtype must be fp32 or bf16, not {dtype!r}")
+    engine = engine or ("native" if dtype == "bf16" else "torch")
+    if engine == "native":
+        if dtype != "bf16":
+            raise ValueError("resnet50: the native engine runs the BF16 record")
+        return resnet50_native(batch, seed, name)
     names, arrays = _state(seed)
     shapes = [a.shape for a in arrays]            # logical (NCHW / OIHW) shapes
     dtypes = [a.dtype.str for a in arrays]
@@ -81,6 +90,135 @@ def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real", dtype: 
     return spec, data
 
 
+_STAGES = ((64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2))   # (planes, blocks, stride) of layer1..4
+
+
+def resnet50_native(batch: int = 8, seed: int = 0, name: str = "resnet50_real"):
+    """The BF16 ResNet-50 function whose body is a native program (no
+    PyTorch at run time).  Record: every conv filter OHWI bf16 in place, the
+    stem's filter padded to 4 input channels and K = 256 ([64][7][7][4] + a
+    zero tail: the C4 gather of csrc/conv_tc.cu), batch-norm parameters and
+    the classifier in bf16.  Request: the images NHWC bf16.  Writable: the
+    image, the fp32 logits and the activation workspace of the program."""
+    names, arrays = _state(seed)
+    sd = dict(zip(names, arrays))
+    rec_names, rec = [], []
+    for n in names:
+        a = sd[n]
+        if a.dtype != np.float32:
+            continue                    # num_batches_tracked: not used at inference
+        if n == "conv1.weight":
+            w = np.zeros((64, 256), np.float32)
+            w[:, :196] = np.concatenate([a.transpose(0, 2, 3, 1), np.zeros((64, 7, 7, 1), np.float32)], 3).reshape(64, 196)
+            a = w
+        elif a.ndim == 4:
+            a = a.transpose(0, 2, 3, 1)   # OIHW -> OHWI
+        rec_names.append(n)
+        rec.append(_bf16_bits(a))
+    layout = SegmentLayout.packed([a.nbytes for a in rec], align=256, names=tuple(rec_names))
+    db = layout.pack(rec)
+    off = dict(zip(rec_names, layout.dst_off))
+    ops, bufs = _native_program(off, batch)
+    rng = np.random.Generator(np.random.PCG64(seed + 1))
+    x = _bf16_bits(rng.standard_normal((batch, 3, 224, 224), dtype=np.float32).transpose(0, 2, 3, 1))
+    out_bytes = batch * 1000 * 4
+    ws = sum(-(-b // 256) * 256 for b in bufs)
+    data = FunctionData(layout, db, body="resnet50_native", args=(0, batch), input=x.reshape(-1).view(np.uint8),
+                        out_bytes=out_bytes)
+    data.scratch_bytes = ws
+    data.meta = {"names": rec_names, "compute": "bf16", "layout": "nhwc", "program": (ops, bufs),
+                 "state_seed": seed}
+    spec = FunctionSpec(name=name, ro_mem_mb=_mb(layout.seg_bytes),
+                        writable_mem_mb=_mb(x.nbytes + 16 + out_bytes + ws + 4096), compute_ms=24.3,
+                        input_bytes_host_mb=_mb(x.nbytes), input_bytes_pcie_mb=_mb(x.nbytes),
+                        body="resnet50_native")
+    return spec, data
+
+
+def _native_program(off: dict, batch: int):
+    """The op list of one forward (sage_net_op fields as dicts) and the
+    workspace buffer sizes.  Buffers rotate so a bottleneck's input stays
+    live until its residual add."""
+    from . import _lib
+    N = batch
+    act = N * 112 * 112 * 64 * 2          # the largest activation (stem out = layer1 out)
+    bufs = [N * 224 * 224 * 4 * 2] + [act] * 5 + [N * 2048 * 4]
+    pad_in, feat = _lib.NET_BUF_WS0, _lib.NET_BUF_WS0 + 6
+    A = [_lib.NET_BUF_WS0 + 1 + i for i in range(5)]
+    ops = [dict(kind=_lib.NET_PAD_INPUT, src=_lib.NET_BUF_INPUT, dst=pad_in, n=N, h=224, w=224)]
+
+    def conv(src, dst, prefix, bn, cin, cout, k, stride, pad, h, relu, res=-1, mode=0):
+        g = bn + "."
+        ops.append(dict(kind=_lib.NET_CONV, src=src, dst=dst, res=res, w_off=off[prefix + ".weight"],
+                        g_off=off[g + "weight"], b_off=off[g + "bias"], m_off=off[g + "running_mean"],
+                        v_off=off[g + "running_var"], eps=1e-5, n=N, h=h, w=h, cin=cin, cout=cout, r=k, s=k,
+                        stride=stride, pad=pad, relu=int(relu), mode=mode))
+
+    conv(pad_in, A[0], "conv1", "bn1", 4, 64, 7, 2, 3, 224, True, mode=_lib.CONV_C4)
+    ops.append(dict(kind=_lib.NET_MAXPOOL, src=A[0], dst=A[1], n=N, h=112, w=112, cin=64))
+    cur, h, cin = A[1], 56, 64
+    for li, (planes, blocks, stride) in enumerate(_STAGES):
+        for bi in range(blocks):
+            s = stride if bi == 0 else 1
+            p = f"layer{li + 1}.{bi}."
+            t1, t2, o, ds = [b for b in A if b != cur][:4]
+            res = cur
+            if bi == 0:
+                conv(cur, ds, p + "downsample.0", p + "downsample.1", cin, 4 * planes, 1, s, 0, h, False)
+                res = ds
+            conv(cur, t1, p + "conv1", p + "bn1", cin, planes, 1, 1, 0, h, True)
+            conv(t1, t2, p + "conv2", p + "bn2", planes, planes, 3, s, 1, h, True)
+            h //= s
+            conv(t2, o, p + "conv3", p + "bn3", planes, 4 * planes, 1, 1, 0, h, True, res=res)
+            cur, cin = o, 4 * planes
+    ops.append(dict(kind=_lib.NET_POOL_FC, src=cur, dst=_lib.NET_BUF_OUT, res=feat, w_off=off["fc.weight"],
+                    b_off=off["fc.bias"], n=N, h=h, w=h, cin=cin, cout=1000))
+    return ops, bufs
+
+
+def native_handle(fd: FunctionData) -> int:
+    """The library handle of the function's program (created once)."""
+    h = fd.meta.get("net_handle")
+    if h:
+        return h
+    from . import _lib
+    ops, bufs = fd.meta["program"]
+    arr = (_lib.NetOp * len(ops))()
+    for i, op in enumerate(ops):
+        for k in ("g_off", "b_off", "m_off", "v_off", "w_off"):
+            op.setdefault(k, (1 << 64) - 1 if k == "g_off" else 0)
+        op.setdefault("res", -1)
+        for k, v in op.items():
+            setattr(arr[i], k, v)
+    out, ws = _lib.H(0), _lib.u64(0)
+    _lib.check(_lib.lib().sage_net_create(arr, len(ops), (_lib.u64 * len(bufs))(*bufs), len(bufs),
+                                          _lib.C.byref(out), _lib.C.byref(ws)), "sage_net_create")
+    if ws.value > fd.scratch_bytes:
+        raise RuntimeError(f"native resnet workspace {ws.value} B exceeds the reserved {fd.scratch_bytes} B")
+    fd.meta["net_handle"] = out.value
+    fd.args = (out.value, fd.args[1])
+    return out.value
+
+
+def reference_cpu(fd: FunctionData, x_bytes: np.ndarray):
+    """torch-CPU fp32 logits of the function's network on its (bf16) weights
+    and a (bf16 NHWC) request -- the parity reference of tests/ (not used on
+    the product path)."""
+    import torch
+    import torchvision
+    torch.manual_seed(fd.meta["state_seed"])
+    model = torchvision.models.resnet50(weights=None).eval()
+    with torch.no_grad():
+        for p in list(model.parameters()) + list(model.buffers()):
+            if p.dtype == torch.float32:
+                p.copy_(p.to(torch.bfloat16).float())
+    n = fd.args[1]
+    x = torch.from_numpy(np.ascontiguousarray(x_bytes).view(np.int16).copy()).view(torch.bfloat16).float()
+    x = x.view(n, 224, 224, 3).permute(0, 3, 1, 2).contiguous()
+    with torch.inference_mode():
+        return model(x).numpy()
+
+
 def _as_logical(t, shp, fd: FunctionData):
     """A flat parameter view shaped to its logical (PyTorch) shape; 4-D
     filters of a channels-last record become OIHW views with NHWC strides."""
@@ -103,7 +241,13 @@ def _torch_dtype(tag: str):
 
 def _compute_dtype(fd: FunctionData):
     import torch
-    return torch.bfloat16 if fd.meta.get("compute") == "bf16" else torch.float32
+    dt = torch.bfloat16 if fd.meta.get("compute") == "bf16" else torch.float32
+    if dt is torch.float32:
+        # the FP32 function computes in FP32: cuDNN / cuBLAS would otherwise
+        # run its convolutions in TF32 (10-bit mantissa) by default
+        torch.backends.cudnn.allow_tf32 = False
+        torch.backends.cuda.matmul.allow_tf32 = False
+    return dt
 
 
 class _CudaBuf:

@@ -206,6 +206,9 @@ class Simulation:
                 from . import dnn
                 for dev in sorted({g % max(1, _lib.device_count()) for g in range(self.gpu_count)}):
                     dnn.prewarm(fd, dev)
+            elif fd.body == "resnet50_native":
+                from . import dnn
+                dnn.native_handle(fd)
 
     # -- workload entry points ----------------------------------------------------------
     def submit(self, fn_name: str, arrival_us: Optional[int] = None, payload=None) -> Invocation:

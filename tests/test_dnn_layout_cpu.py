@@ -17,7 +17,7 @@ def _flat(fd, k):
 def test_bf16_record_is_channels_last_and_views_restore_logical_tensors():
     from paper_2404_14691_b200 import dnn
     _, fd32 = dnn.resnet50(batch=2, seed=0, dtype="fp32")
-    _, fd16 = dnn.resnet50(batch=2, seed=0, dtype="bf16")
+    _, fd16 = dnn.resnet50(batch=2, seed=0, dtype="bf16", engine="torch")
     assert fd32.meta["layout"] == "nchw" and fd16.meta["layout"] == "nhwc"
     assert fd16.layout.seg_bytes < fd32.layout.seg_bytes * 0.51
     names = fd32.meta["names"]
