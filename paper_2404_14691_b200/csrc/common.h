@@ -210,10 +210,17 @@ int64_t mono_us();                  // CLOCK_MONOTONIC µs (absolute)
 int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s);
 int touch_tc_kernels();
 // tcgen05 implicit-GEMM convolution (conv_tc.cu)
-int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms);
+struct ConvFrame {                  // graph mode: buffers read from a device frame
+  const uint64_t *frame;
+  int x_sel, res_sel, out_sel;      // frame slots (res_sel < 0: no residual)
+  uint64_t x_off, res_off, out_off;
+};
+int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame *f);
+int conv_optin_all();
 int touch_conv_kernels();
 // the ResNet-50 program body (resnet.cu)
 int net_run(const sage_body_desc *b, cudaStream_t s, int sms);
+void nets_release_graphs();   // sage_shutdown: captured programs die with the device state
 int touch_net_kernels();
 // column-sliced block spmv (spmv_csb.cu)
 int spmv_csb(const sage_body_desc *b, cudaStream_t s, int sm_count);

@@ -34,14 +34,15 @@ namespace sage {
 constexpr int CV_BM = 128;       // output pixels per CTA (UMMA M)
 constexpr int CV_BK = 64;        // bf16 per K-block = one 128-B row
 constexpr int CV_THREADS = 192;
-constexpr int CV_LAG = 2;        // cp.async groups a gatherer keeps in flight
 
 template <int BN>
 struct CvSmem {
   static constexpr int A_BYTES = CV_BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN >= 256 ? 4 : 6);
+  // shallow enough for two CTAs per SM at BN <= 128: a batch-8 layer is
+  // gather-latency bound, so resident CTAs (memory parallelism) beat depth
+  static constexpr int STAGES = (BN >= 128 ? 3 : 4);
   static constexpr int TOTAL = STAGES * STAGE + 1024 + 256 + 2 * 256 * 4;
 };
 
@@ -68,16 +69,22 @@ struct ConvArgs {
   const __nv_bfloat16 *x;        // NHWC (C4 mode: NHWC4)
   const __nv_bfloat16 *res;      // NHWC [M, Cout] or null
   __nv_bfloat16 *out;            // NHWC [M, Cout]
+  // graph mode (frame != null): x / res / out are frame[sel] + off, read on
+  // the device, so one captured graph serves every invocation's buffers
+  const uint64_t *frame;
+  int x_sel, res_sel, out_sel;
+  uint64_t x_off, res_off, out_off;
   const __nv_bfloat16 *gamma, *beta, *mean, *var;   // [Cout] (null: identity)
   float eps;
   int N, H, W, C, P, Q, R, S, stride, pad, Cout, M, KB, relu;
 };
 
 template <int BN, int C4>
-__global__ void __launch_bounds__(CV_THREADS, 1)
+__global__ void __launch_bounds__(CV_THREADS, 2)
     conv_bf16_kernel(const __grid_constant__ CUtensorMap mapW, const ConvArgs a) {
   using Sm = CvSmem<BN>;
   constexpr int ST = Sm::STAGES;
+  constexpr int CV_LAG = ST - 1;   // cp.async K-blocks a gatherer keeps in flight past the arrived ones
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *sA = smem;                    // ST x A_BYTES
@@ -91,6 +98,13 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * CV_BM, n0 = blockIdx.y * BN;
+  const __nv_bfloat16 *X = a.x, *RES = a.res;
+  __nv_bfloat16 *OUT = a.out;
+  if (a.frame) {
+    X = reinterpret_cast<const __nv_bfloat16 *>(a.frame[a.x_sel] + a.x_off);
+    RES = a.res_sel >= 0 ? reinterpret_cast<const __nv_bfloat16 *>(a.frame[a.res_sel] + a.res_off) : nullptr;
+    OUT = reinterpret_cast<__nv_bfloat16 *>(a.frame[a.out_sel] + a.out_off);
+  }
 
   if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapW)) : "memory");
   if (warp == 1) {
@@ -191,7 +205,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
         const int r = tap / a.S, sx = tap - r * a.S;
         const int ih = ih0 + r, iw = iw0 + sx;
         const bool ok = live && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-        const __nv_bfloat16 *src = ok ? a.x + ((size_t)(n * a.H + ih) * a.W + iw) * a.C + c0 : a.x;
+        const __nv_bfloat16 *src = ok ? X + ((size_t)(n * a.H + ih) * a.W + iw) * a.C + c0 : X;
         const uint32_t bytes = ok ? 16u : 0u;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -206,7 +220,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           const int r = tap / a.S, sx = tap - r * a.S;
           const int ih = ih0 + r, iw = iw0 + sx;
           const bool ok = live && tap < a.R * a.S && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-          const __nv_bfloat16 *src = ok ? a.x + ((size_t)(n * a.H + ih) * a.W + iw) * 4 : a.x;
+          const __nv_bfloat16 *src = ok ? X + ((size_t)(n * a.H + ih) * a.W + iw) * 4 : X;
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + (((j >> 1) ^ rsw) << 4) +
                                                                             ((j & 1) << 3)),
                        "l"(src), "r"(ok ? 8u : 0u)
@@ -249,8 +263,8 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       float y[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]) * s_scale[c + j] + s_bias[c + j];
-      if (a.res) {
-        const uint4 *rp = reinterpret_cast<const uint4 *>(a.res + base);
+      if (RES) {
+        const uint4 *rp = reinterpret_cast<const uint4 *>(RES + base);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 w = rp[u];
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = fmaxf(y[j], 0.f);
       }
-      uint4 *op = reinterpret_cast<uint4 *>(a.out + base);
+      uint4 *op = reinterpret_cast<uint4 *>(OUT + base);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         uint4 w;
@@ -309,10 +323,53 @@ static int encode_filter(CUtensorMap *map, const void *w, uint64_t rows, uint64_
   return SAGE_OK;
 }
 
+// filter tensor maps are a pure function of (address, shape, box): encoded
+// once and reused by every invocation that reads the same landed filter
+struct MapKey {
+  uint64_t w, rows, k;
+  uint32_t box;
+  bool operator==(const MapKey &o) const { return w == o.w && rows == o.rows && k == o.k && box == o.box; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey &k) const { return std::hash<uint64_t>()(k.w ^ (k.rows << 40) ^ (k.k << 20) ^ k.box); }
+};
+static std::mutex g_map_mu;
+static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+static int filter_map(CUtensorMap *out, uint64_t w, uint64_t rows, uint64_t k, uint32_t box) {
+  const MapKey key{w, rows, k, box};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return SAGE_OK;
+    }
+  }
+  SAGE_TRY(encode_filter(out, (const void *)w, rows, k, box));
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (g_maps.size() > 65536) g_maps.clear();   // bounded: segments come and go
+  g_maps.emplace(key, *out);
+  return SAGE_OK;
+}
+
+// the dynamic-smem opt-in is per kernel and context: set once per (kernel, context)
+static int smem_optin(const void *fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, CUcontext>> done;
+  CUcontext ctx = nullptr;
+  if (drv.CtxGetCurrent) drv.CtxGetCurrent(&ctx);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &p : done)
+    if (p.first == fn && p.second == ctx) return SAGE_OK;
+  SAGE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(fn, ctx);
+  return SAGE_OK;
+}
+
 template <int BN, int C4>
 static int launch_conv(const CUtensorMap &map, const ConvArgs &a, cudaStream_t s) {
-  SAGE_CUDA(cudaFuncSetAttribute(conv_bf16_kernel<BN, C4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 CvSmem<BN>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<BN, C4>, CvSmem<BN>::TOTAL));
   dim3 grid((a.M + CV_BM - 1) / CV_BM, a.Cout / BN);
   conv_bf16_kernel<BN, C4><<<grid, CV_THREADS, CvSmem<BN>::TOTAL, s>>>(map, a);
   SAGE_CUDA(cudaGetLastError());
@@ -327,8 +384,8 @@ static int pick_bn(int m_tiles, int cout, int sms) {
   return bn;
 }
 
-int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms) {
-  if (!d || !d->x || !d->w || !d->out) return fail(SAGE_EINVAL, "conv: null tensor");
+int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame *f) {
+  if (!d || (!f && (!d->x || !d->out)) || !d->w) return fail(SAGE_EINVAL, "conv: null tensor");
   const bool c4 = d->mode == SAGE_CONV_C4;
   if (d->n <= 0 || d->h <= 0 || d->w_ <= 0 || d->cout % 64 || d->r <= 0 || d->s <= 0 || d->stride <= 0 ||
       d->pad < 0 || (!c4 && d->cin % 64) || (c4 && d->cin != 4))
@@ -339,6 +396,12 @@ int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms) {
   a.x = (const __nv_bfloat16 *)d->x;
   a.res = (const __nv_bfloat16 *)d->residual;
   a.out = (__nv_bfloat16 *)d->out;
+  if (f) {
+    if ((f->x_off | f->res_off | f->out_off) & 15) return fail(SAGE_EINVAL, "conv: frame offsets must be 16-B aligned");
+    a.frame = f->frame;
+    a.x_sel = f->x_sel; a.res_sel = f->res_sel; a.out_sel = f->out_sel;
+    a.x_off = f->x_off; a.res_off = f->res_off; a.out_off = f->out_off;
+  }
   a.gamma = (const __nv_bfloat16 *)d->bn_gamma;
   a.beta = (const __nv_bfloat16 *)d->bn_beta;
   a.mean = (const __nv_bfloat16 *)d->bn_mean;
@@ -355,11 +418,20 @@ int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms) {
   a.KB = (int)(ktot / CV_BK);
   const int bn = pick_bn((a.M + CV_BM - 1) / CV_BM, a.Cout, sms);
   CUtensorMap map;
-  SAGE_TRY(encode_filter(&map, (const void *)d->w, (uint64_t)d->cout, ktot, (uint32_t)bn));
+  SAGE_TRY(filter_map(&map, d->w, (uint64_t)d->cout, ktot, (uint32_t)bn));
   if (c4) return bn == 64 ? launch_conv<64, 1>(map, a, s) : launch_conv<128, 1>(map, a, s);
   if (bn == 256) return launch_conv<256, 0>(map, a, s);
   if (bn == 128) return launch_conv<128, 0>(map, a, s);
   return launch_conv<64, 0>(map, a, s);
+}
+
+int conv_optin_all() {
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 0>, CvSmem<64>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 0>, CvSmem<128>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0>, CvSmem<256>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 1>, CvSmem<64>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 1>, CvSmem<128>::TOTAL));
+  return SAGE_OK;
 }
 
 int touch_conv_kernels() {
@@ -381,5 +453,5 @@ extern "C" int sage_conv(sage_handle slot, const sage_conv_desc *d) {
   cudaStream_t s;
   SAGE_TRY(slot_stream(slot, &G, &s));
   cudaSetDevice(G->dev);
-  return conv_bf16(d, s, G->sm_count);
+  return conv_bf16(d, s, G->sm_count, nullptr);
 }

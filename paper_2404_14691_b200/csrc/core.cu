@@ -511,6 +511,7 @@ int sage_shutdown(void) {
   invoke_shutdown();
   pool_threads_stop();
   layouts_destroy_all();
+  nets_release_graphs();
   {
     std::lock_guard<std::mutex> lk(g_host_mu);
     for (auto &kv : g_host) cudaFreeHost(kv.second.p);

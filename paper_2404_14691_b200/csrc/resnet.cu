@@ -6,20 +6,42 @@
 // segment (filters, batch-norm parameters and the classifier, addressed by
 // their offsets in the segment) and the invocation's writable segment (the
 // request image, the logits and the activation workspace).  One invocation's
-// COMPUTE launches the program on its stream:
+// COMPUTE runs the program on its stream:
 //   PAD_INPUT   NHWC 3-channel image -> 4-channel (the stem's C4 gather)
 //   CONV        tcgen05 implicit GEMM (conv_tc.cu), BN / residual / ReLU fused
 //   MAXPOOL     3x3 stride 2 pad 1 (the stem)
 //   POOL_FC     global average pool + the 1000-way classifier, fp32 logits
 // No PyTorch, no cuDNN: the BF16 ResNet-50 record runs on these kernels only.
+//
+// Launch: 57 kernels per forward would cost ~0.45 ms of host time on the
+// issuing thread, so the program is captured once per (landed segment,
+// context) as CUDA graphs whose kernels read their activation buffers from a
+// device-side FRAME {input, logits, workspace}.  An invocation then costs two
+// launches: a one-thread kernel writing its frame, and the graph.  Launches
+// of one executable graph serialise, so up to kInstances graphs (each with
+// its own frame) serve concurrent invocations; an instance is reused after
+// its previous run's completion event (device-side wait).
+// SAGE_NET_GRAPHS=0 launches the ops one by one with direct pointers.
 #include "common.h"
 
 #include <cuda_bf16.h>
 
+#include <map>
+
 namespace sage {
 
+struct BufRef {        // a buffer: frame[sel] + off on the device, or `direct`
+  int sel;
+  uint64_t off, direct;
+};
+__device__ __forceinline__ uint64_t resolve(const uint64_t *frame, const BufRef &r) {
+  return frame ? frame[r.sel] + r.off : r.direct;
+}
+
 // NHWC bf16 [P, 3] -> [P, 4] (zero fourth channel)
-__global__ void pad_c4_kernel(const __nv_bfloat16 *__restrict__ in, __nv_bfloat16 *__restrict__ out, long long pix) {
+__global__ void pad_c4_kernel(const uint64_t *frame, BufRef src, BufRef dst, long long pix) {
+  const __nv_bfloat16 *in = reinterpret_cast<const __nv_bfloat16 *>(resolve(frame, src));
+  uint2 *out = reinterpret_cast<uint2 *>(resolve(frame, dst));
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pix; i += (long long)gridDim.x * blockDim.x) {
     const __nv_bfloat16 *s = in + 3 * i;
     __nv_bfloat162 lo = __halves2bfloat162(s[0], s[1]);
@@ -27,13 +49,15 @@ __global__ void pad_c4_kernel(const __nv_bfloat16 *__restrict__ in, __nv_bfloat1
     uint2 v;
     v.x = *reinterpret_cast<uint32_t *>(&lo);
     v.y = *reinterpret_cast<uint32_t *>(&hi);
-    reinterpret_cast<uint2 *>(out)[i] = v;
+    out[i] = v;
   }
 }
 
 // 3x3 stride-2 pad-1 max pool over NHWC bf16; one thread = 8 channels of one output pixel
-__global__ void maxpool_kernel(const __nv_bfloat16 *__restrict__ in, __nv_bfloat16 *__restrict__ out, int N, int H,
-                               int W, int C, int P, int Q) {
+__global__ void maxpool_kernel(const uint64_t *frame, BufRef src, BufRef dst, int N, int H, int W, int C, int P,
+                               int Q) {
+  const __nv_bfloat16 *in = reinterpret_cast<const __nv_bfloat16 *>(resolve(frame, src));
+  __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(resolve(frame, dst));
   const int c8 = C / 8;
   const long long total = (long long)N * P * Q * c8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -71,7 +95,9 @@ __global__ void maxpool_kernel(const __nv_bfloat16 *__restrict__ in, __nv_bfloat
 }
 
 // global average pool: [N, HW, C] bf16 -> [N, C] fp32
-__global__ void avgpool_kernel(const __nv_bfloat16 *__restrict__ in, float *__restrict__ feat, int HW, int C) {
+__global__ void avgpool_kernel(const uint64_t *frame, BufRef src, BufRef dst, int HW, int C) {
+  const __nv_bfloat16 *in = reinterpret_cast<const __nv_bfloat16 *>(resolve(frame, src));
+  float *feat = reinterpret_cast<float *>(resolve(frame, dst));
   const int n = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const __nv_bfloat16 *p = in + (size_t)n * HW * C + c;
@@ -81,8 +107,10 @@ __global__ void avgpool_kernel(const __nv_bfloat16 *__restrict__ in, float *__re
 }
 
 // logits[n, j] = feat[n] . W[j] + b[j]; one warp per class j, all n
-__global__ void fc_kernel(const float *__restrict__ feat, const __nv_bfloat16 *__restrict__ w,
-                          const __nv_bfloat16 *__restrict__ b, float *__restrict__ out, int N, int C, int J) {
+__global__ void fc_kernel(const uint64_t *frame, BufRef src, BufRef dst, const __nv_bfloat16 *__restrict__ w,
+                          const __nv_bfloat16 *__restrict__ b, int N, int C, int J) {
+  const float *feat = reinterpret_cast<const float *>(resolve(frame, src));
+  float *out = reinterpret_cast<float *>(resolve(frame, dst));
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= J) return;
   const __nv_bfloat16 *wr = w + (size_t)warp * C;
@@ -104,10 +132,35 @@ __global__ void fc_kernel(const float *__restrict__ feat, const __nv_bfloat16 *_
   }
 }
 
+// one invocation's frame: where its buffers are
+__global__ void set_frame_kernel(uint64_t *frame, uint64_t input, uint64_t out, uint64_t ws) {
+  if (threadIdx.x == 0) {
+    frame[0] = input;
+    frame[1] = out;
+    frame[2] = ws;
+  }
+}
+
+constexpr int kInstances = 8;   // concurrent runs of one program over one segment
+
+struct GraphInst {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t *frame = nullptr;      // device: {input, logits, workspace}
+  cudaEvent_t done = nullptr;     // end of this instance's last run
+  bool used = false;
+};
+struct GraphSet {                 // the instances of one (segment, context)
+  std::vector<GraphInst> inst;
+  uint64_t next = 0;
+};
+
 struct Net {
   std::vector<sage_net_op> ops;
   std::vector<uint64_t> buf_off;     // workspace offsets of buffers 2..
   uint64_t workspace = 0;
+  std::mutex mu;
+  std::map<std::pair<uint64_t, CUcontext>, GraphSet> graphs;
+  cudaStream_t capture = nullptr;
 };
 static std::mutex g_net_mu;
 static std::unordered_map<uint64_t, Net *> g_nets;
@@ -125,60 +178,65 @@ static int grid_for(long long n, int sms) {
   return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)sms * 16));
 }
 
-// run a registered network on stream s: ro = landed segment, input = request
-// image, out = logits followed by the workspace (b->out_bytes covers logits)
-int net_run(const sage_body_desc *b, cudaStream_t s, int sms) {
-  Net *net = net_get((uint64_t)b->args[0]);
-  if (!net) return fail(SAGE_EINVAL, "resnet body: unknown network handle");
-  const uint64_t ws = (b->out + b->out_bytes + 255) & ~255ull;
-  auto buf = [&](int id) -> uint64_t {
-    if (id == SAGE_NET_BUF_INPUT) return b->input;
-    if (id == SAGE_NET_BUF_OUT) return b->out;
-    if (id < SAGE_NET_BUF_WS0 || id - SAGE_NET_BUF_WS0 >= (int)net->buf_off.size()) return 0;
-    return ws + net->buf_off[id - SAGE_NET_BUF_WS0];
+// enqueue the program on s.  frame != null: buffers come from the device
+// frame (graph capture); else from base[3] = {input, logits, workspace}.
+static int enqueue_ops(Net *net, uint64_t ro, const uint64_t *frame, const uint64_t base[3], cudaStream_t s, int sms) {
+  auto ref = [&](int id, BufRef *r) -> bool {
+    if (id == SAGE_NET_BUF_INPUT) *r = {0, 0, base[0]};
+    else if (id == SAGE_NET_BUF_OUT) *r = {1, 0, base[1]};
+    else if (id >= SAGE_NET_BUF_WS0 && id - SAGE_NET_BUF_WS0 < (int)net->buf_off.size()) {
+      const uint64_t off = net->buf_off[id - SAGE_NET_BUF_WS0];
+      *r = {2, off, base[2] + off};
+    } else {
+      return false;
+    }
+    return true;
   };
   for (const sage_net_op &op : net->ops) {
-    const uint64_t src = buf(op.src), dst = buf(op.dst);
-    if (!src || !dst) return fail(SAGE_EINVAL, "resnet body: op names an unknown buffer");
+    BufRef src, dst, res{};
+    if (!ref(op.src, &src) || !ref(op.dst, &dst) || (op.res >= 0 && !ref(op.res, &res)))
+      return fail(SAGE_EINVAL, "resnet body: op names an unknown buffer");
     switch (op.kind) {
       case SAGE_NET_PAD_INPUT: {
         const long long pix = (long long)op.n * op.h * op.w;
-        pad_c4_kernel<<<grid_for(pix, sms), 256, 0, s>>>((const __nv_bfloat16 *)src, (__nv_bfloat16 *)dst, pix);
+        pad_c4_kernel<<<grid_for(pix, sms), 256, 0, s>>>(frame, src, dst, pix);
         break;
       }
       case SAGE_NET_CONV: {
         sage_conv_desc d{};
-        d.x = src;
-        d.out = dst;
-        d.w = b->ro + op.w_off;
-        d.residual = op.res >= 0 ? buf(op.res) : 0;
+        d.x = frame ? 16 : src.direct;        // direct pointers only validate alignment in frame mode
+        d.out = frame ? 16 : dst.direct;
+        d.residual = op.res >= 0 ? (frame ? 16 : res.direct) : 0;
+        d.w = ro + op.w_off;
         if (op.g_off != UINT64_MAX) {
-          d.bn_gamma = b->ro + op.g_off;
-          d.bn_beta = b->ro + op.b_off;
-          d.bn_mean = b->ro + op.m_off;
-          d.bn_var = b->ro + op.v_off;
+          d.bn_gamma = ro + op.g_off;
+          d.bn_beta = ro + op.b_off;
+          d.bn_mean = ro + op.m_off;
+          d.bn_var = ro + op.v_off;
         }
         d.bn_eps = op.eps;
         d.n = op.n; d.h = op.h; d.w_ = op.w; d.cin = op.cin; d.cout = op.cout;
         d.r = op.r; d.s = op.s; d.stride = op.stride; d.pad = op.pad; d.relu = op.relu; d.mode = op.mode;
-        SAGE_TRY(conv_bf16(&d, s, sms));
+        if (frame) {
+          ConvFrame f{frame, src.sel, op.res >= 0 ? res.sel : -1, dst.sel, src.off, res.off, dst.off};
+          SAGE_TRY(conv_bf16(&d, s, sms, &f));
+        } else {
+          SAGE_TRY(conv_bf16(&d, s, sms, nullptr));
+        }
         continue;
       }
       case SAGE_NET_MAXPOOL: {
         const int P = (op.h + 2 - 3) / 2 + 1, Q = (op.w + 2 - 3) / 2 + 1;
-        maxpool_kernel<<<grid_for((long long)op.n * P * Q * op.cin / 8, sms), 256, 0, s>>>(
-            (const __nv_bfloat16 *)src, (__nv_bfloat16 *)dst, op.n, op.h, op.w, op.cin, P, Q);
+        maxpool_kernel<<<grid_for((long long)op.n * P * Q * op.cin / 8, sms), 256, 0, s>>>(frame, src, dst, op.n,
+                                                                                          op.h, op.w, op.cin, P, Q);
         break;
       }
       case SAGE_NET_POOL_FC: {
-        const uint64_t feat = buf(op.res);
-        if (!feat) return fail(SAGE_EINVAL, "resnet body: POOL_FC needs a feature buffer");
-        avgpool_kernel<<<dim3((op.cin + 255) / 256, op.n), 256, 0, s>>>((const __nv_bfloat16 *)src, (float *)feat,
-                                                                       op.h * op.w, op.cin);
-        fc_kernel<<<(op.cout * 32 + 255) / 256, 256, 0, s>>>((const float *)feat,
-                                                              (const __nv_bfloat16 *)(b->ro + op.w_off),
-                                                              (const __nv_bfloat16 *)(b->ro + op.b_off), (float *)dst,
-                                                              op.n, op.cin, op.cout);
+        if (op.res < 0) return fail(SAGE_EINVAL, "resnet body: POOL_FC needs a feature buffer");
+        avgpool_kernel<<<dim3((op.cin + 255) / 256, op.n), 256, 0, s>>>(frame, src, res, op.h * op.w, op.cin);
+        fc_kernel<<<(op.cout * 32 + 255) / 256, 256, 0, s>>>(frame, res, dst, (const __nv_bfloat16 *)(ro + op.w_off),
+                                                              (const __nv_bfloat16 *)(ro + op.b_off), op.n, op.cin,
+                                                              op.cout);
         break;
       }
       default:
@@ -189,13 +247,107 @@ int net_run(const sage_body_desc *b, cudaStream_t s, int sms) {
   return SAGE_OK;
 }
 
+static bool graphs_enabled() {
+  static const bool on = [] { const char *e = getenv("SAGE_NET_GRAPHS"); return !(e && atoi(e) == 0); }();
+  return on;
+}
+
+// capture one instance of the program over segment `ro` (net->mu held)
+static int capture_instance(Net *net, uint64_t ro, int sms, GraphInst *gi) {
+  SAGE_TRY(conv_optin_all());   // attributes are not settable while capturing
+  SAGE_CUDA(cudaMalloc(&gi->frame, 4 * sizeof(uint64_t)));
+  SAGE_CUDA(cudaEventCreateWithFlags(&gi->done, cudaEventDisableTiming));
+  if (!net->capture) SAGE_CUDA(cudaStreamCreateWithFlags(&net->capture, cudaStreamNonBlocking));
+  SAGE_CUDA(cudaStreamBeginCapture(net->capture, cudaStreamCaptureModeThreadLocal));
+  const uint64_t none[3] = {0, 0, 0};
+  int rc = enqueue_ops(net, ro, gi->frame, none, net->capture, sms);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(net->capture, &g);
+  if (rc != SAGE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture (resnet program)");
+  e = cudaGraphInstantiate(&gi->exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (resnet program)");
+  return SAGE_OK;
+}
+
+// run a registered network on stream s: ro = landed segment, input = request
+// image, out = logits followed by the workspace (b->out_bytes covers logits)
+int net_run(const sage_body_desc *b, cudaStream_t s, int sms) {
+  Net *net = net_get((uint64_t)b->args[0]);
+  if (!net) return fail(SAGE_EINVAL, "resnet body: unknown network handle");
+  const uint64_t ws = (b->out + b->out_bytes + 255) & ~255ull;
+  if (!graphs_enabled()) {
+    const uint64_t base[3] = {b->input, b->out, ws};
+    return enqueue_ops(net, b->ro, nullptr, base, s, sms);
+  }
+  CUcontext ctx = nullptr;
+  drv.CtxGetCurrent(&ctx);
+  std::lock_guard<std::mutex> lk(net->mu);
+  GraphSet &set = net->graphs[{b->ro, ctx}];
+  // an idle instance, else a new one (up to kInstances), else round robin
+  GraphInst *gi = nullptr;
+  for (auto &x : set.inst)
+    if (!x.used || cudaEventQuery(x.done) == cudaSuccess) {
+      gi = &x;
+      break;
+    }
+  if (!gi && (int)set.inst.size() < kInstances) {
+    set.inst.emplace_back();
+    gi = &set.inst.back();
+    int rc = capture_instance(net, b->ro, sms, gi);
+    if (rc != SAGE_OK) {
+      set.inst.pop_back();
+      return rc;
+    }
+  }
+  if (!gi) gi = &set.inst[set.next++ % set.inst.size()];
+  if (gi->used) SAGE_CUDA(cudaStreamWaitEvent(s, gi->done, 0));   // its frame is free once its last run ended
+  set_frame_kernel<<<1, 32, 0, s>>>(gi->frame, b->input, b->out, ws);
+  SAGE_CUDA(cudaGetLastError());
+  SAGE_CUDA(cudaGraphLaunch(gi->exec, s));
+  SAGE_CUDA(cudaEventRecord(gi->done, s));
+  gi->used = true;
+  return SAGE_OK;
+}
+
 int touch_net_kernels() {
   cudaFuncAttributes a;
   SAGE_CUDA(cudaFuncGetAttributes(&a, pad_c4_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, maxpool_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, avgpool_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, fc_kernel));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, set_frame_kernel));
   return touch_conv_kernels();
+}
+
+static void net_drop_graphs(Net *N) {
+  std::lock_guard<std::mutex> lk(N->mu);
+  for (auto &kv : N->graphs)
+    for (auto &gi : kv.second.inst) {
+      if (gi.done) {
+        cudaEventSynchronize(gi.done);
+        cudaEventDestroy(gi.done);
+      }
+      if (gi.exec) cudaGraphExecDestroy(gi.exec);
+      if (gi.frame) cudaFree(gi.frame);
+    }
+  N->graphs.clear();
+  if (N->capture) cudaStreamDestroy(N->capture);
+  N->capture = nullptr;
+}
+
+static void net_free(Net *N) {
+  net_drop_graphs(N);
+  delete N;
+}
+
+void nets_release_graphs() {
+  std::lock_guard<std::mutex> lk(g_net_mu);
+  for (auto &kv : g_nets) net_drop_graphs(kv.second);
 }
 
 }  // namespace sage
@@ -228,10 +380,14 @@ extern "C" int sage_net_create(const sage_net_op *ops, int n_ops, const uint64_t
 }
 
 extern "C" int sage_net_destroy(sage_handle net) {
-  std::lock_guard<std::mutex> lk(g_net_mu);
-  auto it = g_nets.find(net & ((1ull << 56) - 1));
-  if ((net >> 56) != kNetKind || it == g_nets.end()) return fail(SAGE_ESTATE, "net_destroy: unknown network");
-  delete it->second;
-  g_nets.erase(it);
+  Net *N;
+  {
+    std::lock_guard<std::mutex> lk(g_net_mu);
+    auto it = g_nets.find(net & ((1ull << 56) - 1));
+    if ((net >> 56) != kNetKind || it == g_nets.end()) return fail(SAGE_ESTATE, "net_destroy: unknown network");
+    N = it->second;
+    g_nets.erase(it);
+  }
+  net_free(N);
   return SAGE_OK;
 }

@@ -67,11 +67,12 @@ def cfg1(n: int = 16, reps: int = 5) -> dict:
     return out
 
 
-def cfg3(rate: float = 300.0, duration_s: float = 4.0, gpus_list=(1, 2, 4), seed: int = 1, dtype: str = "fp32") -> dict:
+def cfg3(rate: float = 300.0, duration_s: float = 4.0, gpus_list=(1, 2, 4), seed: int = 1, dtype: str = "fp32",
+         engine: str | None = None) -> dict:
     from .dnn import resnet50
-    spec, data = resnet50(dtype=dtype)
+    spec, data = resnet50(dtype=dtype, engine=engine)
     arrivals = generate_arrivals(PoissonOpenSpec(rate, duration_s, {spec.name: 1.0}), seed)
-    out = {"workload": f"ResNet-50 (random init, {data.layout.seg_bytes} B {dtype} weights, batch 8) "
+    out = {"engine": data.body, "workload": f"ResNet-50 (random init, {data.layout.seg_bytes} B {dtype} weights, batch 8) "
                        f"Poisson {rate:g}/s for {duration_s:g} s ({len(arrivals)} arrivals)"}
     for g in gpus_list:
         sim = Simulation(ClusterSpec(gpus=g), policy_preset("SAGE"), {spec.name: spec}, seed=seed,
@@ -282,6 +283,8 @@ def main(argv=None):
     ap.add_argument("--trace", default=None, help="trace: flat trace CSV (timestamp_ms,function)")
     ap.add_argument("--time-scale", type=float, default=1.0)
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"], help="cfg3: ResNet-50 weights / input")
+    ap.add_argument("--engine", default=None, choices=["native", "torch"],
+                    help="cfg3: ResNet-50 body (default: native for bf16, torch for fp32)")
     args = ap.parse_args(argv)
     if args.trace:
         res = trace(args.trace, args.workload, time_scale=args.time_scale, out_dir=args.out)
@@ -300,6 +303,7 @@ def main(argv=None):
             if args.gpus:
                 kw["gpus_list"] = tuple(int(g) for g in args.gpus.split(","))
             kw["dtype"] = args.dtype
+            kw["engine"] = args.engine
         res = RUNNERS[c](**kw)
         res["elapsed_s"] = round(time.perf_counter() - t0, 1)
         line = json.dumps({c: res})
