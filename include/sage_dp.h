@@ -175,6 +175,8 @@ int sage_slot_stream(sage_handle slot, uint64_t *stream);
 #define SAGE_LOAD_SRC_PINNED   0x1u  /* src is pinned/registered: skip the staging memcpy */
 #define SAGE_LOAD_SRC_DEVICE   0x2u  /* src is a device pointer (HBM-resident): no PCIe   */
 #define SAGE_LOAD_SRC_PEER     0x4u  /* src is a device pointer on another GPU: NVLink    */
+#define SAGE_LOAD_NO_VERIFY    0x8u  /* pinned identity loads: DMA only, no checksum pass
+                                        (private payloads; shared segments always verify)  */
 typedef struct {
   int32_t gpu;
   uint32_t flags;
@@ -263,6 +265,9 @@ int sage_return(sage_handle slot, uint64_t src_dptr, void *host_dst, uint64_t by
 #define SAGE_INV_SYNC     0x08u   /* SYNC_WAIT on `wait` (leader tokens)             */
 #define SAGE_INV_RET_HOST 0x10u   /* ret_dst is host memory: the D2H leaves the slot
                                      stream for a return stream (PCIe overlap)      */
+#define SAGE_INV_VERIFY_INPUT 0x20u /* checksum the landed input too (off: the input is
+                                     private to the invocation; only shared segments
+                                     must be verified, north_star)                  */
 #define SAGE_SRC_HOST      0      /* pageable host: staging memcpy (CPU_LOAD) + H2D */
 #define SAGE_SRC_PINNED    1      /* pinned host: H2D only                          */
 #define SAGE_SRC_HBM       2      /* device-resident source: land from HBM          */

@@ -26,7 +26,7 @@ SAGE_INIT_PEER_ACCESS = 0x1
 SAGE_INIT_SHARE_DEVICE = 0x2
 CLASS_CONTEXT, CLASS_READ_ONLY, CLASS_WRITABLE, CLASS_INSTANCE_FIXED = 0, 1, 2, 3
 ALLOC_ACCOUNT_ONLY = 0x100
-LOAD_SRC_PINNED, LOAD_SRC_DEVICE, LOAD_SRC_PEER = 0x1, 0x2, 0x4
+LOAD_SRC_PINNED, LOAD_SRC_DEVICE, LOAD_SRC_PEER, LOAD_NO_VERIFY = 0x1, 0x2, 0x4, 0x8
 BODY_TOUCH, BODY_SGEMM, BODY_STENCIL, BODY_SPMV, BODY_SPIN, BODY_SGEMM_F32, BODY_GATHER = 0, 1, 2, 3, 4, 5, 6
 BODY_SPMV_CSB = 7
 
@@ -67,7 +67,7 @@ class FixedGSLDesc(C.Structure):
                 ("body", BodyDesc), ("result", C.c_void_p), ("result_bytes", u64), ("ctx", H)]
 
 
-INV_CTX, INV_RO, INV_INPUT, INV_SYNC, INV_RET_HOST = 0x1, 0x2, 0x4, 0x8, 0x10
+INV_CTX, INV_RO, INV_INPUT, INV_SYNC, INV_RET_HOST, INV_VERIFY_INPUT = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 SRC_HOST, SRC_PINNED, SRC_HBM, SRC_PEER = 0, 1, 2, 3
 
 

@@ -434,8 +434,10 @@ int sage::launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b) {
       work = 12ull * (uint64_t)b->args[0] * (uint64_t)b->args[1] * (uint64_t)b->args[2];
       break;
     case SAGE_BODY_SPMV:
-      kind = SAGE_KERNEL_SPMV;  // row_ptr + (col, val) per nnz + x gathers + y
-      work = 4ull * (b->args[0] + 1) + 8ull * b->args[1] + 4ull * b->args[1] + 4ull * b->args[0];
+      // 8 B (col, val) per nnz + row_ptr + y + x read once; the
+      // x gathers hit L2 (x is 4 MiB) and are not HBM bytes
+      kind = SAGE_KERNEL_SPMV;
+      work = 8ull * b->args[1] + 4ull * (b->args[0] + 1) + 4ull * b->args[0] + b->input_bytes;
       break;
     case SAGE_BODY_SPMV_CSB:
       kind = SAGE_KERNEL_SPMV;  // 8 B per entry + x once per row group + y

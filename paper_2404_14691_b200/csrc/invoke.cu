@@ -351,7 +351,7 @@ static int issue_tail(Inv *I) {
   if (d->flags & SAGE_INV_INPUT) {
     sage_load_desc L{};
     L.gpu = d->gpu;
-    L.flags = load_flags(d->in_kind);
+    L.flags = load_flags(d->in_kind) | ((d->flags & SAGE_INV_VERIFY_INPUT) ? 0u : SAGE_LOAD_NO_VERIFY);
     L.dst = d->in_dst;
     L.src = d->in_src;
     L.src_bytes = d->in_bytes;

@@ -574,22 +574,25 @@ int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCu
     const uint64_t n = d->src_bytes, seg = lay->seg;
     if (seg > n) SAGE_CUDA(cudaMemsetAsync(dst + n, 0, seg - n, s));
     SAGE_CUDA(cudaMemcpyAsync(dst, d->src, n, cudaMemcpyHostToDevice, s));
-    SAGE_CUDA(cudaEventRecord(G->ev_dma, s));
-    s = G->verify;
-    SAGE_CUDA(cudaStreamWaitEvent(s, G->ev_dma, 0));
     L->link_bytes = n;
     L->chunks = 1;
-    LandArgs a{};
-    a.dst = dst;
-    a.total_vec = (uint32_t)(seg / 16);
-    a.acc = G->scratch.d_acc + L->acc_idx;
-    a.done = G->scratch.d_done + L->acc_idx;
-    a.out = G->scratch.d_res + L->acc_idx;
-    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((seg / 16 + 1023) / 1024, G->sm_count * 8ull));
-    cudaEvent_t sb = stat_begin(G, s);
-    verify_kernel<<<blocks, 256, 0, s>>>(a);
-    SAGE_CUDA(cudaGetLastError());
-    stat_end(G, s, SAGE_KERNEL_VERIFY, sb, seg);
+    if (!(d->flags & SAGE_LOAD_NO_VERIFY)) {
+      SAGE_CUDA(cudaEventRecord(G->ev_dma, s));
+      s = G->verify;
+      SAGE_CUDA(cudaStreamWaitEvent(s, G->ev_dma, 0));
+      LandArgs a{};
+      a.dst = dst;
+      a.total_vec = (uint32_t)(seg / 16);
+      a.acc = G->scratch.d_acc + L->acc_idx;
+      a.done = G->scratch.d_done + L->acc_idx;
+      a.out = G->scratch.d_res + L->acc_idx;
+      const int blocks =
+          (int)std::max<uint64_t>(1, std::min<uint64_t>((seg / 16 + 1023) / 1024, G->sm_count * 8ull));
+      cudaEvent_t sb = stat_begin(G, s);
+      verify_kernel<<<blocks, 256, 0, s>>>(a);
+      SAGE_CUDA(cudaGetLastError());
+      stat_end(G, s, SAGE_KERNEL_VERIFY, sb, seg);
+    }
     SAGE_TRY(event_record(Ee, s));
     SAGE_TRY(event_alias(L->he, end_ev));   // the caller's end handle: same event
     uint64_t id = g_load_next++;

@@ -279,6 +279,10 @@ class DataPlane:
         self.data: dict[str, FunctionData] = {}
         self.results_in_hbm = False   # bench `value` leg: RETURN copies D2D
         self._contexts: set = set()     # DGSF pre-created CUDA contexts
+        # checksum private request payloads too (shared RO segments always are);
+        # off by default: a second HBM read of every input (SAGE_VERIFY_INPUTS=1)
+        import os
+        self.verify_inputs = os.environ.get("SAGE_VERIFY_INPUTS") == "1"
         self._free_slots: dict[int, list] = {}
         self._fast = _FastCompletions(self)
         self._scratch: dict[tuple[int, int], list] = {}
@@ -533,7 +537,7 @@ class DataPlane:
                 run.ro_source = "pcie"
                 publish = box is not None and grant is not None and grant.leader_ro
         if fd.input_bytes:
-            flags |= _lib.INV_INPUT
+            flags |= _lib.INV_INPUT | (_lib.INV_VERIFY_INPUT if self.verify_inputs else 0)
             d.in_dst, d.in_bytes = in_dst, fd.input_bytes
             payload = inv.payload
             if payload is None and fd.input_dev is not None:

@@ -41,7 +41,7 @@ sim.dataplane.pin_host_store()
 out, ok = [], True
 for rep in range(2):
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     dist.barrier()
     invs = sim.submit_many(names)
     sim.drain()

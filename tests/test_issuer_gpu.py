@@ -35,10 +35,11 @@ for n in names:
     pb.view()[:] = data[n].input
     pls.append(pb)
 sim.dataplane.pin_host_store()
+sim.dataplane.verify_inputs = True   # the input checksums are compared across runs
 out, res = [], []
 for rep in range(2):
     for r in list(sim.sharing.residents.values()):
-        sim.sharing._evict(r)
+        sim.sharing.evict(r)
     invs = sim.submit_many(names, payloads=pls)
     sim.drain()
     land = {}
