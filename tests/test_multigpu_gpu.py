@@ -54,7 +54,7 @@ def test_two_gpu_placement_and_pcie_once(built, fanout):
                 assert set(srcs) == {"pcie"}
         sim.check_no_leaks()
         for s in sim.sharing.residents.values():
-            assert s.state.value in ("Stage1",)
+            assert s.state.label == "Stage1"
         sim.sharing.check_consistency()
     finally:
         sim.close()
