@@ -58,6 +58,8 @@ int         sage_shutdown(void);
 const char *sage_last_error(void);
 int         sage_abi_version(void);
 int         sage_device_count(int *n);
+/* physical CUDA device of logical GPU `gpu` (device offset / shared planes applied) */
+int         sage_gpu_device(int gpu, int *dev);
 int64_t     sage_now_us(void);
 /* host threads used for the CPU_LOAD memcpy fan-out (default 8) */
 int         sage_set_host_threads(int n);

@@ -146,6 +146,7 @@ _SIGS = {
     "sage_last_error": (C.c_char_p, []),
     "sage_abi_version": (C.c_int, []),
     "sage_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "sage_gpu_device": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "sage_now_us": (i64, []),
     "sage_set_host_threads": (C.c_int, [C.c_int]),
     "sage_pool_configure": (C.c_int, [C.c_int, u64, u64]),
@@ -283,6 +284,13 @@ _up = False
 
 def is_up() -> bool:
     return _up
+
+
+def gpu_device(gpu: int) -> int:
+    """Physical CUDA device of logical GPU `gpu` (the library's own mapping)."""
+    d = C.c_int(0)
+    check(lib().sage_gpu_device(gpu, C.byref(d)), "sage_gpu_device")
+    return d.value
 
 
 def device_count() -> int:

@@ -110,6 +110,10 @@ struct ChunkScratch {  // per-load device accumulator + pinned result
   unsigned long long *d_res = nullptr;   // ... device view
   uint32_t n = 0;
   std::atomic<uint64_t> next{0};
+  // a slot belongs to one load from open to release: its result must not be
+  // overwritten by a later load while the first is still unread
+  std::vector<uint8_t> busy;
+  std::mutex mu;
 };
 
 struct Gpu {

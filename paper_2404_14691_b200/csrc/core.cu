@@ -429,6 +429,16 @@ const char *sage_last_error(void) { return tl_err.c_str(); }
 int sage_abi_version(void) { return SAGE_ABI_VERSION; }
 int64_t sage_now_us(void) { return host_now_us(); }
 
+// the physical CUDA device logical GPU g runs on (SAGE_DEVICE_OFFSET and
+// SAGE_INIT_SHARE_DEVICE applied): what a framework running a body on the
+// invocation's stream (ResNet-50 via PyTorch) must select
+int sage_gpu_device(int gpu, int *dev) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G || !dev) return fail(SAGE_ENODEV, "gpu_device: bad logical gpu");
+  *dev = G->dev;
+  return SAGE_OK;
+}
 int sage_device_count(int *n) {
   if (!n) return fail(SAGE_EINVAL, "null n");
   int c = 0;

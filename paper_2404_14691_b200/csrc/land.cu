@@ -220,7 +220,7 @@ struct Load {
   std::atomic<int64_t> cpu_begin{-1}, cpu_end{-1};
   uint64_t host_bytes = 0, link_bytes = 0, landed = 0;
   uint32_t chunks = 0;
-  uint32_t acc_idx = 0;
+  uint32_t acc_idx = UINT32_MAX;   // checksum slot (held until release)
   bool has_gpu_begin = false;
 };
 
@@ -533,6 +533,18 @@ int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCu
     int rc = identity_layout(d->src_bytes, &lay);
     if (rc != SAGE_OK) { delete L; return rc; }
   }
+  if (Gpu *G0 = gpu_get(d->gpu); G0 && lay->chunked.chunk != G0->chunk) {
+    // planned with another chunk size (created before sage_init picked this
+    // plane's): re-plan, or staged chunks would overflow their ring slots
+    std::lock_guard<std::mutex> lk(g_lay_mu);
+    if (lay->chunked.chunk != G0->chunk) {
+      Plan fresh;
+      int rc = build_plan(*lay, G0->chunk, &fresh);
+      if (rc != SAGE_OK) { delete L; return rc; }
+      plan_free(&lay->chunked);
+      lay->chunked = std::move(fresh);
+    }
+  }
   {
     int rc = plan_upload(&lay->chunked, d->gpu);
     if (rc == SAGE_OK) rc = plan_upload(&lay->whole, d->gpu);
@@ -556,7 +568,21 @@ int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCu
   L->eb = Eb;
   L->ee = Ee;
   L->landed = lay->seg;
-  L->acc_idx = (uint32_t)(G->scratch.next++ % G->scratch.n);
+  {
+    // a free accumulator slot (owned until sage_load_release)
+    ChunkScratch &S = G->scratch;
+    std::lock_guard<std::mutex> lk(S.mu);
+    uint32_t k = 0;
+    for (; k < S.n; ++k) {
+      const uint32_t idx = (uint32_t)(S.next++ % S.n);
+      if (!S.busy[idx]) {
+        S.busy[idx] = 1;
+        L->acc_idx = idx;
+        break;
+      }
+    }
+    if (k == S.n) { delete L; return fail(SAGE_ENOMEM, "segment_load: every checksum slot is held by an unreleased load"); }
+  }
   G->scratch.h_res[L->acc_idx] = 0;   // an empty load publishes nothing
   uint8_t *dst = reinterpret_cast<uint8_t *>(d->dst);
 
@@ -681,6 +707,10 @@ int sage_load_release(sage_handle h) {
   }
   cudaSetDevice(dev_of(L->gpu));
   cudaEventSynchronize(L->ev_end);  // host copies reference L until the end
+  if (Gpu *G = gpu_get(L->gpu)) {
+    std::lock_guard<std::mutex> lk(G->scratch.mu);
+    if (L->acc_idx < G->scratch.busy.size()) G->scratch.busy[L->acc_idx] = 0;
+  }
   sage_event_release(L->hb);
   sage_event_release(L->he);
   delete L;

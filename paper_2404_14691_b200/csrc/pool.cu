@@ -235,7 +235,8 @@ int gpu_setup(int id, uint64_t pool_bytes, uint64_t staging_bytes, uint64_t chun
     SAGE_CUDA(cudaEventCreateWithFlags(&G->ev_land[i], cudaEventDisableTiming));
   }
   // checksum accumulators: one per in-flight load
-  G->scratch.n = 4096;
+  G->scratch.n = 16384;
+  G->scratch.busy.assign(G->scratch.n, 0);
   SAGE_CUDA(cudaMalloc((void **)&G->scratch.d_acc, G->scratch.n * sizeof(unsigned long long)));
   SAGE_CUDA(cudaMalloc((void **)&G->scratch.d_done, G->scratch.n * sizeof(unsigned int)));
   SAGE_CUDA(cudaMemset(G->scratch.d_acc, 0, G->scratch.n * sizeof(unsigned long long)));

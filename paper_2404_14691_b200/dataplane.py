@@ -772,7 +772,7 @@ class DataPlane:
                     run.slot.wait(deps)
                     b = run.slot.record()
                     dnn.run_resnet50(fd, self._ro_dst(run), in_dst, out_dst, run.slot.stream(),
-                                     gpu % max(1, _lib.device_count()), plane=gpu)
+                                     _lib.gpu_device(gpu), plane=gpu)
                     e = run.slot.record()
                 else:
                     body = self._body(run, fd, resident, in_dst, out_dst)

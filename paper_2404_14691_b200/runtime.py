@@ -204,7 +204,7 @@ class Simulation:
                 fd.layout.handle()
             if fd.body == "resnet50":
                 from . import dnn
-                for dev in sorted({g % max(1, _lib.device_count()) for g in range(self.gpu_count)}):
+                for dev in sorted({_lib.gpu_device(g) for g in range(self.gpu_count)}):
                     dnn.prewarm(fd, dev)
             elif fd.body == "resnet50_native":
                 from . import dnn
