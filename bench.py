@@ -678,6 +678,7 @@ def our_arm(args, rank, world, dist) -> dict:
         per_step = len(names)
         pcie = pcie_probe(_my_device())
         h2d = sum(i.measured.get("pcie_bytes", 0) for i in invs_e2e) / args.steps
+        h2d_rank = float(h2d)        # this rank's PCIe bytes per step (N > 1: homes carry the RO segments)
         d2h = sum(data[n].out_bytes for n in names)
         setups_e2e = [i.setup_us for i in invs_e2e]
         # ---- value: HBM-resident sources ----------------------------------------
@@ -697,6 +698,22 @@ def our_arm(args, rank, world, dist) -> dict:
         sim.dataplane.results_in_hbm = False
         sim.dataplane.drop_hbm_sources()
         sim.check_no_leaks()
+        link = None
+        if box is not None and box.kind == "peer":
+            # the fan-out receive step measured alone: a peer-reading land of a
+            # 256 MiB segment from every other rank's pages over NVLink
+            per_peer = box.link_probe(_my_device() if not _shared_gpu() else 0)
+            mine = [v for v in per_peer.values() if v]
+            lo = min_over_ranks(dist, min(mine) if mine else 0.0)
+            hi = max_over_ranks(dist, max(mine) if mine else 0.0)
+            link = {"nvlink_GBps_min": round(lo, 1), "nvlink_GBps_max": round(hi, 1),
+                    "frac_of_measured_peer_copy_770": round(lo / 770.0, 3), "frac_of_nominal_900": round(lo / 900.0, 3),
+                    "how": "each rank lands every peer's 256 MiB segment with the peer-reading land (checksum "
+                           "fused), median of 5 per peer, device events; min / max over ranks and peers",
+                    "note": ("ranks share one device (SAGE_BENCH_SHARE_GPU): an HBM rate, not NVLink"
+                             if _shared_gpu() else "")}
+        pcie_rank = {"h2d_bytes_per_step_min": int(min_over_ranks(dist, h2d_rank)),
+                     "h2d_bytes_per_step_max": int(max_over_ranks(dist, h2d_rank))}
     finally:
         _lib.check(L.sage_stats_enable(0), "stats_enable")
         if box is not None:
@@ -799,7 +816,8 @@ def our_arm(args, rank, world, dist) -> dict:
             "nvlink_GBps_e2e": round(sum_over_ranks(dist, e2e_box_bytes) / (e2e_us / 1e6) / 1e9, 2),
             "nvlink_GBps_note": "segment bytes received by all ranks in the timed e2e steps over the e2e time "
                                 "(a traffic rate, not a link benchmark)",
-            "ro_checksums_agree": ro_checksums_agree(dist, data)},
+            "ro_checksums_agree": ro_checksums_agree(dist, data),
+            "link_probe": link, "pcie_per_rank": pcie_rank},
         "clocks": clocks_val,
         "clocks_e2e": clocks_e2e,
     }

@@ -217,6 +217,34 @@ int sage_d2h_cache(int gpu, uint64_t src_dptr, void *host_dst, uint64_t bytes,
 /* peer copy of a landed segment to another GPU over NVLink (fan-out)         */
 int sage_fanout(int src_gpu, uint64_t src_dptr, int dst_gpu, uint64_t dst_dptr, uint64_t bytes,
                 const sage_handle *wait, int n_wait, sage_handle *end_ev);
+/* what the box offers for the one-to-many step (simulation.py:113-115 is the
+ * shared host channel it replaces): peer reachability per plane, and whether
+ * an NVSwitch multicast object can be made (why not, if not)               */
+typedef struct {
+  int32_t n_gpus, n_devices;
+  uint32_t peer_mask[32];        /* bit h of [g]: plane g reaches plane h's pages     */
+  int32_t multicast_attr;        /* every device reports MULTICAST_SUPPORTED          */
+  int32_t multicast;             /* a multicast object over all devices was created   */
+  uint64_t multicast_granularity;
+  char why[160];
+} sage_fanout_caps_t;
+int sage_fanout_caps(sage_fanout_caps_t *out);
+/* one segment into up to 32 destination allocations (pool handles, one per
+ * GPU): NVLS multicast (multimem.st through a multicast object binding every
+ * destination's pages, one pass over the source) when every destination is
+ * on its own device and the box allows it, else copy-engine peer copies    */
+#define SAGE_BCAST_P2P_ONLY        0x1u
+#define SAGE_BCAST_PATH_P2P        0
+#define SAGE_BCAST_PATH_MULTICAST  1
+typedef struct {
+  int32_t src_gpu, n_dst;
+  uint64_t src_dptr, bytes;      /* bytes: multiple of 16                            */
+  int32_t dst_gpu[32];
+  sage_handle dst_alloc[32];
+  uint32_t flags;
+  int32_t path;                  /* out: SAGE_BCAST_PATH_*                            */
+} sage_bcast_desc;
+int sage_fanout_broadcast(sage_bcast_desc *d, const sage_handle *wait, int n_wait, sage_handle *end_ev);
 
 /* ---- function bodies (the COMPUTE node, functions.py:276) ----------------- */
 #define SAGE_BODY_TOUCH    0  /* read RO + input, write a digest (synthetic functions) */

@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
-SOURCES = ["core.cu", "pool.cu", "land.cu", "bodies.cu", "gemm_tc.cu", "spmv_csb.cu", "invoke.cu", "fixedgsl.cu", "segtab.cu", "conv_tc.cu", "resnet.cu"]
+SOURCES = ["core.cu", "pool.cu", "land.cu", "bodies.cu", "gemm_tc.cu", "spmv_csb.cu", "invoke.cu", "fixedgsl.cu", "segtab.cu", "conv_tc.cu", "resnet.cu", "fanout.cu"]
 
 
 def _run(cmd: list[str], log: Path | None = None) -> None:

@@ -140,6 +140,20 @@ class ConvDesc(C.Structure):
                 ("pad_", C.c_int32)]
 
 
+BCAST_P2P_ONLY, BCAST_PATH_P2P, BCAST_PATH_MULTICAST = 0x1, 0, 1
+
+
+class FanoutCaps(C.Structure):
+    _fields_ = [("n_gpus", C.c_int32), ("n_devices", C.c_int32), ("peer_mask", C.c_uint32 * 32),
+                ("multicast_attr", C.c_int32), ("multicast", C.c_int32), ("multicast_granularity", u64),
+                ("why", C.c_char * 160)]
+
+
+class BcastDesc(C.Structure):
+    _fields_ = [("src_gpu", C.c_int32), ("n_dst", C.c_int32), ("src_dptr", u64), ("bytes", u64),
+                ("dst_gpu", C.c_int32 * 32), ("dst_alloc", H * 32), ("flags", C.c_uint32), ("path", C.c_int32)]
+
+
 _SIGS = {
     "sage_init": (C.c_int, [C.c_int, u64, u64, u64, C.c_uint32]),
     "sage_shutdown": (C.c_int, []),
@@ -212,6 +226,8 @@ _SIGS = {
     "sage_mark": (C.c_int, [C.c_int, C.POINTER(H)]),
     "sage_event_elapsed": (C.c_int, [H, H, C.POINTER(C.c_double)]),
     "sage_conv": (C.c_int, [H, C.POINTER(ConvDesc)]),
+    "sage_fanout_caps": (C.c_int, [C.POINTER(FanoutCaps)]),
+    "sage_fanout_broadcast": (C.c_int, [C.POINTER(BcastDesc), C.POINTER(H), C.c_int, C.POINTER(H)]),
     "sage_net_create": (C.c_int, [C.POINTER(NetOp), C.c_int, C.POINTER(u64), C.c_int, C.POINTER(H), C.POINTER(u64)]),
     "sage_net_destroy": (C.c_int, [H]),
     "sage_share_create": (C.c_int, [C.c_int, C.c_uint32, i64, C.POINTER(i64), C.POINTER(H)]),

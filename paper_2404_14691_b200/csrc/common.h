@@ -189,6 +189,7 @@ void pool_threads_start(int n);
 void pool_threads_stop();
 
 // pool internals (pool.cu)
+int pool_alloc_phys(sage_handle h, CUmemGenericAllocationHandle *ph, uint64_t *phys, uint64_t *dptr, int *gpu);
 int pool_create(Gpu *g, uint64_t capacity);
 void pool_destroy(Gpu *g);
 

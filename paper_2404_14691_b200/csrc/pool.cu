@@ -457,6 +457,21 @@ int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes) {
 
 }  // extern "C"
 
+// the physical pages behind a pool allocation (multicast binding, fanout.cu)
+int sage::pool_alloc_phys(sage_handle h, CUmemGenericAllocationHandle *ph, uint64_t *phys, uint64_t *dptr, int *gpu) {
+  if (handle_kind(h) != Kind::Alloc) return fail(SAGE_EINVAL, "not a pool handle");
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  auto it = g_allocs.find(h & ((1ull << 56) - 1));
+  if (it == g_allocs.end()) return fail(SAGE_ESTATE, "unknown pool handle");
+  const Alloc *A = it->second;
+  if (A->account_only || !A->ph) return fail(SAGE_EINVAL, "allocation has no device pages");
+  *ph = A->ph;
+  *phys = A->phys;
+  *dptr = (uint64_t)A->va;
+  *gpu = A->gpu;
+  return SAGE_OK;
+}
+
 // ------------------------------------------------- cross-process sharing ----
 // The paper's memory daemon lands a function's read-only data once and the
 // per-function engines (separate processes) map it (PAPER.md:279-281,

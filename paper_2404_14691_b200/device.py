@@ -375,3 +375,29 @@ def instance_ctx_create(gpu: int, body: int) -> int:
 
 def instance_ctx_destroy(h: int) -> None:
     check(lib().sage_instance_ctx_destroy(h), "sage_instance_ctx_destroy")
+
+
+def fanout_caps() -> dict:
+    """The box's one-to-many options (sage_fanout_caps): peer reachability
+    per plane and whether an NVSwitch multicast object can be made."""
+    c = _lib.FanoutCaps()
+    check(lib().sage_fanout_caps(C.byref(c)), "sage_fanout_caps")
+    return {"n_gpus": c.n_gpus, "n_devices": c.n_devices, "peer_mask": [c.peer_mask[g] for g in range(c.n_gpus)],
+            "multicast_attr": bool(c.multicast_attr), "multicast": bool(c.multicast),
+            "multicast_granularity": c.multicast_granularity, "why": c.why.decode(errors="replace")}
+
+
+def fanout_broadcast(src_gpu: int, src_dptr: int, nbytes: int, dsts, p2p_only: bool = False,
+                     wait: Sequence[Event] = ()) -> tuple[str, Event]:
+    """Copy nbytes at src_dptr (on src_gpu) into every (gpu, Segment) of
+    `dsts`: one NVLS multicast pass when the box allows it, else peer copies.
+    Returns ("multicast" | "p2p", end event)."""
+    d = _lib.BcastDesc()
+    d.src_gpu, d.n_dst, d.src_dptr, d.bytes = src_gpu, len(dsts), src_dptr, nbytes
+    for i, (g, seg) in enumerate(dsts):
+        d.dst_gpu[i], d.dst_alloc[i] = g, seg.h
+    d.flags = _lib.BCAST_P2P_ONLY if p2p_only else 0
+    arr, n = _lib.handles([e.h for e in wait])
+    ev = H()
+    check(lib().sage_fanout_broadcast(C.byref(d), arr, n, C.byref(ev)), "sage_fanout_broadcast")
+    return ("multicast" if d.path == _lib.BCAST_PATH_MULTICAST else "p2p"), Event(ev.value)

@@ -289,6 +289,47 @@ class PeerFanout(BoxFanout):
             self.sent, self.received, self.bytes_out, self.bytes_in = stats
         return ok
 
+    def link_probe(self, gpu: int, nbytes: int = 256 << 20, iters: int = 5) -> dict:
+        """Collective NVLink measurement of the fan-out step itself: every
+        rank lands `nbytes` and publishes the pages; every rank then lands each
+        peer's pages `iters` times with the peer-reading `land` (identity
+        layout, checksum fused: exactly the receive side of a fan-out) and
+        times each with its device events.  Returns this rank's median GB/s
+        per peer (segment bytes / land time)."""
+        import numpy as np
+        mine = D.pool_alloc(gpu, nbytes, _lib.CLASS_READ_ONLY, unaccounted=True)
+        tmp = D.pool_alloc(gpu, nbytes, _lib.CLASS_WRITABLE, unaccounted=True)
+        stats = (self.sent, self.received, self.bytes_out, self.bytes_in)
+        sent, out = None, {}
+        try:
+            op = D.load(gpu, mine.dptr, np.full(nbytes, self.rank + 1, np.uint8))
+            op.wait()
+            sent = self.publish(gpu, mine.dptr, nbytes, op.end, seg_handle=mine.h, name=f"__probe_{self.rank}")
+            op.release()
+            for h in range(self.world):
+                if h == self.rank:
+                    continue
+                _, src, ev = self._fetch_from(h, gpu, f"__probe_{h}", nbytes)
+                ev.sync()
+                us = []
+                for _ in range(iters + 1):
+                    ld = D.load(gpu, tmp.dptr, None, None, device_src=src, device_src_bytes=nbytes, peer_gpu=gpu)
+                    info = ld.wait()
+                    us.append(info.gpu_end_us - info.gpu_begin_us)
+                    ld.release()
+                t = float(np.median(us[1:]))
+                out[h] = round(nbytes / (t * 1e-6) / 1e9, 1) if t > 0 else None
+        finally:
+            if self._barrier:
+                self._barrier()                  # peers are done reading `mine`
+            self.reap()
+            if sent is not None:
+                sent.release()
+            mine.free()
+            tmp.free()
+            self.sent, self.received, self.bytes_out, self.bytes_in = stats
+        return out
+
     def reap(self) -> None:
         """Unmap every received segment; call when no device work reads them
         (after the burst that landed them drained)."""
