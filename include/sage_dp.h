@@ -130,6 +130,9 @@ int sage_layout_create(const uint64_t *src_off, const uint64_t *dst_off, const u
 int sage_layout_destroy(sage_handle layout);
 /* number of land launches (chunks) a load of this layout takes */
 int sage_layout_chunks(sage_handle layout, uint32_t *n_chunks);
+/* the checksum a packed record will have once landed (host unpack + checksum):
+ * the registration-time content key of the deduplicating sharing manager    */
+int sage_layout_checksum(sage_handle layout, const void *packed, uint64_t packed_bytes, uint64_t *checksum);
 
 /* ---- events ---------------------------------------------------------------
  * Every asynchronous op returns an END event; stage begin/end times are read

@@ -179,6 +179,7 @@ _SIGS = {
                                      C.POINTER(H)]),
     "sage_layout_destroy": (C.c_int, [H]),
     "sage_layout_chunks": (C.c_int, [H, C.POINTER(C.c_uint32)]),
+    "sage_layout_checksum": (C.c_int, [H, C.c_void_p, u64, C.POINTER(u64)]),
     "sage_event_query": (C.c_int, [H]),
     "sage_event_sync": (C.c_int, [H]),
     "sage_event_time": (C.c_int, [H, C.POINTER(i64)]),

@@ -805,4 +805,19 @@ int sage_debug_emulate_land(sage_handle h, const void *packed, uint64_t packed_b
   return SAGE_OK;
 }
 
+// the content checksum the record WILL have once landed (host unpack +
+// checksum): a registration-time content key, so a function whose record is
+// identical to a resident one can map that segment instead of loading it
+int sage_layout_checksum(sage_handle h, const void *packed, uint64_t packed_bytes, uint64_t *checksum) {
+  Layout *L = layout_get(h);
+  if (!L || !packed || !checksum) return fail(SAGE_EINVAL, "layout_checksum: bad argument");
+  if (packed_bytes != L->packed) return fail(SAGE_EINVAL, "layout_checksum: packed size mismatch");
+  std::vector<uint8_t> seg(L->seg, 0);
+  const uint8_t *pk = static_cast<const uint8_t *>(packed);
+  for (const Tensor &T : L->t)
+    if (T.len) memcpy(seg.data() + T.dst, pk + T.src, T.len);
+  *checksum = host_checksum(seg.data(), L->seg, 0);
+  return SAGE_OK;
+}
+
 }  // extern "C"

@@ -340,6 +340,18 @@ class DataPlane:
             raise ValueError(f"function {name}: DB record size differs from its layout")
         self.data[name] = data
 
+    def content_key(self, spec: FunctionSpec) -> Optional[int]:
+        """The checksum the function's RO record has once landed (computed
+        once on the host by the library: sage_layout_checksum)."""
+        fd = self.data_for(spec)
+        key = fd.__dict__.get("_content_key")
+        if key is None and fd.layout.seg_bytes:
+            out = _lib.u64(0)
+            _lib.check(_lib.lib().sage_layout_checksum(fd.layout.handle(), fd.db.ctypes.data, fd.layout.packed_bytes,
+                                                       _lib.C.byref(out)), "sage_layout_checksum")
+            key = fd.__dict__["_content_key"] = out.value
+        return key
+
     def stage_sources_in_hbm(self, gpu: int = 0) -> None:
         """Copy every registered function's DB record and default input into
         HBM (runtime scratch, outside the ledger): loads then land from HBM
@@ -484,7 +496,9 @@ class DataPlane:
                     ro = self._ro_dst(run)
                 except SimulationError:
                     ro = 0
-        if pf.gpu_load_ro and fd.layout.seg_bytes:
+        if pf.gpu_load_ro and fd.layout.seg_bytes and resident is not None and resident.shares is not None:
+            run.ro_source = "dedup"   # identical content already landed on this GPU: mapped, not loaded
+        elif pf.gpu_load_ro and fd.layout.seg_bytes:
             if not ro:
                 raise SimulationError(f"{inv}: no read-only segment to land into")
             flags |= _lib.INV_RO
@@ -736,9 +750,12 @@ class DataPlane:
                 cpu_deps = [e for p in nodes[i_cpu].preds for e in ends[p]] if (i_cpu is not None and not serial) else []
                 wait = deps + cpu_deps
                 ro_end = None
-                if node.ro and fd.layout.seg_bytes:
+                borrowed = resident is not None and resident.shares is not None
+                if node.ro and fd.layout.seg_bytes and not borrowed:
                     ro_end = self._load_ro(run, fd, resident, wait, staged_ro)
                     ends[i].append(ro_end)
+                elif borrowed:
+                    run.ro_source = "dedup"      # identical content already landed: mapped, not loaded
                 if fd.input_bytes:
                     if fd.input_dev is not None and getattr(inv, "payload", None) is None:
                         op = D.load(gpu, in_dst, None, None, device_src=fd.input_dev.dptr,

@@ -286,10 +286,7 @@ class Simulation:
     def check_no_leaks(self) -> None:
         persistent = 0
         if self.sharing is not None:
-            for r in self.sharing.residents.values():
-                for alloc in (r.gpu_ro, r.gpu_ctx):
-                    if alloc is not None:
-                        persistent += alloc.effective
+            persistent += self.sharing.held_bytes()
         if isinstance(self.policy, PoolPolicy):
             for pool in self.policy.pools.values():
                 for slot in pool.contexts:
