@@ -64,6 +64,12 @@ constexpr int TC_BK = 32;         // fp32 elements per K-block = 128 bytes
 template <int BN>
 constexpr int tc_stages() { return BN >= 256 ? 4 : BN >= 128 ? 6 : 8; }
 constexpr int TC_THREADS = 192;
+// 3xTF32: eight converter warps (2..9) split each stage -- four could not keep
+// the tensor pipe fed (ncu: the split's smem loads dominated the stalls,
+// tensor pipe 13% active, profiles/r2_sgemm_x3_ncu.txt); warps 2..5 are the epilogue
+constexpr int TC_CONV_WARPS_X3 = 8;
+template <int X3>
+constexpr int tc_threads() { return X3 ? 64 + 32 * TC_CONV_WARPS_X3 : TC_THREADS; }
 
 template <int BN, int X3 = 0>
 struct TcSmem {
@@ -136,22 +142,22 @@ __device__ __forceinline__ uint32_t tf32_idesc() {
 // hi = x with the low 13 mantissa bits cleared (a TF32 value); lo = x - hi exactly
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// 3xTF32 split of one landed stage (X3 > 0): 128 epilogue threads, float4 granularity
-template <int X3>
+// 3xTF32 split of one landed stage (X3 > 0): NT converter threads, float4 granularity
+template <int X3, int NT>
 __device__ __forceinline__ void split_tile(uint8_t *raw, uint8_t *lo, int bytes, int t) {
   float4 *r4 = reinterpret_cast<float4 *>(raw), *l4 = reinterpret_cast<float4 *>(lo);
   constexpr int U = 4;
-  for (int i0 = t; i0 < bytes / 16; i0 += 128 * U) {
+  for (int i0 = t; i0 < bytes / 16; i0 += NT * U) {
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (i0 + u * 128 < bytes / 16) v[u] = r4[i0 + u * 128];
+      if (i0 + u * NT < bytes / 16) v[u] = r4[i0 + u * NT];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (i0 + u * 128 >= bytes / 16) break;
+      if (i0 + u * NT >= bytes / 16) break;
       const float4 h = make_float4(tf32_hi(v[u].x), tf32_hi(v[u].y), tf32_hi(v[u].z), tf32_hi(v[u].w));
-      l4[i0 + u * 128] = make_float4(v[u].x - h.x, v[u].y - h.y, v[u].z - h.z, v[u].w - h.w);
-      if constexpr (X3 == 2) r4[i0 + u * 128] = h;
+      l4[i0 + u * NT] = make_float4(v[u].x - h.x, v[u].y - h.y, v[u].z - h.z, v[u].w - h.w);
+      if constexpr (X3 == 2) r4[i0 + u * NT] = h;
     }
   }
 }
@@ -165,7 +171,7 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
 }
 
 template <int BN, bool MC = false, bool CR = false, int X3 = 0>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(tc_threads<X3>(), 1)
     sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
                       int M, int N, int K) {
   using S = TcSmem<BN, X3>;
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int s = 0; s < TC_STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], MC ? 2 : 1);   // MC: both CTAs' MMAs must release a slot
-        mbar_init(&conv[s], 4);
+        mbar_init(&conv[s], TC_CONV_WARPS_X3);
       }
       mbar_init(tmem_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -283,13 +289,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     if constexpr (X3 > 0) {
-      // ---- 3xTF32 split: warps 2..5 convert each landed stage ----
+      // ---- 3xTF32 split: warps 2..9 convert each landed stage ----
+      constexpr int NT = 32 * TC_CONV_WARPS_X3;
       const int t = threadIdx.x - 64;
       for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % TC_STAGES, round = kb / TC_STAGES;
         mbar_wait(&full[s], round & 1);
-        split_tile<X3>(sA + s * S::A_BYTES, sAl + s * S::A_BYTES, S::A_BYTES, t);
-        split_tile<X3>(sB + s * S::B_BYTES, sBl + s * S::B_BYTES, S::B_BYTES, t);
+        split_tile<X3, NT>(sA + s * S::A_BYTES, sAl + s * S::A_BYTES, S::A_BYTES, t);
+        split_tile<X3, NT>(sB + s * S::B_BYTES, sBl + s * S::B_BYTES, S::B_BYTES, t);
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -297,10 +304,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // ---- epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) ----
-    mbar_wait(tmem_full, 0);
+    if (warp < 6) mbar_wait(tmem_full, 0);
     if (warp == 2 && lane == 0) gemm_mark(5);
   }
-  if (warp >= 2) {
+  if (warp >= 2 && warp < 6) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int quad = warp & 3;
     const int row = m0 + quad * 32 + lane;
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (threadIdx.x == 64) gemm_mark(7);
     cluster_sync_all();    // every partial is in its CTA's smem
     if (threadIdx.x == 64) gemm_mark(8);
-    if (warp >= 2) {
+    if (warp >= 2 && warp < 6) {
       const int nz = (int)gridDim.z, rows = TC_BM / nz, t = threadIdx.x - 64;
       const int r0 = (int)blockIdx.z * rows;
       constexpr int U = 4;   // outputs per thread in flight, each summing up to 8 partials
@@ -460,7 +467,7 @@ static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float 
                                  TcSmem<BN, X3>::TOTAL));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(N / BN, M / TC_BM, split);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads<X3>());
   cfg.dynamicSmemBytes = TcSmem<BN, X3>::TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

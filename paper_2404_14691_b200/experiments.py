@@ -40,29 +40,40 @@ def _round(d):
 
 
 def cfg1(n: int = 16, reps: int = 5) -> dict:
+    """BASELINE cfg 1: n concurrent cold starts of one 100 MiB function.
+    SAGE vs DGSF (4 pre-created contexts) vs FixedGSL with a fresh context per
+    instance -- on a library thread, or in its own OS process -- alone (N=1)
+    and n at once."""
     spec, data = synthetic_function("fn100", 100, 10, 1, tensors=64)
     out = {}
-    for pol, r in (("SAGE", reps + 1), ("FixedGSL", 1)):
-        sim = Simulation(ClusterSpec(gpus=1), policy_preset(pol), {spec.name: spec}, seed=1,
+    rows = (("SAGE", "SAGE", "thread", n, reps + 1), ("DGSF", "DGSF", "thread", n, 3),
+            ("FixedGSL_thread_n1", "FixedGSL", "thread", 1, 4), ("FixedGSL", "FixedGSL", "thread", n, 2),
+            ("FixedGSL_process_n1", "FixedGSL", "process", 1, 4), ("FixedGSL_process", "FixedGSL", "process", n, 2))
+    for row, pol, mode, burst, r in rows:
+        sim = Simulation(ClusterSpec(gpus=1, instance_mode=mode), policy_preset(pol), {spec.name: spec}, seed=1,
                          function_data={spec.name: data})
         try:
             sim.prepare()
             samples = []
             for rep in range(r):
                 _evict_all(sim)
-                invs = sim.submit_many([spec.name] * n)
+                invs = sim.submit_many([spec.name] * burst)
                 sim.drain()
-                if rep >= (1 if r > 1 else 0):     # first SAGE burst warms the process
+                if rep >= (1 if r > 1 else 0):     # the first burst warms the process
                     samples += invs
             s = summarize_setup(samples)
             s["bursts"] = r - (1 if r > 1 else 0)
+            s["concurrent"] = burst
             if pol == "FixedGSL":
                 ctx = [i.stages[Stage.GPU_CTX][1] - i.stages[Stage.GPU_CTX][0] for i in samples]
                 s["fresh_context_ms_p50"] = percentile(ctx, 50) / 1e3
-            out[pol] = _round(s)
+            out[row] = _round(s)
         finally:
             sim.close()
-    out["p50_setup_ratio"] = round(out["FixedGSL"]["setup_p50_ms"] / out["SAGE"]["setup_p50_ms"], 1)
+    sage = out["SAGE"]["setup_p50_ms"]
+    out["p50_setup_ratio"] = round(out["FixedGSL"]["setup_p50_ms"] / sage, 1)
+    out["p50_setup_ratio_process"] = round(out["FixedGSL_process"]["setup_p50_ms"] / sage, 1)
+    out["p50_setup_ratio_dgsf"] = round(out["DGSF"]["setup_p50_ms"] / sage, 1)
     out["workload"] = f"{n} concurrent cold starts, 100 MiB RO (64 ragged tensors), 10 MiB writable, 1 MiB input"
     return out
 
