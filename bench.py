@@ -332,30 +332,40 @@ def gather_probe(data, iters: int = 20) -> dict | None:
             x.free()
 
 
-def land_probe(data, iters: int = 20) -> dict:
-    """Back-to-back lands of the largest RO segment from HBM, timed live."""
+def land_probe(data, iters: int = 8, gib: float = 1.0) -> dict:
+    """Back-to-back lands of a 1 GiB, 8-tensor segment (8x the L2) from an
+    HBM-resident record, timed live (the land kernel away from L2 effects)."""
+    import numpy as np
+
     from paper_2404_14691_b200 import _lib
     from paper_2404_14691_b200 import device as D
+    from paper_2404_14691_b200.layout import SegmentLayout
     L = _lib.lib()
-    name = max(data, key=lambda n: data[n].layout.seg_bytes)
-    fd = data[name]
-    seg = D.pool_alloc(0, fd.layout.seg_bytes, _lib.CLASS_READ_ONLY, unaccounted=True)
+    total = int(gib * (1 << 30)) // 4096 * 4096
+    lay = SegmentLayout.packed([total // 8 - 37 * k for k in range(8)], align=256)
+    db = np.random.default_rng(1).integers(0, 256, lay.packed_bytes, dtype=np.uint8)
+    src = D.pool_alloc(0, lay.packed_bytes + 64, _lib.CLASS_WRITABLE, unaccounted=True)
+    seg = D.pool_alloc(0, lay.seg_bytes, _lib.CLASS_READ_ONLY, unaccounted=True)
     try:
+        up = D.load(0, src.dptr, db, None)
+        up.wait()
+        up.release()
         _lib.check(L.sage_device_sync(0), "device_sync")
         _lib.check(L.sage_stats_reset(), "stats_reset")
-        ops = [D.load(0, seg.dptr, None, fd.layout, device_src=fd.db_dev.dptr,
-                      device_src_bytes=fd.layout.packed_bytes) for _ in range(iters)]
+        ops = [D.load(0, seg.dptr, None, lay, device_src=src.dptr, device_src_bytes=lay.packed_bytes)
+               for _ in range(iters)]
         sums = {op.wait().checksum for op in ops}
         for op in ops:
             op.release()
         if len(sums) != 1:
             raise RuntimeError("land probe: checksums differ between identical lands")
         s = kernel_stats()["land"]
-        s["segment"] = f"{name} ({fd.layout.seg_bytes} B, {fd.layout.n} tensors)"
-        s["d2d_GBps"] = d2d_reference(seg.dptr, fd.db_dev.dptr, min(fd.layout.packed_bytes, fd.layout.seg_bytes))
+        s["segment"] = f"synthetic ({lay.seg_bytes} B, {lay.n} ragged tensors, 8x L2)"
+        s["d2d_GBps"] = d2d_reference(seg.dptr, src.dptr, min(lay.packed_bytes, lay.seg_bytes))
         return s
     finally:
         seg.free()
+        src.free()
 
 
 def d2d_reference(dst: int, src: int, nbytes: int, iters: int = 20) -> float:
@@ -377,7 +387,7 @@ def d2d_reference(dst: int, src: int, nbytes: int, iters: int = 20) -> float:
     return round(2 * nbytes * iters / us.value / 1e3, 1)
 
 
-_TRAFFIC = {"spmv": "r1_spmv_traffic.json", "land": "r1_land_traffic.json"}
+_TRAFFIC = {"spmv": "r1_spmv_traffic.json", "land": "r2_land_traffic.json", "sgemm": "r2_sgemm_traffic.json"}
 
 
 def dominant_roofline(rooflines: dict, stats: dict, peaks: dict, isolated: dict | None = None,
@@ -409,6 +419,13 @@ def dominant_roofline(rooflines: dict, stats: dict, peaks: dict, isolated: dict 
         r["isolated"] = {"achieved": round(ach, 1), "frac": round(ach / r["peak"], 4), "avg_launch_us": round(us, 2),
                          "launches": isolated["launches"],
                          "how": "the same kernel back to back on one stream right after the timed region"}
+    ser = ncu_serialized(name)
+    if ser and stats[name]["launches"]:
+        per = stats[name]["work"] / stats[name]["launches"]
+        ach = per / (ser["mean_us"] * 1e-6) / (1e12 if r["unit"] == "TFLOP/s" else 1e9)
+        r["serialized"] = {"achieved": round(ach, 1), "frac": round(ach / r["peak"], 4), **ser,
+                           "how": "the same kernel's mean duration in the committed ncu launch list of this bench "
+                                  "(cold-cache, serialised launches), algorithmic work per launch as above"}
     if name == "spmv" and gather and nnz:
         # the limiter's own ceiling: x gathers per second vs the pure-gather rate
         ceil = gather["G_gathers_per_s"]
@@ -422,10 +439,41 @@ def dominant_roofline(rooflines: dict, stats: dict, peaks: dict, isolated: dict 
     return r
 
 
+_NCU_NAMES = {"spmv": "spmv4_kernel", "sgemm": "sgemm_tf32_kernel", "land": "land_kernel",
+              "stencil": "stencil4_kernel"}
+
+
+def ncu_serialized(name: str, path: str = "profiles/r2_bench_launches.csv") -> dict | None:
+    """Mean duration and share of `name`'s launches in a committed ncu launch
+    list of this bench (`ncu --metrics gpu__time_duration.sum --csv`)."""
+    import csv
+    import io
+    f = ROOT / path
+    if not f.exists() or name not in _NCU_NAMES:
+        return None
+    text = f.read_text()
+    if '"ID"' not in text:
+        return None
+    rows = list(csv.DictReader(io.StringIO(text[text.index('"ID"'):])))
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    mine, total = [], 0.0
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1e-3)
+        total += v
+        if _NCU_NAMES[name] in r["Kernel Name"]:
+            mine.append(v)
+    if not mine:
+        return None
+    return {"mean_us": round(sum(mine) / len(mine), 2), "launches": len(mine),
+            "share_of_kernel_time": round(sum(mine) / total, 3), "source": path}
+
+
 def land_traffic(segment: str):
     """DRAM bytes per launch of the probe's land from the committed ncu --set
-    full capture (profiles/r1_land_traffic.json), if it is the same segment."""
-    p = ROOT / "profiles" / "r1_land_traffic.json"
+    full capture (profiles/r2_land_traffic.json), if it is the same segment."""
+    p = ROOT / "profiles" / "r2_land_traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text())
@@ -794,7 +842,7 @@ def our_arm(args, rank, world, dist) -> dict:
                                       next((int(data[n].args[1]) for n in sorted(data) if data[n].body == "spmv"), 0)),
         "roofline_land": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
                           "unit": "GB/s", "frac": land["frac"], "traffic": land_traffic(probe["segment"]),
-                          "traffic_source": "profiles/r1_land_traffic.json (ncu --set full, one launch)",
+                          "traffic_source": "profiles/r2_land_traffic.json (ncu --set full, one 256 MiB launch)",
                           "peak_source": peaks["source"], "same_size_d2d_GBps": probe["d2d_GBps"],
                           "frac_of_same_size_d2d": round(land["achieved"] / probe["d2d_GBps"], 4),
                           "avg_launch_us": land["avg_launch_us"], "alg_bytes_per_launch": land["alg_bytes_per_launch"],
