@@ -18,7 +18,7 @@
 // context) as CUDA graphs whose kernels read their activation buffers from a
 // device-side FRAME {input, logits, workspace}.  An invocation then costs two
 // launches: a one-thread kernel writing its frame, and the graph.  Launches
-// of one executable graph serialise, so up to kInstances graphs (each with
+// of one executable graph serialise, so up to SAGE_NET_INSTANCES graphs (each with
 // its own frame) serve concurrent invocations; an instance is reused after
 // its previous run's completion event (device-side wait).
 // SAGE_NET_GRAPHS=0 launches the ops one by one with direct pointers.
@@ -141,7 +141,11 @@ __global__ void set_frame_kernel(uint64_t *frame, uint64_t input, uint64_t out, 
   }
 }
 
-constexpr int kInstances = 8;   // concurrent runs of one program over one segment
+// concurrent runs of one program over one segment (SAGE_NET_INSTANCES, default 16)
+static int instances() {
+  static const int n = [] { const char *e = getenv("SAGE_NET_INSTANCES"); return e ? std::max(1, atoi(e)) : 16; }();
+  return n;
+}
 
 struct GraphInst {
   cudaGraphExec_t exec = nullptr;
@@ -288,14 +292,14 @@ int net_run(const sage_body_desc *b, cudaStream_t s, int sms) {
   drv.CtxGetCurrent(&ctx);
   std::lock_guard<std::mutex> lk(net->mu);
   GraphSet &set = net->graphs[{b->ro, ctx}];
-  // an idle instance, else a new one (up to kInstances), else round robin
+  // an idle instance, else a new one (up to instances()), else round robin
   GraphInst *gi = nullptr;
   for (auto &x : set.inst)
     if (!x.used || cudaEventQuery(x.done) == cudaSuccess) {
       gi = &x;
       break;
     }
-  if (!gi && (int)set.inst.size() < kInstances) {
+  if (!gi && (int)set.inst.size() < instances()) {
     set.inst.emplace_back();
     gi = &set.inst.back();
     int rc = capture_instance(net, b->ro, sms, gi);
