@@ -61,6 +61,9 @@ int         sage_device_count(int *n);
 /* physical CUDA device of logical GPU `gpu` (device offset / shared planes applied) */
 int         sage_gpu_device(int gpu, int *dev);
 int64_t     sage_now_us(void);
+/* the clock's epoch on CLOCK_MONOTONIC (ns): a host reads the library clock
+ * without a call as (clock_gettime(CLOCK_MONOTONIC) - epoch_ns) / 1000       */
+int64_t     sage_clock_epoch_ns(void);
 /* host threads used for the CPU_LOAD memcpy fan-out (default 8) */
 int         sage_set_host_threads(int n);
 
@@ -520,6 +523,19 @@ int sage_share_preview(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, 
                        uint32_t fn_flags, sage_share_grant *g);                /* sharing.py:108-134 */
 int sage_share_admit(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
                      uint32_t fn_flags, int64_t now_us, sage_share_grant *g);  /* sharing.py:136-177 */
+/* preview + capacity check + admit in one call (policies.py:286-297 + the
+ * admit): the shared segments this admission would lead plus extra_bytes of
+ * private ones, rounded up to granularity as one request, must fit in
+ * avail_bytes (< 0: unlimited).  Refused: SAGE_ENOMEM, *g holds the preview,
+ * the table is unchanged (the caller demotes and calls sage_share_admit).
+ * opts SAGE_ADMIT_DEFER_RO_LEADER: an admission that would lead a new RO
+ * segment returns SAGE_ADMIT_DEFERRED (> 0) with the preview, table unchanged
+ * (content dedup: the caller looks for identical landed content first).     */
+#define SAGE_ADMIT_DEFER_RO_LEADER 0x1u
+#define SAGE_ADMIT_DEFERRED        1
+int sage_share_admit_within(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
+                            uint32_t fn_flags, int64_t now_us, int64_t avail_bytes, uint64_t extra_bytes,
+                            uint64_t granularity, uint32_t opts, sage_share_grant *g);
 /* attach the leader's stage END event to a token (ev != 0) or mark it ready  */
 int sage_share_token(sage_handle tab, uint64_t resident, int kind, sage_handle ev);
 int sage_share_token_ready(sage_handle tab, uint64_t resident, int kind, int *ready);

@@ -5,6 +5,7 @@ missing the import of `lib()` raises, and every data-plane call fails loudly.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import threading
@@ -92,6 +93,7 @@ class FixedGSLInfo(C.Structure):
 
 SHARE_RO, SHARE_CTX, SHARE_MULTI_STAGE = 0x1, 0x2, 0x4
 FN_HAS_RO = 0x1
+ADMIT_DEFER_RO_LEADER, ADMIT_DEFERRED = 0x1, 1
 TOKEN_RO, TOKEN_CTX = 0, 1
 STEP_CACHE_RO, STEP_FREE_RO, STEP_FREE_CTX, STEP_DROP_CACHE = 0x01, 0x02, 0x04, 0x08
 STEP_EVICT, STEP_GPU_FREED, STEP_ARM = 0x10, 0x20, 0x40
@@ -162,6 +164,7 @@ _SIGS = {
     "sage_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "sage_gpu_device": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "sage_now_us": (i64, []),
+    "sage_clock_epoch_ns": (i64, []),
     "sage_set_host_threads": (C.c_int, [C.c_int]),
     "sage_pool_configure": (C.c_int, [C.c_int, u64, u64]),
     "sage_pool_alloc": (C.c_int, [C.c_int, u64, C.c_int, C.POINTER(H), C.POINTER(u64), C.POINTER(u64)]),
@@ -235,6 +238,8 @@ _SIGS = {
     "sage_share_destroy": (C.c_int, [H]),
     "sage_share_preview": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, C.POINTER(ShareGrant)]),
     "sage_share_admit": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, i64, C.POINTER(ShareGrant)]),
+    "sage_share_admit_within": (C.c_int, [H, C.c_int32, C.c_int, u64, u64, C.c_uint32, i64, i64, u64, u64,
+                                          C.c_uint32, C.POINTER(ShareGrant)]),
     "sage_share_token": (C.c_int, [H, u64, C.c_int, H]),
     "sage_share_token_ready": (C.c_int, [H, u64, C.c_int, C.POINTER(C.c_int)]),
     "sage_share_release": (C.c_int, [H, C.c_int32, C.c_int, i64, C.POINTER(ShareStep)]),
@@ -292,11 +297,26 @@ def init(n_gpus: int = 1, pool_bytes: int = 0, staging_bytes: int = 0, chunk_byt
     check(L.sage_set_host_threads(host_threads or host_threads_default()), "sage_set_host_threads")
     check(L.sage_init(n_gpus, pool_bytes, staging_bytes, chunk_bytes, flags), "sage_init")
     _generation += 1
-    global _up
+    global _up, _exit_hook
     _up = True
+    if not _exit_hook:
+        atexit.register(_shutdown_at_exit)
+        _exit_hook = True
 
 
 _up = False
+_exit_hook = False
+
+
+def _shutdown_at_exit() -> None:
+    """A process that exits with the plane up (no Simulation.close) drains
+    the device and stops the native threads while the CUDA runtime is still
+    alive; Python's atexit runs before the C runtime's exit handlers."""
+    if _up:
+        try:
+            shutdown()
+        except Exception:   # noqa: BLE001 - best effort on the way out
+            pass
 
 
 def is_up() -> bool:

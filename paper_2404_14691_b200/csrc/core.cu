@@ -239,7 +239,10 @@ struct MemcpyPool {
   std::atomic<size_t> finished{0};
   uint64_t gen = 0;
   std::mutex job_mu;  // one job at a time
-} mp;
+};
+// never destroyed: workers parked on its condition variables at process exit
+// (no sage_shutdown) would otherwise block the static destructor / terminate
+MemcpyPool &mp = *new MemcpyPool;
 
 void memcpy_worker() {
   uint64_t seen = 0;
@@ -428,6 +431,7 @@ extern "C" {
 const char *sage_last_error(void) { return tl_err.c_str(); }
 int sage_abi_version(void) { return SAGE_ABI_VERSION; }
 int64_t sage_now_us(void) { return host_now_us(); }
+int64_t sage_clock_epoch_ns(void) { return g_epoch_ns; }
 
 // the physical CUDA device logical GPU g runs on (SAGE_DEVICE_OFFSET and
 // SAGE_INIT_SHARE_DEVICE applied): what a framework running a body on the

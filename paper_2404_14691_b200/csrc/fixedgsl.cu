@@ -191,7 +191,7 @@ static std::mutex g_job_mu;
 static std::unordered_map<uint64_t, Job *> g_jobs;
 static std::atomic<uint64_t> g_job_next{1};
 static std::mutex g_sem_mu;
-static std::condition_variable g_sem_cv;
+static std::condition_variable &g_sem_cv = *new std::condition_variable;   // never destroyed (exit with jobs parked)
 static int g_running = 0;
 static const int kMaxConcurrent = 32;
 

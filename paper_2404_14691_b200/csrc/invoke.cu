@@ -76,12 +76,14 @@ static std::atomic<uint64_t> g_inv_next{1};
 // completion order.
 namespace {
 std::mutex done_mu;
-std::condition_variable done_cv;
+// waitables a parked thread may still wait on at process exit live on the heap
+// and are never destroyed: glibc's pthread_cond_destroy blocks on waiters
+std::condition_variable &done_cv = *new std::condition_variable;
 std::deque<Inv *> done_q;          // device-complete, not yet resolved
 bool collector_stop = false;
 std::thread *collector = nullptr;   // never destroyed while joinable (exit without shutdown)
 std::mutex ready_mu;
-std::condition_variable ready_cv;
+std::condition_variable &ready_cv = *new std::condition_variable;
 std::deque<uint64_t> ready_q;      // resolved, not yet handed out
 }  // namespace
 
@@ -418,8 +420,8 @@ static int issue_notify(Inv *I) {
 
 namespace {
 std::mutex iss_mu;
-std::condition_variable iss_cv;       // work arrived / stop
-std::condition_variable iss_idle_cv;  // something was issued
+std::condition_variable &iss_cv = *new std::condition_variable;       // work arrived / stop
+std::condition_variable &iss_idle_cv = *new std::condition_variable;  // something was issued
 std::deque<Inv *> iss_q;              // submitted, not yet issued (submit order)
 std::deque<Inv *> iss_open;           // head issued, staged RO load still being enqueued
 int iss_busy = 0;                     // being issued right now

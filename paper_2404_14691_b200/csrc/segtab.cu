@@ -308,14 +308,8 @@ extern "C" int sage_share_preview(sage_handle tab, int32_t fn, int gpu, uint64_t
   return SAGE_OK;
 }
 
-extern "C" int sage_share_admit(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
-                                uint32_t fn_flags, int64_t now_us, sage_share_grant *g) {
-  TAB_OR_FAIL(T, tab);
-  if (!g || gpu < 0 || gpu >= T->n_gpus) return fail(SAGE_EINVAL, "share_admit: bad arguments");
-  const bool has_ro = fn_flags & SAGE_FN_HAS_RO;
-  auto it = T->by_key.find({fn, gpu});
-  Res *r = it == T->by_key.end() ? nullptr : it->second;
-  fill_grant(T, r, ro_bytes, ctx_bytes, has_ro, g);
+static void admit_locked(Table *T, Res *r, int32_t fn, int gpu, bool has_ro, int64_t now_us,
+                         sage_share_grant *g) {
   if (!r) {
     r = new Res();
     r->id = T->next_id++;
@@ -346,6 +340,43 @@ extern "C" int sage_share_admit(sage_handle tab, int32_t fn, int gpu, uint64_t r
   }
   if (has_ro && g->warmth != W_STAGE1_HOT) T->ro_loads[{fn, gpu}]++;
   g->resident = r->id;
+}
+
+extern "C" int sage_share_admit(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
+                                uint32_t fn_flags, int64_t now_us, sage_share_grant *g) {
+  TAB_OR_FAIL(T, tab);
+  if (!g || gpu < 0 || gpu >= T->n_gpus) return fail(SAGE_EINVAL, "share_admit: bad arguments");
+  const bool has_ro = fn_flags & SAGE_FN_HAS_RO;
+  auto it = T->by_key.find({fn, gpu});
+  Res *r = it == T->by_key.end() ? nullptr : it->second;
+  fill_grant(T, r, ro_bytes, ctx_bytes, has_ro, g);
+  admit_locked(T, r, fn, gpu, has_ro, now_us, g);
+  return SAGE_OK;
+}
+
+// preview + capacity check + admit under one lock: the admission's own
+// shared segments plus `extra_bytes` of private ones, rounded up to
+// `granularity` as one request, must fit in `avail_bytes` (< 0: unlimited).
+// Refused: SAGE_ENOMEM with the preview in *g and no state change.
+// SAGE_ADMIT_DEFER_RO_LEADER: an admission that would lead a new RO segment
+// returns SAGE_ADMIT_DEFERRED (> 0) with the preview instead (the caller looks
+// for identical content first).
+extern "C" int sage_share_admit_within(sage_handle tab, int32_t fn, int gpu, uint64_t ro_bytes, uint64_t ctx_bytes,
+                                       uint32_t fn_flags, int64_t now_us, int64_t avail_bytes, uint64_t extra_bytes,
+                                       uint64_t granularity, uint32_t opts, sage_share_grant *g) {
+  TAB_OR_FAIL(T, tab);
+  if (!g || gpu < 0 || gpu >= T->n_gpus) return fail(SAGE_EINVAL, "share_admit_within: bad arguments");
+  const bool has_ro = fn_flags & SAGE_FN_HAS_RO;
+  auto it = T->by_key.find({fn, gpu});
+  Res *r = it == T->by_key.end() ? nullptr : it->second;
+  fill_grant(T, r, ro_bytes, ctx_bytes, has_ro, g);
+  if ((opts & SAGE_ADMIT_DEFER_RO_LEADER) && g->alloc_ro) return SAGE_ADMIT_DEFERRED;
+  if (avail_bytes >= 0) {
+    uint64_t need = g->alloc_ro + g->alloc_ctx + extra_bytes;
+    if (granularity > 1) need = (need + granularity - 1) / granularity * granularity;
+    if (need > (uint64_t)avail_bytes) return SAGE_ENOMEM;   // not an error: tl_err untouched
+  }
+  admit_locked(T, r, fn, gpu, has_ro, now_us, g);
   return SAGE_OK;
 }
 

@@ -27,7 +27,7 @@ FixedGSL instances (fresh_context) run as native serial jobs instead.
 from __future__ import annotations
 
 from collections import deque
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Callable, Optional
 
 import numpy as np
@@ -172,6 +172,19 @@ def _plan_facts(plan: StagePlan) -> _PlanFacts:
     return pf
 
 
+def _desc_template(fd: "FunctionData", gpu: int) -> "_lib.InvokeDesc":
+    """A sage_invoke descriptor with this function's constant fields (GPU,
+    body template) filled in, built once per (function, GPU); each
+    invocation starts from a copy."""
+    memo = fd.__dict__.setdefault("_desc_tmpl", {})
+    d = memo.get(gpu)
+    if d is None:
+        d = memo[gpu] = _lib.InvokeDesc()
+        d.gpu = gpu
+        d.body = _body_template(fd)
+    return d
+
+
 def _body_template(fd: "FunctionData") -> "_lib.BodyDesc":
     """The function's COMPUTE descriptor without pointers, built once."""
     b = fd.__dict__.get("_body_tmpl")
@@ -185,27 +198,28 @@ def _body_template(fd: "FunctionData") -> "_lib.BodyDesc":
     return b
 
 
-@dataclass
 class _Run:
-    inv: object
-    plan: StagePlan
-    gpu: int
-    slot: Optional[D.Slot] = None
-    events: list = field(default_factory=list)      # every Event to release
-    loads: list = field(default_factory=list)       # (node idx, kind, LoadOp)
-    marks: dict = field(default_factory=dict)       # stage -> (begin src, end src)
-    hooks: dict = field(default_factory=dict)
-    pinned: list = field(default_factory=list)      # pinned buffers to return
-    scratch: list = field(default_factory=list)     # unaccounted device segments
-    result: Optional[D.PinnedBuffer] = None
-    out_bytes: int = 0
-    job: Optional[D.FixedGSLJob] = None
-    end: Optional[D.Event] = None
-    fd: Optional[FunctionData] = None
-    ro_source: str = ""
-    t_enqueue: int = 0
-    invh: int = 0              # native invocation (sage_invoke fast path)
-    keep: object = None        # host payload kept alive until completion
+    """One invocation's device-side state."""
+
+    __slots__ = ("inv", "plan", "gpu", "slot", "events", "loads", "marks", "hooks", "pinned", "scratch", "result",
+                 "out_bytes", "job", "end", "fd", "ro_source", "t_enqueue", "invh", "keep")
+
+    def __init__(self, inv, plan: StagePlan, gpu: int, hooks: dict, fd: Optional["FunctionData"] = None):
+        self.inv, self.plan, self.gpu, self.hooks, self.fd = inv, plan, gpu, hooks, fd
+        self.slot: Optional[D.Slot] = None
+        self.events: list = []        # every Event to release
+        self.loads: list = []         # (node idx, kind, LoadOp)
+        self.marks: dict = {}         # stage -> (begin src, end src)
+        self.pinned: list = []        # pinned buffers to return
+        self.scratch: list = []       # unaccounted device segments
+        self.result: Optional[D.PinnedBuffer] = None
+        self.out_bytes = 0
+        self.job: Optional[D.FixedGSLJob] = None
+        self.end: Optional[D.Event] = None
+        self.ro_source = ""
+        self.t_enqueue = 0
+        self.invh = 0                 # native invocation (sage_invoke fast path)
+        self.keep = None              # host payload kept alive until completion
 
 
 _STAGES = [Stage.CONTAINER, Stage.CPU_CTX, Stage.CPU_LOAD, Stage.GPU_CTX, Stage.GPU_LOAD, Stage.SYNC_WAIT,
@@ -289,6 +303,9 @@ class DataPlane:
         self.box = None               # fanout.BoxFanout: PCIe once per box across processes
         self._gate_q: dict[int, deque] = {}
         self._fast_source = False
+        # sage_invoke's four output handles, reused call after call (read at once)
+        self._inv_out = (_lib.H(), _lib.H(), _lib.H(), _lib.H())
+        self._inv_out_refs = tuple(_lib.C.byref(x) for x in self._inv_out)
 
     # ------------------------------------------------------- compute gate ----
     def _gate_wait(self, run: _Run) -> Optional[int]:
@@ -438,7 +455,7 @@ class DataPlane:
     def start(self, inv, plan: StagePlan, wait_tokens=(), hooks=None, fresh_context: bool = False) -> None:
         spec = inv.spec
         fd = self.data_for(spec)
-        run = _Run(inv=inv, plan=plan, gpu=inv.gpu, hooks=dict(hooks or {}), fd=fd)
+        run = _Run(inv, plan, inv.gpu, dict(hooks) if hooks else {}, fd)
         run.t_enqueue = self.sim.engine.tick()
         inv.run = run
         slot = getattr(inv, "ctx_slot", None)
@@ -472,8 +489,7 @@ class DataPlane:
     def _enqueue_fast(self, run: _Run, fd: FunctionData, wait_tokens) -> None:
         inv, plan, gpu = run.inv, run.plan, run.gpu
         pf = _plan_facts(plan)
-        d = _lib.InvokeDesc()
-        d.gpu = gpu
+        d = _lib.InvokeDesc.from_buffer_copy(_desc_template(fd, gpu))
         flags = 0
         if pf.cpu_ctx:
             t = self.sim.engine.tick()
@@ -575,8 +591,8 @@ class DataPlane:
             d.wait[n] = gate
             n += 1
         d.n_wait = n
-        # COMPUTE: the function's body template + this invocation's pointers
-        d.body = _body_template(fd)
+        # COMPUTE: the function's body template (in the desc template) + this
+        # invocation's pointers
         body = d.body
         body.ro, body.input, body.out = ro, in_dst, out_dst
         run.out_bytes = fd.out_bytes
@@ -590,9 +606,8 @@ class DataPlane:
             d.ret_dst = run.result.ptr
             flags |= _lib.INV_RET_HOST
         d.flags = flags
-        h, done, ro_end, ctx_end = _lib.H(), _lib.H(), _lib.H(), _lib.H()
-        _lib.check(_lib.lib().sage_invoke(_lib.C.byref(d), _lib.C.byref(h), _lib.C.byref(done), _lib.C.byref(ro_end),
-                                          _lib.C.byref(ctx_end)), "sage_invoke")
+        h, done, ro_end, ctx_end = self._inv_out
+        _lib.check(_lib.lib().sage_invoke(_lib.C.byref(d), *self._inv_out_refs), "sage_invoke")
         run.invh = h.value
         run.end = _Borrowed(done.value)
         self._gate_push(run)

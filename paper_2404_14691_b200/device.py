@@ -8,6 +8,7 @@ pool's SAGE_ENOMEM into the reference's `Denied` value
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -55,8 +56,16 @@ def poll(events: Sequence[Event], timeout_us: int = 0) -> list[bool]:
     return [bool(d) for d in done]
 
 
+_clock = [-1, 0]   # [library generation, epoch ns]
+
+
 def now_us() -> int:
-    return int(lib().sage_now_us())
+    """The library clock (sage_now_us) read in Python: CLOCK_MONOTONIC minus
+    the epoch sage_init set (re-read once per init)."""
+    c = _clock
+    if c[0] != _lib._generation:
+        c[0], c[1] = _lib._generation, int(lib().sage_clock_epoch_ns())
+    return (time.monotonic_ns() - c[1]) // 1000
 
 
 # ---------------------------------------------------------------- pool ------

@@ -234,11 +234,13 @@ class Simulation:
                          stage_hooks=None, fresh_context: bool = False) -> None:
         inv.start_us = self.engine.tick()
         inv.warmth = warmth
-        for n in plan.nodes:
-            if n.stage is Stage.CPU_LOAD:
-                inv.host_bytes_umb += n.bytes_umb
-            elif n.stage is Stage.GPU_LOAD:
-                inv.pcie_bytes_umb += n.bytes_umb
+        moved = plan.__dict__.get("_moved")
+        if moved is None:   # (host, PCIe) bytes the plan moves, once per (immutable) plan
+            moved = plan.__dict__["_moved"] = (
+                sum(n.bytes_umb for n in plan.nodes if n.stage is Stage.CPU_LOAD),
+                sum(n.bytes_umb for n in plan.nodes if n.stage is Stage.GPU_LOAD))
+        inv.host_bytes_umb += moved[0]
+        inv.pcie_bytes_umb += moved[1]
         self._in_flight += 1
         self.dataplane.start(inv, plan, wait_tokens, stage_hooks, fresh_context=fresh_context)
 

@@ -28,20 +28,39 @@ def timed_invoke(*a):
 
 
 L.sage_invoke = timed_invoke
+
+
+def wrap(obj, name, key):
+    orig_fn = getattr(obj, name)
+
+    def w(*a, **k):
+        t = time.perf_counter()
+        r = orig_fn(*a, **k)
+        acc[key] = acc.get(key, 0.0) + time.perf_counter() - t
+        return r
+    setattr(obj, name, w)
+
+
+wrap(sim.policy, "_try_start", "try_start")
+wrap(sim, "start_invocation", "start_inv")
+wrap(sim.dataplane, "_enqueue_fast", "enqueue_fast")
+wrap(sim.sharing, "preview", "preview")
+wrap(sim.sharing, "admit", "admit")
 for stats in (0, 1):
     L.sage_stats_enable(stats)
     for rep in range(8):
         for r in list(sim.sharing.residents.values()):
             sim.sharing.evict(r)
-        acc["invoke"] = 0.0
-        acc["n"] = 0
+        for k in list(acc):
+            acc[k] = 0.0 if k != "n" else 0
         t0 = time.perf_counter()
         sim.submit_many(names)
         t1 = time.perf_counter()
         sim.drain()
         t2 = time.perf_counter()
     print(f"stats={stats}: submit {1e6*(t1-t0)/64:.1f} us/inv, of which sage_invoke {1e6*acc['invoke']/acc['n']:.1f} us; "
-          f"burst total {1e3*(t2-t0):.2f} ms")
+          f"burst total {1e3*(t2-t0):.2f} ms; per inv: " +
+          ", ".join(f"{k} {1e6*v/64:.1f}" for k, v in acc.items() if k not in ("n", "invoke")))
 sim.close()
 
 # ---- where the host time goes (cProfile over 4 bursts, stats off) ----------
