@@ -667,8 +667,9 @@ def our_arm(args, rank, world, dist) -> dict:
 
     table, data = cfg2_functions()
     names = burst_names(table, args.burst)
-    sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), table, seed=1, function_data=data,
-                     copy_results=False)
+    cc = args.compute_concurrency or None
+    sim = Simulation(ClusterSpec(gpus=1, compute_concurrency=cc), policy_preset("SAGE"), table, seed=1,
+                     function_data=data, copy_results=False)
     box = None
     fanout_note = None
     if world > 1 and args.fanout != "none":
@@ -814,7 +815,7 @@ def our_arm(args, rank, world, dist) -> dict:
         "warmup": args.warmup, "ms_per_step": round(val_us / 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "fp32 (bodies; sgemm as 3xTF32 on tcgen05, FP32-accurate) / u8 (land)", "data": "synthetic",
-        "config": workload_config(per_step, world),
+        "config": workload_config(per_step, world, args.compute_concurrency),
         "setup_p50_ms": round(percentile(setups_val, 50) / 1e3, 3),
         "setup_p99_ms": round(percentile(setups_val, 99) / 1e3, 3),
         "step_ms": val_steps,
@@ -872,13 +873,16 @@ def our_arm(args, rank, world, dist) -> dict:
     return line
 
 
-def workload_config(burst: int, world: int) -> dict:
+def workload_config(burst: int, world: int, cc: int = 0) -> dict:
     """The `config` both arms report (the reference arm times a bounded
     sample of the same workload, described in its cpu_baseline.sample)."""
-    return {"workload": f"cfg2: burst of {burst} concurrent invocations (sgemm/stencil/spmv uniform "
-                        f"mix, shared RO segments, cold start per burst) per GPU",
-            "policy": "SAGE", "burst": burst, "gpus": world,
-            "l2": "inputs larger than L2 (212 MiB RO + 504 MiB inputs per step)"}
+    c = {"workload": f"cfg2: burst of {burst} concurrent invocations (sgemm/stencil/spmv uniform "
+                     f"mix, shared RO segments, cold start per burst) per GPU",
+         "policy": "SAGE", "burst": burst, "gpus": world,
+         "l2": "inputs larger than L2 (212 MiB RO + 504 MiB inputs per step)"}
+    if cc:
+        c["compute_concurrency"] = cc
+    return c
 
 
 def reference_arm(args, rank, world) -> dict:
@@ -921,6 +925,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--burst", type=int, default=64)
     ap.add_argument("--no-cfg1", action="store_true")
+    ap.add_argument("--compute-concurrency", type=int, default=0,
+                    help="ComputeGate slots per GPU (functions.py:304-327; 0 = no gate)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fanout", choices=["p2p", "nccl", "none"], default="p2p",
                     help="N>1: how non-home ranks get a segment (peer land of the home's pages / ncclBroadcast / "

@@ -69,12 +69,12 @@ constexpr int TC_THREADS = 192;
 // tensor pipe 13% active, profiles/r2_sgemm_x3_ncu.txt); warps 2..5 are the epilogue
 constexpr int TC_CONV_WARPS_X3 = 8;
 template <int X3>
-constexpr int tc_threads() { return X3 ? 64 + 32 * TC_CONV_WARPS_X3 : TC_THREADS; }
+__host__ __device__ constexpr int tc_threads() { return X3 ? 64 + 32 * TC_CONV_WARPS_X3 : TC_THREADS; }
 
-template <int BN, int X3 = 0>
+template <int BN, int X3 = 0, bool PAIR = false>
 struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
-  static constexpr int B_BYTES = BN * TC_BK * 4;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * TC_BK * 4;   // PAIR: this CTA's half of B
   static constexpr int RAW = A_BYTES + B_BYTES;
   static constexpr int STAGE = X3 ? 2 * RAW : RAW;     // 3xTF32: + lo copies of both tiles
   static constexpr int STAGES = X3 ? (192 * 1024) / STAGE : tc_stages<BN>();
@@ -100,6 +100,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+// a barrier other CTAs of the cluster arrive on (release.cluster)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// arrive on the barrier at the same smem offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
                                                uint16_t mask) {
@@ -130,13 +146,13 @@ __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
   return d;
 }
 // instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = BN
-template <int BN>
+template <int BN, int UM = TC_BM>
 __device__ __forceinline__ uint32_t tf32_idesc() {
   return (1u << 4)                 // c_format = F32
          | (2u << 7)               // a_format = TF32
          | (2u << 10)              // b_format = TF32
          | ((uint32_t)(BN >> 3) << 17)
-         | ((uint32_t)(TC_BM >> 4) << 24);
+         | ((uint32_t)(UM >> 4) << 24);
 }
 
 // hi = x with the low 13 mantissa bits cleared (a TF32 value); lo = x - hi exactly
@@ -170,11 +186,32 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-template <int BN, bool MC = false, bool CR = false, int X3 = 0>
+// CTA pair (PAIR): one M = 256 MMA across the two SMs of a TPC; the leader
+// issues it, reading A rows [0,128) + B rows [0,BN/2) from its smem and the
+// peer's A rows [128,256) + B rows [BN/2,BN) from the peer's (same offsets)
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// PAIR: CTAs (2j, 2j+1) of a cluster -- adjacent along x, where the driver
+// forms pairs for a cta_group::2 kernel -- own M tiles 2j, 2j+1 of one 256-row
+// pair tile.  Each loads its A rows and its HALF of B (BN/2 rows) with its
+// own TMA + full barrier, and (3xTF32) splits its own stage; the converters
+// of both CTAs arrive on the LEADER's conv barrier (count 2 x warps), the
+// leader issues tcgen05.mma.cta_group::2 (M = 256, N = BN) and commits to
+// the empty / tmem_full barriers of both CTAs (multicast).  Per SM: half of
+// B's smem, TMA and split traffic, so a 3xTF32 stage is 64 KB and the ring
+// holds 3 stages instead of 2.  Each CTA's TMEM holds its 128 rows.
+template <int BN, bool MC = false, bool CR = false, int X3 = 0, bool PAIR = false>
 __global__ void __launch_bounds__(tc_threads<X3>(), 1)
     sgemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
                       int M, int N, int K) {
-  using S = TcSmem<BN, X3>;
+  static_assert(!(PAIR && MC), "PAIR and B-multicast clusters are exclusive");
+  using S = TcSmem<BN, X3, PAIR>;
   constexpr int TC_STAGES = S::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -190,14 +227,17 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) gemm_mark(0);
-  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+  // PAIR: M tiles along x (the driver forms CTA pairs along the cluster's x)
+  const int m0 = (PAIR ? blockIdx.x : blockIdx.y) * TC_BM, n0 = (PAIR ? blockIdx.y : blockIdx.x) * BN;
   // split-K: CTA z covers K-blocks [z*kblocks, (z+1)*kblocks) and adds its
   // partial tile into C (zeroed by the host) with vector reductions
   const int kblocks = K / TC_BK / gridDim.z;
   const int kb0 = blockIdx.z * kblocks;
   const bool split = gridDim.z > 1;
   uint32_t crank = 0;
-  if constexpr (MC) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  if constexpr (MC || PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const uint32_t prank = PAIR ? (crank & 1u) : 0u;   // 0: pair leader (issues the MMAs)
+  const uint32_t leader_rank = crank & ~1u;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -208,20 +248,26 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
       for (int s = 0; s < TC_STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], MC ? 2 : 1);   // MC: both CTAs' MMAs must release a slot
-        mbar_init(&conv[s], TC_CONV_WARPS_X3);
+        mbar_init(&conv[s], PAIR ? 2 * TC_CONV_WARPS_X3 : TC_CONV_WARPS_X3);   // PAIR: both CTAs' converters
       }
       mbar_init(tmem_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
     // TMEM: BN fp32 columns x 128 lanes for the accumulator
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN < 32 ? 32 : BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {   // both CTAs' warp 1, same smem slot
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if constexpr (MC) cluster_sync_all();   // the peer's barriers exist before any multicast lands
+  if constexpr (MC || PAIR) cluster_sync_all();   // the peer's barriers exist before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) gemm_mark(1);
@@ -238,16 +284,17 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
           tma_load_2d_mc(sB + s * S::B_BYTES + crank * (S::B_BYTES / 2), &mapB, &full[s], (kb0 + kb) * TC_BK,
                          n0 + (int)crank * (BN / 2), (uint16_t)0x3);
         else
-          tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], (kb0 + kb) * TC_BK, n0);
+          tma_load_2d(sB + s * S::B_BYTES, &mapB, &full[s], (kb0 + kb) * TC_BK, n0 + (int)prank * (BN / 2));
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer (single thread) ----
-      const uint32_t idesc = tf32_idesc<BN>();
+    if (lane == 0 && prank == 0) {
+      // ---- MMA issuer (single thread; PAIR: the leader CTA's only) ----
+      const uint32_t idesc = tf32_idesc<BN, PAIR ? 2 * TC_BM : TC_BM>();
       for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % TC_STAGES, round = kb / TC_STAGES;
-        mbar_wait(X3 ? &conv[s] : &full[s], round & 1);
+        if constexpr (PAIR) mbar_wait_cluster(&conv[s], round & 1);
+        else mbar_wait(X3 ? &conv[s] : &full[s], round & 1);
         if (kb == 0) gemm_mark(2);
         if (kb == kblocks / 2) gemm_mark(3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -260,18 +307,30 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
           // advance 32 B (8 tf32) along K inside the 128-B swizzle row: +2 in 16-B units
           const uint64_t a = da + (uint64_t)(2 * k), b = db + (uint64_t)(2 * k);
           const uint32_t acc = (kb | k) ? 1u : 0u;
-          if constexpr (X3) {
+          if constexpr (X3 && PAIR) {
+            mma_tf32_pair(tmem, dal + (uint64_t)(2 * k), b, idesc, acc);
+            mma_tf32_pair(tmem, a, dbl + (uint64_t)(2 * k), idesc, 1u);
+            mma_tf32_pair(tmem, a, b, idesc, 1u);
+          } else if constexpr (X3) {
             // correction terms first (smallest magnitudes), then hi.hi
             mma_tf32(tmem, dal + (uint64_t)(2 * k), b, idesc, acc);
             mma_tf32(tmem, a, dbl + (uint64_t)(2 * k), idesc, 1u);
             mma_tf32(tmem, a, b, idesc, 1u);
+          } else if constexpr (PAIR) {
+            mma_tf32_pair(tmem, a, b, idesc, acc);
           } else {
             mma_tf32(tmem, a, b, idesc, acc);
           }
         }
         // free the smem slot once these MMAs have read it (MC: in both CTAs,
         // whose producers both write into it)
-        if constexpr (MC)
+        if constexpr (PAIR)
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[s])),
+              "h"((uint16_t)(0x3u << leader_rank))
+              : "memory");
+        else if constexpr (MC)
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                   smem_u32(&empty[s])),
@@ -283,9 +342,16 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
                        : "memory");
       }
       gemm_mark(4);
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(tmem_full))
-                   : "memory");
+      if constexpr (PAIR)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(tmem_full)),
+            "h"((uint16_t)(0x3u << leader_rank))
+            : "memory");
+      else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(tmem_full))
+                     : "memory");
     }
   } else {
     if constexpr (X3 > 0) {
@@ -298,9 +364,13 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
         split_tile<X3, NT>(sA + s * S::A_BYTES, sAl + s * S::A_BYTES, S::A_BYTES, t);
         split_tile<X3, NT>(sB + s * S::B_BYTES, sBl + s * S::B_BYTES, S::B_BYTES, t);
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if constexpr (PAIR) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+        else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_remote(&conv[s], leader_rank);   // the leader's MMA reads both halves
+          else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+        }
       }
     }
     // ---- epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) ----
@@ -360,11 +430,13 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
     if (threadIdx.x == 64) gemm_mark(7);
     cluster_sync_all();    // every partial is in its CTA's smem
     if (threadIdx.x == 64) gemm_mark(8);
-    if (warp >= 2 && warp < 6) {
-      const int nz = (int)gridDim.z, rows = TC_BM / nz, t = threadIdx.x - 64;
+    {
+      // every warp of the CTA (the producer, MMA and converter warps are idle now)
+      constexpr int NT = tc_threads<X3>();
+      const int nz = (int)gridDim.z, rows = TC_BM / nz, t = threadIdx.x;
       const int r0 = (int)blockIdx.z * rows;
       constexpr int U = 4;   // outputs per thread in flight, each summing up to 8 partials
-      for (int f0 = t; f0 < rows * (BN / 4); f0 += 128 * U) {
+      for (int f0 = t; f0 < rows * (BN / 4); f0 += NT * U) {
         float4 acc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -374,11 +446,12 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
           float4 v[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {   // independent remote loads, issued back to back
-            const int f = f0 + u * 128;
+            const int f = f0 + u * NT;
             const int row = r0 + f / (BN / 4), c4 = f % (BN / 4);
             const uint32_t la = smem_u32(smem + (size_t)row * (BN * 4 + 16) + c4 * 16);
             uint32_t ra;
-            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(q));
+            // split-K peers: cluster rank q (PAIR: the same pair slot of pair q)
+            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(PAIR ? prank + 2u * q : (uint32_t)q));
             if (f < rows * (BN / 4))
               asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                            : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
@@ -393,7 +466,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int f = f0 + u * 128;
+          const int f = f0 + u * NT;
           const int row = r0 + f / (BN / 4), c4 = f % (BN / 4);
           if (f < rows * (BN / 4) && m0 + row < M)
             *reinterpret_cast<float4 *>(C + (size_t)(m0 + row) * N + n0 + 4 * c4) = acc[u];
@@ -406,9 +479,13 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) gemm_mark(6);
+  if constexpr (PAIR) cluster_sync_all();   // both CTAs are done with the pair's TMEM
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
   }
   // MC: the peer may still signal this CTA's empty barriers / land multicast
   // bytes in its smem until it is done; neither CTA exits before both are
@@ -458,38 +535,47 @@ static bool sgemm_mc_enabled() {
   return on;
 }
 
-template <int BN, bool MC, bool CR, int X3>
+template <int BN, bool MC, bool CR, int X3, bool PAIR = false>
 static int launch_tc_kernel(const CUtensorMap &ma, const CUtensorMap &mb, float *C, int M, int N, int K, int split,
                             cudaStream_t s) {
+  using S = TcSmem<BN, X3, PAIR>;
+  auto kern = sgemm_tf32_kernel<BN, MC, CR, X3, PAIR>;
   // the smem opt-in is per device and context (FixedGSL instances launch from
   // fresh contexts): cheap, so set it on every launch
-  SAGE_CUDA(cudaFuncSetAttribute(sgemm_tf32_kernel<BN, MC, CR, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TcSmem<BN, X3>::TOTAL));
+  SAGE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(N / BN, M / TC_BM, split);
+  cfg.gridDim = PAIR ? dim3(M / TC_BM, N / BN, split) : dim3(N / BN, M / TC_BM, split);
   cfg.blockDim = dim3(tc_threads<X3>());
-  cfg.dynamicSmemBytes = TcSmem<BN, X3>::TOTAL;
+  cfg.dynamicSmemBytes = S::TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  if (MC || CR) {
+  if (MC || CR || PAIR) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
     attr[0].val.clusterDim.y = MC ? 2 : 1;
     attr[0].val.clusterDim.z = CR ? split : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  SAGE_CUDA(cudaLaunchKernelEx(&cfg, sgemm_tf32_kernel<BN, MC, CR, X3>, ma, mb, C, M, N, K));
+  SAGE_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, C, M, N, K));
   return SAGE_OK;
+}
+
+// SAGE_SGEMM_PAIR=1 (opt-in): the CTA-pair (cta_group::2) 3xTF32 kernel.
+// Off by default: on the cfg-2 shape its K loop takes as long as the 1-CTA
+// kernel's (36.4 vs 36.6 us -- both issue the tensor pipe at the TF32 rate,
+// 1.14 us per 3-pass K-block), and clusters of 2 x split = 8 CTAs at ~198 KB
+// of smem do not all co-schedule in one wave (tools/call_pair.sh phase trace:
+// the last clusters start 48 us late), so the kernel takes 2x as long
+static bool sgemm_pair_enabled() {
+  static const bool on = [] { const char *e = getenv("SAGE_SGEMM_PAIR"); return e && atoi(e) != 0; }();
+  return on;
 }
 
 template <int BN, int X3>
 static int launch_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
   // 2-CTA clusters along M when the M tiles pair up
   const bool mc = sgemm_mc_enabled() && (M / TC_BM) % 2 == 0;
-  CUtensorMap ma, mb;
-  SAGE_TRY(encode_kmajor(&ma, A, (uint64_t)M, (uint64_t)K, TC_BM));
-  SAGE_TRY(encode_kmajor(&mb, BT, (uint64_t)N, (uint64_t)K, mc ? BN / 2 : BN));
   // split K so the grid covers the SMs: a skinny GEMM (N <= 256) has only
   // M/128 full-width tiles; splitting K keeps every A element read once
   int dev = 0;
@@ -502,10 +588,26 @@ static int launch_tc(const float *A, const float *BT, float *C, int M, int N, in
   // unless disabled (SAGE_SGEMM_CR=0) or B-multicast clusters are requested
   static const bool cr_on = [] { const char *e = getenv("SAGE_SGEMM_CR"); return !(e && atoi(e) == 0); }();
   const bool cr = cr_on && !mc && split > 1 && split <= 8 && TC_BM % split == 0;
+  // CTA pairs: 3xTF32 at BN = 256, M tiles pairing up, cluster (1, 2, split) within the portable 8
+  const bool pair = X3 == 1 && BN == 256 && !mc && sgemm_pair_enabled() && (M / TC_BM) % 2 == 0 &&
+                    2 * (cr ? split : 1) <= 8;
+  CUtensorMap ma, mb;
+  SAGE_TRY(encode_kmajor(&ma, A, (uint64_t)M, (uint64_t)K, TC_BM));
+  SAGE_TRY(encode_kmajor(&mb, BT, (uint64_t)N, (uint64_t)K, (mc || pair) ? BN / 2 : BN));
   if (split > 1 && !cr) SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
-  const int rc = mc ? launch_tc_kernel<BN, true, false, X3>(ma, mb, C, M, N, K, split, s)
-                 : cr ? launch_tc_kernel<BN, false, true, X3>(ma, mb, C, M, N, K, split, s)
-                      : launch_tc_kernel<BN, false, false, X3>(ma, mb, C, M, N, K, split, s);
+  int rc;
+  if constexpr (X3 == 1 && BN == 256) {
+    if (pair) {
+      rc = cr ? launch_tc_kernel<BN, false, true, X3, true>(ma, mb, C, M, N, K, split, s)
+              : launch_tc_kernel<BN, false, false, X3, true>(ma, mb, C, M, N, K, split, s);
+      if (rc != SAGE_OK) return rc;
+      SAGE_CUDA(cudaGetLastError());
+      return SAGE_OK;
+    }
+  }
+  rc = mc ? launch_tc_kernel<BN, true, false, X3>(ma, mb, C, M, N, K, split, s)
+       : cr ? launch_tc_kernel<BN, false, true, X3>(ma, mb, C, M, N, K, split, s)
+            : launch_tc_kernel<BN, false, false, X3>(ma, mb, C, M, N, K, split, s);
   if (rc != SAGE_OK) return rc;
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
@@ -548,6 +650,10 @@ int sgemm_tc(const float *A, const float *BT, float *C, int M, int N, int K, cud
 template <int X3>
 static int touch_x() {
   cudaFuncAttributes a;
+  if constexpr (X3 == 1) {
+    SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, true, X3, true>));
+    SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, false, X3, true>));
+  }
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, true, X3>));
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, false, X3>));
   SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<128, false, true, X3>));

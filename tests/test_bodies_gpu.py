@@ -36,7 +36,7 @@ def run_body(kind, ro, ro_bytes, inp, inp_bytes, out_bytes, args):
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 64, 32), (256, 128, 256), (512, 256, 4096), (4096, 256, 4096),
-                                   (1024, 192, 96)])
+                                   (1024, 192, 96), (384, 256, 512), (1024, 256, 1024)])
 def test_sgemm_tcgen05_fp32(dp, m, n, k):
     rng = np.random.default_rng(m + n + k)
     A = rng.standard_normal((m, k), dtype=np.float32)

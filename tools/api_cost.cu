@@ -59,6 +59,38 @@ int main() {
   MEASURE("cudaMemcpyAsync D2H 4KiB", cudaMemcpyAsync(hp, d, 4096, cudaMemcpyDeviceToHost, s));
   MEASURE("cudaMemcpyAsync D2D 4KiB", cudaMemcpyAsync(d + 4096, d, 4096, cudaMemcpyDeviceToDevice, s));
   MEASURE("cudaLaunchHostFunc", cudaLaunchHostFunc(s, [](void *) {}, nullptr));
+  MEASURE("cudaFuncSetAttribute (smem 198K)",
+          cudaFuncSetAttribute(noop, cudaFuncAttributeMaxDynamicSharedMemorySize, 198 * 1024));
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 32, 4);
+    cfg.blockDim = dim3(320);
+    cfg.dynamicSmemBytes = 198 * 1024;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 4;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MEASURE("cudaLaunchKernelEx cluster4 198K", cudaLaunchKernelEx(&cfg, noop, d));
+    cudaDeviceSynchronize();
+    // device time per launch of back-to-back cluster launches
+    cudaEventRecord(ev[0], s);
+    for (int i = 0; i < 200; ++i) cudaLaunchKernelEx(&cfg, noop, d);
+    cudaEventRecord(ev[1], s);
+    cudaEventSynchronize(ev[1]);
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    printf("%-34s %8.3f us\n", "device: cluster4 198K noop each", ms * 1e3 / 200);
+    cfg.numAttrs = 0;
+    cudaEventRecord(ev[0], s);
+    for (int i = 0; i < 200; ++i) cudaLaunchKernelEx(&cfg, noop, d);
+    cudaEventRecord(ev[1], s);
+    cudaEventSynchronize(ev[1]);
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    printf("%-34s %8.3f us\n", "device: 198K noop (no cluster) each", ms * 1e3 / 200);
+  }
   // globaltimer vs host clock: resolution and offset stability
   cudaDeviceSynchronize();
   for (int k = 0; k < 5; ++k) {

@@ -27,7 +27,9 @@ out = D.pool_alloc(0, m * n * 4, _lib.CLASS_WRITABLE)
 slot = D.Slot(0)
 body = D.body_desc(_lib.BODY_SGEMM, ro=segs[0].dptr, ro_bytes=A.nbytes, inp=segs[1].dptr, inp_bytes=BT.nbytes,
                    out=out.dptr, out_bytes=m * n * 4, args=(m, n, k))
+t0 = time.perf_counter()
 evs = [slot.launch(body) for _ in range(iters)]
+host_us = (time.perf_counter() - t0) / iters * 1e6
 evs[-1][1].sync()
 us = []
 for b, e in evs[2:]:
@@ -36,5 +38,5 @@ for b, e in evs[2:]:
     _lib.check(_lib.lib().sage_event_elapsed(b.h, e.h, D.C.byref(d)), "elapsed")
     us.append(d.value)
 import json, os  # noqa: E402
-print(json.dumps({"sgemm": f"{m}x{n}x{k}", "passes": os.environ.get("SAGE_SGEMM_PASSES", "3"), "bn": os.environ.get("SAGE_SGEMM_BN", "auto"), "median_us": round(float(np.median(us)), 2), "tflops_alg": round(2 * m * n * k / np.median(us) / 1e6, 1)}))
+print(json.dumps({"sgemm": f"{m}x{n}x{k}", "passes": os.environ.get("SAGE_SGEMM_PASSES", "3"), "bn": os.environ.get("SAGE_SGEMM_BN", "auto"), "median_us": round(float(np.median(us)), 2), "host_enqueue_us": round(host_us, 2), "tflops_alg": round(2 * m * n * k / np.median(us) / 1e6, 1)}))
 _lib.shutdown()
