@@ -843,7 +843,7 @@ def our_arm(args, rank, world, dist) -> dict:
                                       next((int(data[n].args[1]) for n in sorted(data) if data[n].body == "spmv"), 0)),
         "roofline_land": {"kernel": "land", "bound": "hbm", "achieved": land["achieved"], "peak": peaks["hbm_gbs"],
                           "unit": "GB/s", "frac": land["frac"], "traffic": land_traffic(probe["segment"]),
-                          "traffic_source": "profiles/r2_land_traffic.json (ncu --set full, one 256 MiB launch)",
+                          "traffic_source": "profiles/r2_land_traffic.json (ncu --set full, the same 1 GiB launch)",
                           "peak_source": peaks["source"], "same_size_d2d_GBps": probe["d2d_GBps"],
                           "frac_of_same_size_d2d": round(land["achieved"] / probe["d2d_GBps"], 4),
                           "avg_launch_us": land["avg_launch_us"], "alg_bytes_per_launch": land["alg_bytes_per_launch"],

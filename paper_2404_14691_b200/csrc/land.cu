@@ -60,7 +60,7 @@ struct Layout {
   Plan chunked, whole;
 };
 
-static constexpr uint64_t kWholeChunk = 256ull << 20;
+static constexpr uint64_t kWholeChunk = 4ull << 30;   // one launch per segment (<= 4 GiB: 32-bit vector indices)
 static std::mutex g_lay_mu;
 static std::unordered_map<uint64_t, Layout *> g_layouts;
 static std::atomic<uint64_t> g_lay_next{1};
@@ -182,8 +182,9 @@ static int layout_build(const uint64_t *src_off, const uint64_t *dst_off, const 
   }
   if (n == 0 && seg) return fail(SAGE_EINVAL, "layout: empty layout must have seg_bytes == 0");
   SAGE_TRY(build_plan(*L, chunk, &L->chunked));
-  // HBM-resident / peer sources need no staging: land in 256 MiB virtual
-  // chunks (keeps in-chunk offsets 32-bit) straight from the source
+  // HBM-resident / peer sources need no staging: land straight from the
+  // source in one launch per 4 GiB (a 1 GiB segment in 4 x 256 MiB launches
+  // measured 391 us vs 361 us in one: ramp and tail per launch)
   SAGE_TRY(build_plan(*L, kWholeChunk, &L->whole));
   return SAGE_OK;
 }

@@ -88,35 +88,54 @@ __device__ __forceinline__ void land_finalize(const LandArgs &a) {
 
 constexpr int kLandThreads = 256;
 #ifndef SAGE_LAND_U
-#define SAGE_LAND_U 4
+#define SAGE_LAND_U 8
 #endif
 #ifndef SAGE_LAND_MINB
-#define SAGE_LAND_MINB 4
+#define SAGE_LAND_MINB 3   // U = 8: 85 registers, no spills; 1 GiB 5.99 TB/s vs 5.95 at 4 (profiles/r2_land_u_sweep.txt)
 #endif
 constexpr int kLandU = SAGE_LAND_U;  // vectors per lane per tile
+static_assert(kLandU % 2 == 0, "the partial-tile path steps two rows at a time");
 
 // fastest path: a full tile of whole data vectors (no tail, no padding, no
-// bound checks) -- the common case inside every large tensor
+// bound checks) -- the common case inside every large tensor.  All kLandU
+// 512-B warp rows are loaded before any is used (kLandU x 16 B per lane in
+// flight).  A misaligned run needs, for lane l of row u, the source vector
+// after its own: that is lane l+1's vector (shuffle), or for lane 31 lane
+// 0's vector of row u+1 (shuffle), or past the tile (one extra load by lane
+// 31) -- one 16-B load per destination vector instead of two.
 template <int WS>
-__device__ __forceinline__ unsigned long long land_tile_full(const uint4 *__restrict__ qbase, uint32_t nB,
-                                                             uint4 *__restrict__ dbase, unsigned long long pbase,
-                                                             uint32_t loc0, uint32_t lane, uint32_t bs) {
+__device__ __forceinline__ unsigned long long land_tile_full(const uint4 *__restrict__ qbase, uint4 *__restrict__ dbase,
+                                                             unsigned long long pbase, uint32_t loc0, uint32_t lane,
+                                                             uint32_t bs) {
   unsigned long long acc = 0;
-  uint4 A[kLandU], B[kLandU];
+  uint4 A[kLandU];
 #pragma unroll
-  for (int u = 0; u < kLandU; ++u) {
-    const uint32_t loc = loc0 + u * 32u + lane;
-    A[u] = __ldg(qbase + loc);
-    // a whole data vector with a nonzero shift always needs (and may read) the next block
-    if (WS >= 0) B[u] = __ldg(qbase + loc + 1);
-  }
-  (void)nB;
+  for (int u = 0; u < kLandU; ++u) A[u] = __ldg(qbase + loc0 + u * 32u + lane);
+  uint4 X = make_uint4(0, 0, 0, 0);
+  // a whole data vector with a nonzero shift always needs (and may read) the next block
+  if (WS >= 0 && lane == 31) X = __ldg(qbase + loc0 + 32u * kLandU);
 #pragma unroll
   for (int u = 0; u < kLandU; ++u) {
     const uint32_t loc = loc0 + u * 32u + lane;
     uint4 o;
-    if (WS < 0) o = A[u];
-    else o = funnel_ws<WS < 0 ? 0 : WS>(A[u], B[u], bs);
+    if constexpr (WS < 0) {
+      o = A[u];
+    } else {
+      uint32_t a[4] = {A[u].x, A[u].y, A[u].z, A[u].w};
+      uint32_t b[4] = {0u, 0u, 0u, 0u};
+      uint32_t n[4] = {X.x, X.y, X.z, X.w};
+      if (u + 1 < kLandU) {
+        const uint4 &Nx = A[u + 1 < kLandU ? u + 1 : u];
+        n[0] = Nx.x; n[1] = Nx.y; n[2] = Nx.z; n[3] = Nx.w;
+      }
+#pragma unroll
+      for (int j = 0; j <= WS; ++j) {   // funnel_ws<WS> reads words 0..WS of the next vector
+        const uint32_t dn = __shfl_down_sync(0xffffffffu, a[j], 1);
+        const uint32_t nx = (u + 1 < kLandU) ? __shfl_sync(0xffffffffu, n[j], 0) : n[j];
+        b[j] = lane == 31 ? nx : dn;
+      }
+      o = funnel_ws<WS < 0 ? 0 : WS>(A[u], make_uint4(b[0], b[1], b[2], b[3]), bs);
+    }
     dbase[loc] = o;
     acc += vec_sum(o, pbase + 2ull * loc);
   }
@@ -131,29 +150,34 @@ __device__ __forceinline__ unsigned long long land_tile_uniform(const uint4 *__r
                                                                 uint32_t nfull, uint32_t ndata, uint32_t bs,
                                                                 long long data0) {
   if (nvalid == 32u * kLandU && loc0 + 32u * kLandU <= nfull)
-    return land_tile_full<WS>(qbase, nB, dbase, pbase, loc0, lane, bs);
+    return land_tile_full<WS>(qbase, dbase, pbase, loc0, lane, bs);
+  // partial tile (a tensor's last tile: its tail vector and zero padding):
+  // two rows at a time, bounds-checked
   unsigned long long acc = 0;
-  uint4 A[kLandU], B[kLandU];
+#pragma unroll 1
+  for (int u0 = 0; u0 < kLandU; u0 += 2) {
+    uint4 A[2], B[2];
 #pragma unroll
-  for (int u = 0; u < kLandU; ++u) {
-    uint32_t loc = loc0 + u * 32u + lane;
-    A[u] = make_uint4(0, 0, 0, 0);
-    B[u] = make_uint4(0, 0, 0, 0);
-    if (u * 32u + lane < nvalid && loc < ndata) {
-      A[u] = __ldg(qbase + loc);
-      if (WS >= 0 && loc + 1 < nB) B[u] = __ldg(qbase + loc + 1);
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t loc = loc0 + (u0 + h) * 32u + lane;
+      A[h] = make_uint4(0, 0, 0, 0);
+      B[h] = make_uint4(0, 0, 0, 0);
+      if ((u0 + h) * 32u + lane < nvalid && loc < ndata) {
+        A[h] = __ldg(qbase + loc);
+        if (WS >= 0 && loc + 1 < nB) B[h] = __ldg(qbase + loc + 1);
+      }
     }
-  }
 #pragma unroll
-  for (int u = 0; u < kLandU; ++u) {
-    uint32_t loc = loc0 + u * 32u + lane;
-    if (u * 32u + lane >= nvalid) continue;
-    uint4 o;
-    if (WS < 0) o = A[u];
-    else o = funnel_ws<WS < 0 ? 0 : WS>(A[u], B[u], bs);
-    if (loc >= nfull) o = (loc < ndata) ? mask_tail(o, data0 - 16ll * loc) : make_uint4(0, 0, 0, 0);
-    dbase[loc] = o;
-    acc += vec_sum(o, pbase + 2ull * loc);
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t loc = loc0 + (u0 + h) * 32u + lane;
+      if ((u0 + h) * 32u + lane >= nvalid) continue;
+      uint4 o;
+      if (WS < 0) o = A[h];
+      else o = funnel_ws<WS < 0 ? 0 : WS>(A[h], B[h], bs);
+      if (loc >= nfull) o = (loc < ndata) ? mask_tail(o, data0 - 16ll * loc) : make_uint4(0, 0, 0, 0);
+      dbase[loc] = o;
+      acc += vec_sum(o, pbase + 2ull * loc);
+    }
   }
   return acc;
 }

@@ -207,6 +207,18 @@ int main(int argc, char **argv) {
       LandArgs a{d_item, d_prefix, 1, (uint32_t)(S / 16), src, S, dst, acc, d_done, nullptr};
       land_kernel<<<land_grid(&G, (uint32_t)(S / 16)), kLandThreads, 0, st>>>(a);
     }, true, 20, F);
+    for (int sh : {4, 7}) {   // misaligned source runs (funnel-shift paths)
+      LandItem it2{0, 0, (long long)(S - 16), (unsigned)(S / 16), 0};
+      CK(cudaMemcpy(d_item, &it2, sizeof(it2), cudaMemcpyHostToDevice));
+      char nm[32];
+      snprintf(nm, sizeof nm, "land_sh%d", sh);
+      run(nm, [&] {
+        LandArgs a{d_item, d_prefix, 1, (uint32_t)(S / 16), src + sh, S - 16, dst, acc, d_done, nullptr};
+        land_kernel<<<land_grid(&G, (uint32_t)(S / 16)), kLandThreads, 0, st>>>(a);
+      }, false, 20, F);
+      CK(cudaMemcpy(d_item, &item, sizeof(item), cudaMemcpyHostToDevice));
+    }
+    if (getenv("LM_SHORT")) continue;
     run("sum_u4", [&] { sum_u<4><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
     run("sum_u8", [&] { sum_u<8><<<sm * 4, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);
     run("sum_u8_g8", [&] { sum_u<8><<<sm * 8, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, S / 16, acc); }, true, 20, F);

@@ -2,7 +2,7 @@
 HBM-resident packed record, timed with the load's device events; the
 roofline evidence for `land` away from L2 effects.
 python tools/prof_land_big.py [GiB] [iters]
-ncu: the host upload is 128 staged chunk lands, then 4 x 256 MiB lands per
+ncu: the host upload is 128 staged chunk lands, then one 1 GiB land per
 iteration: ncu -k regex:land_kernel -s 128 -c 1 python tools/prof_land_big.py 1 1"""
 import json
 import sys
