@@ -10,9 +10,10 @@
 //              SWIZZLE_128B row) x BN output channels per K-block
 //   warp 1     TMEM allocator + single-thread MMA issuer: 4 x
 //              tcgen05.mma.kind::f16 (K = 16 each) per K-block
-//   warps 2-5  im2col gatherers: thread t owns output pixel m0 + t and fills
-//              its 128-B row of the A tile per K-block with cp.async (16 B
-//              per 8 channels; zero-fill for padding and rows past M), then
+//   warps 2-5  im2col gatherers: warp w fills A rows [32w, 32w + 32) per
+//              K-block with cp.async, 4 whole 128-B pixel slices per
+//              instruction (16 B = 8 channels per lane; zero-fill for padding
+//              and rows past M), then
 //              -- when its copies have landed -- a proxy fence and an arrive
 //              on the stage's barrier; after the K loop the same warps are
 //              the epilogue: tcgen05.ld 32 channels at a time, y = acc * scale
@@ -42,7 +43,8 @@ struct CvSmem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // shallow enough for two CTAs per SM at BN <= 128: a batch-8 layer is
   // gather-latency bound, so resident CTAs (memory parallelism) beat depth
-  static constexpr int STAGES = (BN >= 128 ? 3 : 4);
+  // BN = 256 runs one CTA per SM anyway: 4 stages (196 KB) for the long-K layers
+  static constexpr int STAGES = (BN >= 256 ? 4 : BN >= 128 ? 3 : 4);
   static constexpr int TOTAL = STAGES * STAGE + 1024 + 256 + 2 * 256 * 4;
 };
 
@@ -182,37 +184,69 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
                    : "memory");
     }
   } else {
-    // ---- im2col gather: this thread's output pixel ----
+    // ---- im2col gather ----
+    // C4 (stem): thread t owns output pixel m0 + t.  Otherwise a warp covers
+    // its 32 pixel rows 4 at a time: lane l copies 16-B chunk (l & 7) of
+    // pixel row 4j + (l >> 3), so one cp.async instruction reads 4 whole
+    // 128-B pixel slices (full lines) instead of 16 B of 32 pixels
     const int row = threadIdx.x - 64;
-    const int m = m0 + row;
-    const bool live = m < a.M;
-    int n = 0, p = 0, q = 0;
-    if (live) {
-      q = m % a.Q;
-      const int t = m / a.Q;
-      p = t % a.P;
-      n = t / a.P;
-    }
-    const int ih0 = p * a.stride - a.pad, iw0 = q * a.stride - a.pad;
+    const int gw = row >> 5;
     const int cslices = C4 ? 1 : a.C / CV_BK;
+    int n = 0, ih0 = 0, iw0 = 0;
+    bool live = false;
+    int jn[8], jh[8], jw[8];   // per pixel row j of this lane (non-C4)
+    if constexpr (C4) {
+      const int m = m0 + row;
+      live = m < a.M;
+      int p = 0, q = 0;
+      if (live) {
+        q = m % a.Q;
+        const int t = m / a.Q;
+        p = t % a.P;
+        n = t / a.P;
+      }
+      ih0 = p * a.stride - a.pad;
+      iw0 = q * a.stride - a.pad;
+    } else {
+      // pixel rows j step by 4 pixels: one division for j = 0, then carries (Q >= 4)
+      const int m_first = m0 + gw * 32 + (lane >> 3);
+      int q = m_first % a.Q, t = m_first / a.Q;
+      int p = t % a.P, nn = t / a.P;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (m_first + 4 * j < a.M) {
+          jn[j] = nn;
+          jh[j] = p * a.stride - a.pad;
+          jw[j] = q * a.stride - a.pad;
+        } else {
+          jn[j] = 0; jh[j] = -(1 << 28); jw[j] = 0;   // never in bounds: zero-filled
+        }
+        q += 4;
+        while (q >= a.Q) { q -= a.Q; if (++p == a.P) { p = 0; ++nn; } }
+      }
+    }
     const uint32_t rbase = (uint32_t)row * 128u, rsw = (uint32_t)(row & 7);
+    const uint32_t chunk = (uint32_t)(lane & 7);
     for (int kb = 0; kb < KB; ++kb) {
       const int s = kb % ST, round = kb / ST;
       cv_wait(&empty[s], (round & 1) ^ 1);
-      const uint32_t dst = cv_smem(sA + s * Sm::A_BYTES) + rbase;
       if constexpr (!C4) {
+        const uint32_t tile = cv_smem(sA + s * Sm::A_BYTES) + (uint32_t)gw * 32u * 128u;
         const int tap = kb / cslices, c0 = (kb - tap * cslices) * CV_BK;
         const int r = tap / a.S, sx = tap - r * a.S;
-        const int ih = ih0 + r, iw = iw0 + sx;
-        const bool ok = live && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-        const __nv_bfloat16 *src = ok ? X + ((size_t)(n * a.H + ih) * a.W + iw) * a.C + c0 : X;
-        const uint32_t bytes = ok ? 16u : 0u;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + ((j ^ rsw) << 4)),
-                       "l"(src + 8 * j), "r"(bytes)
+        for (int j = 0; j < 8; ++j) {
+          const int ih = jh[j] + r, iw = jw[j] + sx;
+          const bool ok = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+          const __nv_bfloat16 *src = ok ? X + ((size_t)(jn[j] * a.H + ih) * a.W + iw) * a.C + c0 + 8 * chunk : X;
+          const uint32_t prow = 4u * j + (uint32_t)(lane >> 3);     // row within the warp's 32
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tile + prow * 128u +
+                                                                              ((chunk ^ (prow & 7u)) << 4)),
+                       "l"(src), "r"(ok ? 16u : 0u)
                        : "memory");
+        }
       } else {
+        const uint32_t dst = cv_smem(sA + s * Sm::A_BYTES) + rbase;
         // 16 taps x 4 channels (8 B) per K-block over the NHWC4 input
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
