@@ -186,3 +186,47 @@ def test_spmv_csb_rejects_bad_formats(dp):
             run_body(_lib.BODY_SPMV_CSB, sr.dptr, ro.size, sx.dptr, x.nbytes, 3000 * 4, tuple(a))
     sr.free()
     sx.free()
+
+
+_ENV_CHECK = r'''
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_2404_14691_b200 import _lib
+from paper_2404_14691_b200 import device as D
+sys.path.insert(0, sys.argv[1] + "/tests")
+from test_bodies_gpu import run_body, upload
+_lib.init(n_gpus=1, pool_bytes=4 << 30)
+try:
+    for m, n, k in [(512, 256, 4096), (4096, 256, 4096), (256, 256, 64)]:
+        rng = np.random.default_rng(m + 7 * k)
+        A = rng.standard_normal((m, k), dtype=np.float32)
+        BT = rng.standard_normal((n, k), dtype=np.float32)
+        sa, sb = upload(A), upload(BT)
+        got = run_body(_lib.BODY_SGEMM, sa.dptr, A.nbytes, sb.dptr, BT.nbytes, m * n * 4, (m, n, k))
+        got = got.view(np.float32).reshape(m, n)
+        want = O.sgemm_ref(A, BT.T)
+        np.testing.assert_allclose(got, want, rtol=1e-3, atol=1e-4 * np.abs(want).max())
+        sa.free(); sb.free()
+finally:
+    _lib.shutdown()
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("env", [{"SAGE_SGEMM_PAIR": "1"}, {"SAGE_SGEMM_CR": "0"}, {"SAGE_SGEMM_MC": "1"}])
+def test_sgemm_variants_fp32(env, tmp_path):
+    """The opt-in sgemm kernels (CTA pair cta_group::2, split-K by red.add,
+    B-multicast clusters) hold the same FP32 contract; the variant is chosen
+    at library load, so each runs in its own process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    script = tmp_path / "check.py"
+    script.write_text(_ENV_CHECK)
+    r = subprocess.run([sys.executable, str(script), root], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
