@@ -36,15 +36,17 @@ constexpr int CV_BM = 128;       // output pixels per CTA (UMMA M)
 constexpr int CV_BK = 64;        // bf16 per K-block = one 128-B row
 constexpr int CV_THREADS = 192;
 
-template <int BN>
+template <int BN, int SHORT = 0>
 struct CvSmem {
   static constexpr int A_BYTES = CV_BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // shallow enough for two CTAs per SM at BN <= 128: a batch-8 layer is
   // gather-latency bound, so resident CTAs (memory parallelism) beat depth
-  // BN = 256 runs one CTA per SM anyway: 4 stages (196 KB) for the long-K layers
-  static constexpr int STAGES = (BN >= 256 ? 4 : BN >= 128 ? 3 : 4);
+  // BN = 256: 4 stages (196 KB, one CTA per SM) for the long-K layers; SHORT
+  // (a few K-blocks) keeps 2 stages (98 KB) so two CTAs share an SM and one's
+  // prologue / epilogue overlaps the other's K loop
+  static constexpr int STAGES = SHORT ? 2 : (BN >= 256 ? 4 : BN >= 128 ? 3 : 4);
   static constexpr int TOTAL = STAGES * STAGE + 1024 + 256 + 2 * 256 * 4;
 };
 
@@ -81,10 +83,10 @@ struct ConvArgs {
   int N, H, W, C, P, Q, R, S, stride, pad, Cout, M, KB, relu;
 };
 
-template <int BN, int C4>
+template <int BN, int C4, int SHORT = 0>
 __global__ void __launch_bounds__(CV_THREADS, 2)
     conv_bf16_kernel(const __grid_constant__ CUtensorMap mapW, const ConvArgs a) {
-  using Sm = CvSmem<BN>;
+  using Sm = CvSmem<BN, SHORT>;
   constexpr int ST = Sm::STAGES;
   constexpr int CV_LAG = ST - 1;   // cp.async K-blocks a gatherer keeps in flight past the arrived ones
   extern __shared__ uint8_t smem_raw[];
@@ -401,11 +403,11 @@ static int smem_optin(const void *fn, int bytes) {
   return SAGE_OK;
 }
 
-template <int BN, int C4>
+template <int BN, int C4, int SHORT = 0>
 static int launch_conv(const CUtensorMap &map, const ConvArgs &a, cudaStream_t s) {
-  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<BN, C4>, CvSmem<BN>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<BN, C4, SHORT>, CvSmem<BN, SHORT>::TOTAL));
   dim3 grid((a.M + CV_BM - 1) / CV_BM, a.Cout / BN);
-  conv_bf16_kernel<BN, C4><<<grid, CV_THREADS, CvSmem<BN>::TOTAL, s>>>(map, a);
+  conv_bf16_kernel<BN, C4, SHORT><<<grid, CV_THREADS, CvSmem<BN, SHORT>::TOTAL, s>>>(map, a);
   SAGE_CUDA(cudaGetLastError());
   return SAGE_OK;
 }
@@ -460,15 +462,23 @@ int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame 
   CUtensorMap map;
   SAGE_TRY(filter_map(&map, d->w, (uint64_t)d->cout, ktot, (uint32_t)bn));
   if (c4) return bn == 64 ? launch_conv<64, 1>(map, a, s) : launch_conv<128, 1>(map, a, s);
-  if (bn == 256) return launch_conv<256, 0>(map, a, s);
-  if (bn == 128) return launch_conv<128, 0>(map, a, s);
-  return launch_conv<64, 0>(map, a, s);
+  // SAGE_CONV_SHORT_KB: layers with at most this many K-blocks take the
+  // 2-stage BN = 256 kernel (two CTAs per SM)
+  static const int short_kb = [] { const char *e = getenv("SAGE_CONV_SHORT_KB"); return e ? atoi(e) : 8; }();
+  static const bool short_all = [] { const char *e = getenv("SAGE_CONV_SHORT_ALL"); return e && atoi(e) != 0; }();
+  const bool shrt = a.KB <= short_kb;
+  if (bn == 256) return shrt ? launch_conv<256, 0, 1>(map, a, s) : launch_conv<256, 0>(map, a, s);
+  if (bn == 128) return shrt && short_all ? launch_conv<128, 0, 1>(map, a, s) : launch_conv<128, 0>(map, a, s);
+  return shrt && short_all ? launch_conv<64, 0, 1>(map, a, s) : launch_conv<64, 0>(map, a, s);
 }
 
 int conv_optin_all() {
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 0>, CvSmem<64>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 0>, CvSmem<128>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0>, CvSmem<256>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0, 1>, CvSmem<256, 1>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 0, 1>, CvSmem<128, 1>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 0, 1>, CvSmem<64, 1>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 1>, CvSmem<64>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 1>, CvSmem<128>::TOTAL));
   return SAGE_OK;
@@ -479,6 +489,9 @@ int touch_conv_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 0>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 0>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0, 1>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 0, 1>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 0, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 1>));
   return SAGE_OK;
