@@ -58,6 +58,7 @@ struct Inv {
   sage_handle last = 0;                 // the stage boundary most recently recorded on s
   LoadCursor *ro_cur = nullptr;         // staged RO load still being enqueued
   std::atomic<bool> issued{false};
+  bool ready = false;                   // issuer only: every held event recorded
   std::string err;                      // issue failure (reported by collect)
   sage_invoke_info info{};
   std::atomic<int> resolved{0};   // 1: `info` computed by the completion thread, 2: done (lazy)
@@ -443,7 +444,8 @@ static bool issuer_enabled() {
   return on;
 }
 
-static bool inv_ready(const Inv *I) {
+static bool inv_ready(Inv *I) {
+  if (I->ready) return true;   // readiness never reverts: checked once per hold
   for (sage_handle h : I->hold) {
     if (!h) continue;
     Event *e = event_get(h);
@@ -451,6 +453,7 @@ static bool inv_ready(const Inv *I) {
     if (e->ev ? !e->recorded.load(std::memory_order_acquire) : !e->host_done.load(std::memory_order_acquire))
       return false;
   }
+  I->ready = true;
   return true;
 }
 
@@ -513,6 +516,8 @@ static bool issue_step(Inv *I, int64_t piece, std::deque<Flight> &flights) {
   return true;
 }
 
+static constexpr int kIssueScan = 256;
+
 static void issuer_main() {
   const int64_t lookahead = env_i64("SAGE_ISSUE_LOOKAHEAD_MB", 32) << 20;
   const int64_t max_defer = env_i64("SAGE_ISSUE_MAX_DEFER_US", 3000);
@@ -568,7 +573,11 @@ static void issuer_main() {
         auto fol = iss_q.end(), cold = iss_q.end();
         int64_t fol_key = INT64_MAX, cold_key = INT64_MAX;
         bool fol_overdue = false;
-        for (auto it = iss_q.begin(); it != iss_q.end(); ++it) {
+        // the pick looks at the oldest kIssueScan waiting invocations only:
+        // a backlog of thousands (offered load above capacity) must not make
+        // every pick O(backlog) -- that collapsed cfg-3 at 4000/s offered
+        int scanned = 0;
+        for (auto it = iss_q.begin(); it != iss_q.end() && scanned < kIssueScan; ++it, ++scanned) {
           Inv *I = *it;
           if (I->gpu != g || !inv_ready(I)) continue;
           if (I->h2d > 0 && !has_room) continue;

@@ -1,0 +1,12 @@
+#!/bin/bash
+mkdir -p gpurun_out/cfgs
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+timeout 600 python -m pytest tests/test_issuer_gpu.py tests/test_runtime_gpu.py -x -q > gpurun_out/pytest_iss.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_iss.log; tail -2 gpurun_out/pytest_iss.log
+for r in 3500 4000 5000; do timeout 300 python -m paper_2404_14691_b200.experiments cfg3 --dtype bf16 --rate $r --gpus 1 2>&1 | tail -1; done > gpurun_out/cfgs/cfg3_native_r2d.jsonl
+python - <<'PY'
+import json
+for l in open('gpurun_out/cfgs/cfg3_native_r2d.jsonl'):
+    try: d=json.loads(l)['cfg3']
+    except Exception: print(l[:300]); continue
+    g=d['G1']; print(d['workload'][-40:], {k:g.get(k) for k in ('completed','throughput_per_s','setup_p50_ms','setup_p99_ms','latency_p50_ms','wall_s')})
+PY
