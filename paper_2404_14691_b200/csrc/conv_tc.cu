@@ -13,9 +13,9 @@
 //   warps 2-5  im2col gatherers: warp w fills A rows [32w, 32w + 32) per
 //              K-block with cp.async, 4 whole 128-B pixel slices per
 //              instruction (16 B = 8 channels per lane; zero-fill for padding
-//              and rows past M), then
-//              -- when its copies have landed -- a proxy fence and an arrive
-//              on the stage's barrier; after the K loop the same warps are
+//              and rows past M) and hands the stage's arrival to the copy
+//              unit (cp.async.mbarrier.arrive.noinc: it arrives when the
+//              thread's copies have landed); after the K loop the same warps are
 //              the epilogue: tcgen05.ld 32 channels at a time, y = acc * scale
 //              + bias (+ residual), ReLU, bf16, 64-B stores (NHWC)
 // K-block order: filter tap (r, s) outer, 64-channel slice inner, so every
@@ -88,7 +88,6 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
     conv_bf16_kernel(const __grid_constant__ CUtensorMap mapW, const ConvArgs a) {
   using Sm = CvSmem<BN, SHORT>;
   constexpr int ST = Sm::STAGES;
-  constexpr int CV_LAG = ST - 1;   // cp.async K-blocks a gatherer keeps in flight past the arrived ones
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *sA = smem;                    // ST x A_BYTES
@@ -263,17 +262,12 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
                        : "memory");
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (kb >= CV_LAG) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(CV_LAG) : "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cv_smem(&full[(kb - CV_LAG) % ST])) : "memory");
-      }
+      // the stage's arrival is made by the copy unit when this thread's
+      // copies have landed (as CUTLASS's sm100 cp.async UMMA mainloop does):
+      // the thread moves on to the next stage at once, so a stage's readiness
+      // never waits for a later stage's slot to be released by the MMA
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(cv_smem(&full[s])) : "memory");
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (int kb = KB > CV_LAG ? KB - CV_LAG : 0; kb < KB; ++kb)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cv_smem(&full[kb % ST])) : "memory");
 
     // ---- epilogue: TMEM lane quadrant (warp % 4) = 32 output pixels ----
     cv_wait(tmem_full, 0);

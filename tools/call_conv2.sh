@@ -6,4 +6,4 @@ timeout 900 python -m pytest tests/test_conv_gpu.py tests/test_dnn_gpu.py -x -q 
 tail -2 gpurun_out/pytest_conv.log
 timeout 300 python tools/prof_resnet_native.py 8 8 20 | tail -1
 timeout 300 python tools/prof_resnet_native.py 8 16 20 | tail -1
-timeout 300 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -c 130 --csv --log-file gpurun_out/resnet_layers3.csv env SAGE_NET_GRAPHS=0 python tools/prof_resnet_native.py 8 1 1 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -c 130 --csv --log-file gpurun_out/resnet_layers4.csv env SAGE_NET_GRAPHS=0 python tools/prof_resnet_native.py 8 1 1 > /dev/null 2>&1
