@@ -162,10 +162,14 @@ static void unmap_segment(Pool *P, Alloc *A) {
   if (!A->va) return;
   P->physical -= A->phys;
   // keep the segment MAPPED for reuse by the next allocation of this size
-  // (per-invocation writable churn then costs no driver call) while the
-  // cache stays within budget; otherwise unmap and release the pages
-  if (!A->exported && P->cached + A->phys + P->physical <= P->capacity + (4ull << 30) &&
-      P->cached + A->phys <= (16ull << 30)) {
+  // (per-invocation writable churn then costs no driver call) while mapped +
+  // cached pages stay within the budget; otherwise unmap and release them.
+  // No separate cap on the cache: with thousands of invocations in flight
+  // (offered load above capacity) a 16 GiB cap made every alloc / free a
+  // cuMemCreate+Map / Unmap+Release (~150-250 us of host time each), which
+  // halved cfg-3 throughput; a cuMemCreate that finds the HBM held by the
+  // cache releases it and retries (map_segment)
+  if (!A->exported && P->cached + A->phys + P->physical <= P->capacity + (4ull << 30)) {
     P->free_mapped.emplace(A->phys, std::make_pair(A->va, A->ph));
     P->cached += A->phys;
   } else {
