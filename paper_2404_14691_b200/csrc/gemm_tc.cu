@@ -492,6 +492,160 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
   if constexpr (MC) cluster_sync_all();
 }
 
+// ------------------------------------------------------------ stream-K ----
+// 3xTF32, one CTA per SM: the (tile, K-block) units of the whole GEMM -- for
+// the cfg-2 shape 32 tiles x 128 K-blocks -- are cut into equal contiguous
+// ranges, one per CTA, so every SM of the GPU runs K-blocks (the split-K
+// grid above uses 128 of 148).  A range spans at most two tiles (range <
+// K-blocks per tile); each segment accumulates in its own TMEM half and is
+// added into C (zeroed by the host) with vector reductions.  No clusters:
+// in a busy burst a CTA needs one free SM, not four in one GPC.
+template <int BN>
+__global__ void __launch_bounds__(tc_threads<1>(), 1)
+    sgemm_x3_sk_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float *C,
+                       int M, int N, int K, int units_per_cta) {
+  using S = TcSmem<BN, 1>;
+  constexpr int ST = S::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *sA = smem, *sB = smem + ST * S::A_BYTES;
+  uint8_t *sAl = smem + ST * S::RAW, *sBl = sAl + ST * S::A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * S::STAGE);
+  uint64_t *empty = full + ST;
+  uint64_t *conv = empty + ST;
+  uint64_t *tmem_full = conv + ST;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kblk = K / TC_BK, ntn = N / BN;
+  const int total = (M / TC_BM) * ntn * kblk;
+  const int u0 = blockIdx.x * units_per_cta;
+  const int u1 = min(total, u0 + units_per_cta);
+  const int nu = u1 - u0;
+  if (nu <= 0) return;   // (the host sizes the grid so this does not happen)
+  const int t0 = u0 / kblk;                // first tile; a second one starts at unit (t0 + 1) * kblk
+  const int split_u = min(u1, (t0 + 1) * kblk);
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int i = 0; i < ST; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], 1);
+        mbar_init(&conv[i], TC_CONV_WARPS_X3);
+      }
+      mbar_init(tmem_full, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < nu; ++j) {
+        const int u = u0 + j, t = u / kblk, kb = u - t * kblk;
+        const int m0 = (t / ntn) * TC_BM, n0 = (t % ntn) * BN;
+        const int st = j % ST, round = j / ST;
+        mbar_wait(&empty[st], (round & 1) ^ 1);
+        mbar_expect_tx(&full[st], S::RAW);
+        tma_load_2d(sA + st * S::A_BYTES, &mapA, &full[st], kb * TC_BK, m0);
+        tma_load_2d(sB + st * S::B_BYTES, &mapB, &full[st], kb * TC_BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tf32_idesc<BN>();
+      for (int j = 0; j < nu; ++j) {
+        const int u = u0 + j;
+        const int st = j % ST, round = j / ST;
+        mbar_wait(&conv[st], round & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc_t = tmem + (u >= split_u ? (uint32_t)BN : 0u);   // segment's TMEM half
+        const bool first = (u == u0) || (u == split_u);
+        const uint64_t da = kmajor_sw128_desc(smem_u32(sA + st * S::A_BYTES));
+        const uint64_t db = kmajor_sw128_desc(smem_u32(sB + st * S::B_BYTES));
+        const uint64_t dal = kmajor_sw128_desc(smem_u32(sAl + st * S::A_BYTES));
+        const uint64_t dbl = kmajor_sw128_desc(smem_u32(sBl + st * S::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < TC_BK / 8; ++k) {
+          const uint64_t a = da + (uint64_t)(2 * k), b = db + (uint64_t)(2 * k);
+          const uint32_t acc = (first && k == 0) ? 0u : 1u;
+          mma_tf32(acc_t, dal + (uint64_t)(2 * k), b, idesc, acc);
+          mma_tf32(acc_t, a, dbl + (uint64_t)(2 * k), idesc, 1u);
+          mma_tf32(acc_t, a, b, idesc, 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[st]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(tmem_full))
+                   : "memory");
+    }
+  } else {
+    constexpr int NT = 32 * TC_CONV_WARPS_X3;
+    const int t = threadIdx.x - 64;
+    for (int j = 0; j < nu; ++j) {
+      const int st = j % ST, round = j / ST;
+      mbar_wait(&full[st], round & 1);
+      split_tile<1, NT>(sA + st * S::A_BYTES, sAl + st * S::A_BYTES, S::A_BYTES, t);
+      split_tile<1, NT>(sB + st * S::B_BYTES, sBl + st * S::B_BYTES, S::B_BYTES, t);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[st])) : "memory");
+    }
+    if (warp < 6) mbar_wait(tmem_full, 0);
+  }
+  if (warp >= 2 && warp < 6) {
+    // ---- epilogue: each segment's partial tile, added into C ----
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quad = warp & 3;
+    const int nseg = u1 > split_u ? 2 : 1;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const int tile = t0 + sg;
+      const int row = (tile / ntn) * TC_BM + quad * 32 + lane, n0 = (tile % ntn) * BN;
+      float *crow = C + (size_t)row * N + n0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sg * BN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+          float4 *dst = reinterpret_cast<float4 *>(crow + c);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + q), "f"(__uint_as_float(r[4 * q])),
+                         "f"(__uint_as_float(r[4 * q + 1])), "f"(__uint_as_float(r[4 * q + 2])),
+                         "f"(__uint_as_float(r[4 * q + 3]))
+                         : "memory");
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
 // ------------------------------------------------------------------ host -----
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -572,8 +726,41 @@ static bool sgemm_pair_enabled() {
   return on;
 }
 
+// SAGE_SGEMM_SK=1 (opt-in): the stream-K 3xTF32 kernel over every SM.  Off
+// by default: measured 51.3 vs 49.2 us back to back (the memset launch and
+// the red.add epilogue of up to two partial tiles per CTA outweigh the 12%
+// shorter K range), and slower inside the cfg-2 burst (tools/call_sk.sh)
+static bool sgemm_sk_enabled() {
+  static const bool on = [] { const char *e = getenv("SAGE_SGEMM_SK"); return e && atoi(e) != 0; }();
+  return on;
+}
+
+template <int BN>
+static int launch_sk(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s, int sms) {
+  CUtensorMap ma, mb;
+  SAGE_TRY(encode_kmajor(&ma, A, (uint64_t)M, (uint64_t)K, TC_BM));
+  SAGE_TRY(encode_kmajor(&mb, BT, (uint64_t)N, (uint64_t)K, BN));
+  const int kblk = K / TC_BK, total = (M / TC_BM) * (N / BN) * kblk;
+  int per = (total + sms - 1) / sms;
+  if (per > kblk) per = kblk;   // a range must not span more than two tiles
+  const int grid = (total + per - 1) / per;
+  SAGE_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+  using S = TcSmem<BN, 1>;
+  SAGE_CUDA(cudaFuncSetAttribute(sgemm_x3_sk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
+  sgemm_x3_sk_kernel<BN><<<grid, tc_threads<1>(), S::TOTAL, s>>>(ma, mb, C, M, N, K, per);
+  SAGE_CUDA(cudaGetLastError());
+  return SAGE_OK;
+}
+
 template <int BN, int X3>
 static int launch_tc(const float *A, const float *BT, float *C, int M, int N, int K, cudaStream_t s) {
+  if constexpr (X3 == 1 && BN == 256) {
+    if (sgemm_sk_enabled()) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      return launch_sk<BN>(A, BT, C, M, N, K, s, sm_count_of(dev));
+    }
+  }
   // 2-CTA clusters along M when the M tiles pair up
   const bool mc = sgemm_mc_enabled() && (M / TC_BM) % 2 == 0;
   // split K so the grid covers the SMs: a skinny GEMM (N <= 256) has only
@@ -651,6 +838,7 @@ template <int X3>
 static int touch_x() {
   cudaFuncAttributes a;
   if constexpr (X3 == 1) {
+    SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_x3_sk_kernel<256>));
     SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, true, X3, true>));
     SAGE_CUDA(cudaFuncGetAttributes(&a, sgemm_tf32_kernel<256, false, false, X3, true>));
   }

@@ -215,9 +215,10 @@ print("ok")
 '''
 
 
-@pytest.mark.parametrize("env", [{"SAGE_SGEMM_PAIR": "1"}, {"SAGE_SGEMM_CR": "0"}, {"SAGE_SGEMM_MC": "1"}])
+@pytest.mark.parametrize("env", [{"SAGE_SGEMM_PAIR": "1"}, {"SAGE_SGEMM_CR": "0"}, {"SAGE_SGEMM_MC": "1"},
+                                 {"SAGE_SGEMM_SK": "1"}])
 def test_sgemm_variants_fp32(env, tmp_path):
-    """The opt-in sgemm kernels (CTA pair cta_group::2, split-K by red.add,
+    """The opt-in sgemm kernels (CTA pair cta_group::2, split-K by red.add, stream-K,
     B-multicast clusters) hold the same FP32 contract; the variant is chosen
     at library load, so each runs in its own process."""
     import os

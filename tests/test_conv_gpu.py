@@ -2,7 +2,8 @@
 (sage_conv) against torch-CPU fp32 on the same bf16 values: every ResNet-50
 convolution shape class (1x1 stride 1 / 2, 3x3 stride 1 / 2, conv1's 7x7
 stride 2 in the C4 mode), folded batch-norm, residual add, ReLU, ragged M
-(rows past the last full 128-pixel tile).  BF16 outputs: rtol 1e-2 with
+(rows past the last full 128-pixel tile), the 2-stage short-K and 4-stage
+long-K BN = 256 kernels.  BF16 outputs: rtol 1e-2 with
 atol 1e-2 * max|y| (BASELINE.json north_star BF16 tolerance)."""
 import ctypes as C
 
@@ -90,6 +91,10 @@ SHAPES = [  # n, h, w, cin, cout, k, stride, pad, bn, residual, relu
     (2, 15, 15, 128, 128, 3, 2, 1, False, False, False),    # 3x3 stride 2, odd size, no BN
     (1, 7, 7, 512, 2048, 1, 1, 0, True, True, True),        # layer4 expand: M = 49
     (3, 9, 11, 192, 320, 3, 1, 1, True, True, True),        # non power-of-two channels (Cout % 64)
+    (2, 14, 14, 256, 256, 3, 1, 1, True, False, True),      # BN = 256, 36 K-blocks: the 4-stage kernel
+    (1, 7, 7, 512, 512, 3, 1, 1, True, True, True),         # layer4 3x3: 72 K-blocks, 4 M tiles
+    (2, 28, 28, 256, 256, 3, 2, 1, True, False, True),      # 3x3 stride 2, BN = 256, long K
+    (4, 56, 56, 64, 256, 1, 1, 0, True, True, True),        # layer1 expand: 1 K-block, 98 M tiles (2-stage kernel)
 ]
 
 
