@@ -522,6 +522,7 @@ static void issuer_main() {
   const int64_t lookahead = env_i64("SAGE_ISSUE_LOOKAHEAD_MB", 32) << 20;
   const int64_t max_defer = env_i64("SAGE_ISSUE_MAX_DEFER_US", 3000);
   const int64_t piece = env_i64("SAGE_ISSUE_PIECE_MB", 0) << 20;
+  const bool tiebreak_d2h = env_i64("SAGE_ISSUE_BIG_RETURN_FIRST", 1) != 0;
   std::deque<Flight> flights;   // H2D queued by this thread, not yet landed
   std::vector<int64_t> pending;
   std::vector<char> piece_turn; // per GPU: the next slot goes to an open staged load
@@ -571,13 +572,16 @@ static void issuer_main() {
           for (auto it = iss_open.begin(); it != iss_open.end(); ++it)
             if ((*it)->gpu == g) { open = it; break; }
         auto fol = iss_q.end(), cold = iss_q.end();
-        int64_t fol_key = INT64_MAX, cold_key = INT64_MAX;
+        int64_t fol_key = INT64_MAX, cold_key = INT64_MAX, fol_d2h = -1;
         bool fol_overdue = false;
-        // the pick looks at the oldest kIssueScan waiting invocations only:
-        // a backlog of thousands (offered load above capacity) must not make
-        // every pick O(backlog) -- that collapsed cfg-3 at 4000/s offered
+        // the pick looks at the oldest kIssueScan waiting invocations, and
+        // further only until it has a candidate: a backlog of thousands
+        // (offered load above capacity) must not make every pick O(backlog)
+        // -- that collapsed cfg-3 at 4000/s offered -- while a window of
+        // followers whose leader waits further back cannot stall the queue
         int scanned = 0;
-        for (auto it = iss_q.begin(); it != iss_q.end() && scanned < kIssueScan; ++it, ++scanned) {
+        for (auto it = iss_q.begin(); it != iss_q.end(); ++it, ++scanned) {
+          if (scanned >= kIssueScan && (fol != iss_q.end() || cold != iss_q.end())) break;
           Inv *I = *it;
           if (I->gpu != g || !inv_ready(I)) continue;
           if (I->h2d > 0 && !has_room) continue;
@@ -586,7 +590,11 @@ static void issuer_main() {
             if (key < cold_key) { cold_key = key; cold = it; }
           } else if (!fol_overdue) {
             if (now - I->t_enqueue >= max_defer) { fol = it; fol_overdue = true; }
-            else if (key < fol_key) { fol_key = key; fol = it; }
+            else if (key < fol_key || (key == fol_key && tiebreak_d2h && I->d2h > fol_d2h)) {
+              // equal balance: the larger return first, so a burst ends on
+              // small returns (a big D2H alone at the end idles the H2D lane)
+              fol_key = key; fol_d2h = I->d2h; fol = it;
+            }
           }
         }
         if (open != iss_open.end()) {
