@@ -19,6 +19,7 @@ struct Alloc {
   int cls = 0;
   bool account_only = false;
   bool exported = false;   // pages handed to another process: never recycled through the cache
+  bool carved = false;     // a piece of a pool chunk (private writable data): no handle of its own
   CUdeviceptr va = 0;
   CUmemGenericAllocationHandle ph = 0;
 };
@@ -31,6 +32,27 @@ struct Pool {
   uint64_t vmm_gran = 2ull << 20;
   std::multimap<uint64_t, std::pair<CUdeviceptr, CUmemGenericAllocationHandle>> free_mapped;
   std::vector<std::pair<Alloc *, cudaEvent_t>> zombies;  // ledger-freed, pages pending an event
+  // private writable segments are carved from chunks mapped once: a fresh
+  // segment otherwise costs a cuMemCreate + cuMemSetAccess each (~0.2 ms,
+  // ms while the device's pages are first touched), which made the first
+  // burst of N concurrent invocations spend ~9 ms of host time per
+  // invocation (cfg 5 at N = 512).  Pieces are cached by size when freed and
+  // never unmapped; the chunks go at pool teardown.
+  struct Chunk {
+    CUdeviceptr va = 0;
+    CUmemGenericAllocationHandle ph = 0;
+    uint64_t live = 0;   // pieces handed out and not freed
+    uint64_t used = 0;   // bytes carved (an abandoned tail included)
+  };
+  std::vector<Chunk> chunks;
+  uint64_t chunk_bytes = 1ull << 30, carve_next = 0, carve_left = 0, carved = 0;
+  double carve_gb = -1;   // SAGE_POOL_CARVE_GB; < 0: half the budget
+  uint64_t carve_cap() const { return carve_gb >= 0 ? (uint64_t)(carve_gb * (1ull << 30)) : capacity / 2; }
+  Chunk *chunk_of(CUdeviceptr va) {
+    for (auto &c : chunks)
+      if (va >= c.va && va < c.va + chunk_bytes) return &c;
+    return nullptr;
+  }
 };
 
 static void unmap_segment(Pool *P, Alloc *A);
@@ -68,19 +90,59 @@ int pool_create(Gpu *G, uint64_t capacity) {
   size_t gran = 0;
   SAGE_CU(drv.MemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
   if (gran) P->vmm_gran = gran;
+  // chunk-carved private segments: at most half the budget (env SAGE_POOL_CARVE_GB)
+  const char *e = getenv("SAGE_POOL_CARVE_GB");
+  if (e) P->carve_gb = atof(e);
   G->pool = P;
   return SAGE_OK;
 }
 
-static void release_cache(Pool *P) {
-  for (auto &kv : P->free_mapped) {
-    drv.MemUnmap(kv.second.first, kv.first);
-    drv.MemAddressFree(kv.second.first, kv.first);
-    drv.MemRelease(kv.second.second);
-  }
-  P->free_mapped.clear();
-  P->cached = 0;
+static void release_chunk(Pool *P, const Pool::Chunk &c) {
+  drv.MemUnmap(c.va, P->chunk_bytes);
+  drv.MemAddressFree(c.va, P->chunk_bytes);
+  drv.MemRelease(c.ph);
 }
+
+// unmap every cached segment, and every chunk none of whose pieces is in use
+// (its cached pieces leave the cache with it); called under memory pressure
+static void release_cache(Pool *P) {
+  for (auto it = P->free_mapped.begin(); it != P->free_mapped.end();) {
+    if (!it->second.second) { ++it; continue; }   // carved piece: goes with its chunk
+    drv.MemUnmap(it->second.first, it->first);
+    drv.MemAddressFree(it->second.first, it->first);
+    drv.MemRelease(it->second.second);
+    P->cached -= it->first;
+    it = P->free_mapped.erase(it);
+  }
+  for (size_t k = 0; k < P->chunks.size();) {
+    Pool::Chunk c = P->chunks[k];
+    if (c.live) { ++k; continue; }
+    for (auto it = P->free_mapped.begin(); it != P->free_mapped.end();) {
+      if (it->second.first >= c.va && it->second.first < c.va + P->chunk_bytes) {
+        P->cached -= it->first;
+        it = P->free_mapped.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    P->carved -= c.used;
+    if (P->carve_left && P->carve_next >= c.va && P->carve_next <= c.va + P->chunk_bytes) {   // being carved
+      P->carve_left = 0;
+      P->carve_next = 0;
+    }
+    release_chunk(P, c);
+    P->chunks[k] = P->chunks.back();
+    P->chunks.pop_back();
+  }
+}
+
+static void release_chunks(Pool *P) {
+  for (auto &c : P->chunks) release_chunk(P, c);
+  P->chunks.clear();
+}
+
+// map `bytes` (granularity-rounded) of fresh pages at a fresh VA range
+static int map_fresh(Gpu *G, Pool *P, uint64_t bytes, CUdeviceptr *va, CUmemGenericAllocationHandle *ph);
 
 void pool_destroy(Gpu *G) {
   Pool *P = G->pool;
@@ -97,46 +159,32 @@ void pool_destroy(Gpu *G) {
     reap(P, true);
   }
   release_cache(P);
+  release_chunks(P);
   delete P;
   G->pool = nullptr;
 }
 
-static int map_segment(Gpu *G, Pool *P, Alloc *A) {
-  A->phys = round_up(A->bytes, P->vmm_gran);
-  // reuse a cached mapped segment of exactly this size: no driver call
-  {
-    auto it = P->free_mapped.find(A->phys);
-    if (it != P->free_mapped.end()) {
-      A->va = it->second.first;
-      A->ph = it->second.second;
-      P->free_mapped.erase(it);
-      P->cached -= A->phys;
-      P->physical += A->phys;
-      return SAGE_OK;
-    }
+static int map_fresh(Gpu *G, Pool *P, uint64_t bytes, CUdeviceptr *va, CUmemGenericAllocationHandle *ph) {
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = G->dev;
+  // exportable as a POSIX file descriptor: function processes map shared
+  // segments zero-copy (sage_pool_export / sage_segment_import)
+  static const bool shareable = [] { const char *e = getenv("SAGE_POOL_SHAREABLE"); return !(e && atoi(e) == 0); }();
+  if (shareable) prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUresult r = drv.MemCreate(ph, bytes, &prop, 0);
+  if (r == CUDA_ERROR_OUT_OF_MEMORY && (P->cached || !P->zombies.empty())) {
+    reap(P, true);
+    release_cache(P);
+    r = drv.MemCreate(ph, bytes, &prop, 0);
   }
-  if (!A->ph) {
-    CUmemAllocationProp prop{};
-    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    prop.location.id = G->dev;
-    // exportable as a POSIX file descriptor: function processes map shared
-    // segments zero-copy (sage_pool_export / sage_segment_import)
-    static const bool shareable = [] { const char *e = getenv("SAGE_POOL_SHAREABLE"); return !(e && atoi(e) == 0); }();
-    if (shareable) prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-    CUresult r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
-    if (r == CUDA_ERROR_OUT_OF_MEMORY && (P->cached || !P->zombies.empty())) {
-      reap(P, true);
-      release_cache(P);
-      r = drv.MemCreate(&A->ph, A->phys, &prop, 0);
-    }
-    if (r != CUDA_SUCCESS) { A->ph = 0; return cu_fail(r, "cuMemCreate"); }
-  }
-  CUresult r = drv.MemAddressReserve(&A->va, A->phys, P->vmm_gran, 0, 0);
-  if (r != CUDA_SUCCESS) { drv.MemRelease(A->ph); A->ph = 0; return cu_fail(r, "cuMemAddressReserve"); }
-  r = drv.MemMap(A->va, A->phys, 0, A->ph, 0);
+  if (r != CUDA_SUCCESS) { *ph = 0; return cu_fail(r, "cuMemCreate"); }
+  r = drv.MemAddressReserve(va, bytes, P->vmm_gran, 0, 0);
+  if (r != CUDA_SUCCESS) { drv.MemRelease(*ph); *ph = 0; return cu_fail(r, "cuMemAddressReserve"); }
+  r = drv.MemMap(*va, bytes, 0, *ph, 0);
   if (r != CUDA_SUCCESS) {
-    drv.MemAddressFree(A->va, A->phys); drv.MemRelease(A->ph); A->ph = 0; A->va = 0;
+    drv.MemAddressFree(*va, bytes); drv.MemRelease(*ph); *ph = 0; *va = 0;
     return cu_fail(r, "cuMemMap");
   }
   std::vector<CUmemAccessDesc> acc;
@@ -148,12 +196,65 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
     a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
     acc.push_back(a);
   }
-  r = drv.MemSetAccess(A->va, A->phys, acc.data(), acc.size());
+  r = drv.MemSetAccess(*va, bytes, acc.data(), acc.size());
   if (r != CUDA_SUCCESS) {
-    drv.MemUnmap(A->va, A->phys); drv.MemAddressFree(A->va, A->phys); drv.MemRelease(A->ph);
-    A->ph = 0; A->va = 0;
+    drv.MemUnmap(*va, bytes); drv.MemAddressFree(*va, bytes); drv.MemRelease(*ph);
+    *ph = 0; *va = 0;
     return cu_fail(r, "cuMemSetAccess");
   }
+  return SAGE_OK;
+}
+
+static int map_segment(Gpu *G, Pool *P, Alloc *A) {
+  A->phys = round_up(A->bytes, P->vmm_gran);
+  // reuse a cached mapped segment of exactly this size: no driver call
+  {
+    // (a carved piece has no handle of its own: only private writable data reuses one)
+    auto rng = P->free_mapped.equal_range(A->phys);
+    auto it = rng.first;
+    if (A->cls != SAGE_CLASS_WRITABLE)
+      while (it != rng.second && !it->second.second) ++it;
+    if (it != rng.second) {
+      A->va = it->second.first;
+      A->ph = it->second.second;
+      A->carved = A->ph == 0;
+      if (A->carved) P->chunk_of(A->va)->live++;
+      P->free_mapped.erase(it);
+      P->cached -= A->phys;
+      P->physical += A->phys;
+      return SAGE_OK;
+    }
+  }
+  // private writable data: a piece of a chunk (see Pool::chunks)
+  if (A->cls == SAGE_CLASS_WRITABLE && A->phys <= P->chunk_bytes / 4 && P->carved + A->phys <= P->carve_cap()) {
+    if (P->carve_left < A->phys) {
+      // (the old chunk's uncarved tail stays unused: at most a quarter chunk)
+      Pool::Chunk c;
+      if (map_fresh(G, P, P->chunk_bytes, &c.va, &c.ph) == SAGE_OK) {
+        if (P->carve_left) {          // the abandoned tail counts as carved
+          if (Pool::Chunk *old = P->chunk_of(P->carve_next)) old->used += P->carve_left;
+          P->carved += P->carve_left;
+        }
+        P->chunks.push_back(c);
+        P->carve_next = c.va;
+        P->carve_left = P->chunk_bytes;
+      }
+    }
+    if (P->carve_left >= A->phys) {
+      A->va = P->carve_next;
+      A->ph = 0;
+      A->carved = true;
+      Pool::Chunk *ck = P->chunk_of(A->va);
+      ck->live++;
+      ck->used += A->phys;
+      P->carve_next += A->phys;
+      P->carve_left -= A->phys;
+      P->carved += A->phys;
+      P->physical += A->phys;
+      return SAGE_OK;
+    }
+  }
+  SAGE_TRY(map_fresh(G, P, A->phys, &A->va, &A->ph));
   P->physical += A->phys;
   return SAGE_OK;
 }
@@ -169,7 +270,8 @@ static void unmap_segment(Pool *P, Alloc *A) {
   // cuMemCreate+Map / Unmap+Release (~150-250 us of host time each), which
   // halved cfg-3 throughput; a cuMemCreate that finds the HBM held by the
   // cache releases it and retries (map_segment)
-  if (!A->exported && P->cached + A->phys + P->physical <= P->capacity + (4ull << 30)) {
+  if (A->carved) P->chunk_of(A->va)->live--;
+  if (A->carved || (!A->exported && P->cached + A->phys + P->physical <= P->capacity + (4ull << 30))) {
     P->free_mapped.emplace(A->phys, std::make_pair(A->va, A->ph));
     P->cached += A->phys;
   } else {
@@ -468,7 +570,9 @@ int sage::pool_alloc_phys(sage_handle h, CUmemGenericAllocationHandle *ph, uint6
   auto it = g_allocs.find(h & ((1ull << 56) - 1));
   if (it == g_allocs.end()) return fail(SAGE_ESTATE, "unknown pool handle");
   const Alloc *A = it->second;
-  if (A->account_only || !A->ph) return fail(SAGE_EINVAL, "allocation has no device pages");
+  if (A->account_only || !A->ph)
+    return fail(SAGE_EINVAL, A->carved ? "allocation is a piece of a pool chunk (private writable data): no pages of its own"
+                                       : "allocation has no device pages");
   *ph = A->ph;
   *phys = A->phys;
   *dptr = (uint64_t)A->va;
@@ -502,6 +606,7 @@ extern "C" int sage_pool_export(sage_handle h, int *fd, uint64_t *phys_bytes) {
     auto it = g_allocs.find(h & ((1ull << 56) - 1));
     if (handle_kind(h) == Kind::Alloc && it != g_allocs.end()) A = it->second;
   }
+  if (A && A->carved) return fail(SAGE_EINVAL, "pool_export: private writable segments are carved from pool chunks");
   if (!A || !A->ph) return fail(SAGE_ESTATE, "pool_export: unknown or unmapped segment");
   int out = -1;
   SAGE_CU(drv.MemExportToShareableHandle(&out, A->ph, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));

@@ -122,26 +122,68 @@ def synthetic_data(spec: FunctionSpec, tensors: int = 16) -> FunctionData:
     return FunctionData(layout, db, "touch", (), inp, 16)
 
 
+class _SlabBuffer(D.PinnedBuffer):
+    """A size-class slot carved from a pinned slab (no handle of its own)."""
+
+    def __init__(self, ptr: int, cap: int):   # noqa: super().__init__ would allocate
+        self.h, self.ptr, self.nbytes, self.cap = 0, ptr, cap, cap
+
+    def free(self) -> None:
+        pass
+
+
 class _PinnedPool:
-    """Reuse pinned host buffers by size (cudaHostAlloc costs ms per 100 MiB)."""
+    """Reuse pinned host buffers.  cudaHostAlloc costs ~0.4 ms however small
+    the buffer (ms per 100 MiB), so buffers up to SMALL bytes come from 64 MiB
+    slabs in power-of-two size classes: the first burst of N concurrent
+    invocations pays one host allocation per slab, not one per return buffer
+    (cfg 5 at N = 512: the first burst's submit took ~1 s); larger ones are
+    cached by exact size."""
+
+    SMALL = 16 << 20
+    SLAB = 64 << 20
 
     def __init__(self):
         self.free: dict[int, list] = {}
+        self.small: dict[int, list] = {}
+        self.slabs: list = []
+
+    @staticmethod
+    def _cls(nbytes: int) -> int:
+        return max(4096, 1 << (max(1, nbytes) - 1).bit_length())
 
     def get(self, nbytes: int) -> D.PinnedBuffer:
+        if nbytes <= self.SMALL:
+            c = self._cls(nbytes)
+            lst = self.small.get(c)
+            if not lst:
+                slab = D.PinnedBuffer(self.SLAB)
+                self.slabs.append(slab)
+                lst = self.small.setdefault(c, [])
+                lst.extend(_SlabBuffer(slab.ptr + k * c, c) for k in range(self.SLAB // c))
+            buf = lst.pop()
+            buf.nbytes = nbytes
+            return buf
         lst = self.free.get(nbytes)
         if lst:
             return lst.pop()
         return D.PinnedBuffer(nbytes)
 
     def put(self, buf: D.PinnedBuffer) -> None:
-        self.free.setdefault(buf.nbytes, []).append(buf)
+        if isinstance(buf, _SlabBuffer):
+            self.small.setdefault(buf.cap, []).append(buf)
+        else:
+            self.free.setdefault(buf.nbytes, []).append(buf)
 
     def close(self) -> None:
         for lst in self.free.values():
             for b in lst:
                 b.free()
         self.free.clear()
+        self.small.clear()
+        for slab in self.slabs:
+            slab.free()
+        self.slabs.clear()
 
 
 class _PlanFacts:
