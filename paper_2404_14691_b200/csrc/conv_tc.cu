@@ -36,18 +36,19 @@ constexpr int CV_BM = 128;       // output pixels per CTA (UMMA M)
 constexpr int CV_BK = 64;        // bf16 per K-block = one 128-B row
 constexpr int CV_THREADS = 192;
 
-template <int BN, int SHORT = 0>
+template <int BN, int SHORT = 0, int PAIR = 0>
 struct CvSmem {
   static constexpr int A_BYTES = CV_BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * 128;   // PAIR: this CTA's half of the filter tile
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // shallow enough for two CTAs per SM at BN <= 128: a batch-8 layer is
   // gather-latency bound, so resident CTAs (memory parallelism) beat depth
   // BN = 256: 4 stages (196 KB, one CTA per SM) for the long-K layers; SHORT
   // (a few K-blocks) keeps 2 stages (98 KB) so two CTAs share an SM and one's
   // prologue / epilogue overlaps the other's K loop
-  static constexpr int STAGES = SHORT ? 2 : (BN >= 256 ? 4 : BN >= 128 ? 3 : 4);
-  static constexpr int TOTAL = STAGES * STAGE + 1024 + 256 + 2 * 256 * 4;
+  // PAIR halves the filter tile per CTA (32 KB stages): 3 short / 6 long
+  static constexpr int STAGES = PAIR ? (SHORT ? 3 : 6) : SHORT ? 2 : (BN >= 256 ? 4 : BN >= 128 ? 3 : 4);
+  static constexpr int TOTAL = STAGES * STAGE + 1024 + 512 + 2 * 256 * 4;
 };
 
 __device__ __forceinline__ uint32_t cv_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -83,10 +84,19 @@ struct ConvArgs {
   int N, H, W, C, P, Q, R, S, stride, pad, Cout, M, KB, relu;
 };
 
-template <int BN, int C4, int SHORT = 0>
+// PAIR: CTAs 2j, 2j+1 of a cluster (adjacent M tiles) run one M = 256 tile
+// as a CTA pair: each gathers its own 128 pixel rows and TMA-loads HALF of
+// the filter tile (BN/2 output channels), the leader issues
+// tcgen05.mma.cta_group::2 over both CTAs' shared memory and commits to both
+// CTAs' barriers.  Per SM the filter bytes per K-block halve -- the batch-8
+// layers are bound by L2 -> SM traffic (widest-BN tiles win for the same
+// reason).  The peer's stage readiness reaches the leader through a relay
+// thread (its warp 1) that waits on the peer's own full barrier and arrives
+// on the leader's pfull barrier.  Each CTA's TMEM holds its 128 rows.
+template <int BN, int C4, int SHORT = 0, int PAIR = 0>
 __global__ void __launch_bounds__(CV_THREADS, 2)
     conv_bf16_kernel(const __grid_constant__ CUtensorMap mapW, const ConvArgs a) {
-  using Sm = CvSmem<BN, SHORT>;
+  using Sm = CvSmem<BN, SHORT, PAIR>;
   constexpr int ST = Sm::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -95,12 +105,16 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * Sm::STAGE);
   uint64_t *empty = full + ST;
   uint64_t *tmem_full = empty + ST;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
-  float *s_scale = reinterpret_cast<float *>(smem + ST * Sm::STAGE + 256);
+  uint64_t *pfull = tmem_full + 1;   // PAIR (leader): the peer's stage is ready
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pfull + ST);
+  float *s_scale = reinterpret_cast<float *>(smem + ST * Sm::STAGE + 512);
   float *s_bias = s_scale + 256;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * CV_BM, n0 = blockIdx.y * BN;
+  uint32_t crank = 0;
+  if constexpr (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const uint32_t prank = crank & 1u, leader = crank & ~1u;
   const __nv_bfloat16 *X = a.x, *RES = a.res;
   __nv_bfloat16 *OUT = a.out;
   if (a.frame) {
@@ -117,12 +131,21 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(&empty[s])), "r"(1));
       }
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(tmem_full)), "r"(1));
+      if constexpr (PAIR)
+        for (int s = 0; s < ST; ++s)
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(&pfull[s])), "r"(1));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cv_smem(tmem_slot)),
-                 "r"(BN < 32 ? 32 : BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cv_smem(tmem_slot)),
+                   "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cv_smem(tmem_slot)),
+                   "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (warp >= 2) {
     // folded batch-norm of this CTA's channels
@@ -139,6 +162,8 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (PAIR)   // both CTAs' barriers exist before any remote arrive / multicast commit
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const int KB = a.KB;
@@ -155,34 +180,76 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
                 cv_smem(sB + s * Sm::B_BYTES)),
-            "l"(reinterpret_cast<uint64_t>(&mapW)), "r"(cv_smem(&full[s])), "r"(kb * CV_BK), "r"(n0)
+            "l"(reinterpret_cast<uint64_t>(&mapW)), "r"(cv_smem(&full[s])), "r"(kb * CV_BK),
+            "r"(n0 + (int)prank * (BN / 2))
             : "memory");
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer ----
-      const uint32_t idesc = bf16_idesc<BN>();
+    if (PAIR && lane == 0 && prank == 1) {
+      // ---- peer: relay each landed stage to the leader's MMA issuer ----
+      uint32_t ra;
       for (int kb = 0; kb < KB; ++kb) {
         const int s = kb % ST, round = kb / ST;
         cv_wait(&full[s], round & 1);
+        asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(cv_smem(&pfull[s])), "r"(leader));
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+      }
+    }
+    if (lane == 0 && prank == 0) {
+      // ---- MMA issuer (PAIR: the leader's, over both CTAs) ----
+      const uint32_t idesc = PAIR ? ((bf16_idesc<BN>() & ~(0x1Fu << 24)) | ((uint32_t)(2 * CV_BM >> 4) << 24))
+                                  : bf16_idesc<BN>();
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % ST, round = kb / ST;
+        cv_wait(&full[s], round & 1);
+        if constexpr (PAIR) {
+          asm volatile(
+              "{\n\t.reg .pred P1;\n\t"
+              "WP_%=:\n\t"
+              "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+              "@!P1 bra WP_%=;\n\t}" ::"r"(cv_smem(&pfull[s])),
+              "r"(round & 1)
+              : "memory");
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint64_t da = cv_desc(cv_smem(sA + s * Sm::A_BYTES)), db = cv_desc(cv_smem(sB + s * Sm::B_BYTES));
 #pragma unroll
         for (int k = 0; k < CV_BK / 16; ++k) {   // K = 16 bf16 = 32 B per MMA: +2 in 16-B units
           const uint32_t acc = (kb | k) ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc));
+          if constexpr (PAIR)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc));
+          else
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         cv_smem(&empty[s]))
-                     : "memory");
+        if constexpr (PAIR)
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  cv_smem(&empty[s])),
+              "h"((uint16_t)(0x3u << leader))
+              : "memory");
+        else
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           cv_smem(&empty[s]))
+                       : "memory");
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       cv_smem(tmem_full))
-                   : "memory");
+      if constexpr (PAIR)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                cv_smem(tmem_full)),
+            "h"((uint16_t)(0x3u << leader))
+            : "memory");
+      else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         cv_smem(tmem_full))
+                     : "memory");
     }
   } else {
     // ---- im2col gather ----
@@ -324,9 +391,14 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (PAIR)   // both CTAs are done with the pair's TMEM and each other's barriers
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
   }
 }
 
@@ -397,12 +469,27 @@ static int smem_optin(const void *fn, int bytes) {
   return SAGE_OK;
 }
 
-template <int BN, int C4, int SHORT = 0>
+template <int BN, int C4, int SHORT = 0, int PAIR = 0>
 static int launch_conv(const CUtensorMap &map, const ConvArgs &a, cudaStream_t s) {
-  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<BN, C4, SHORT>, CvSmem<BN, SHORT>::TOTAL));
-  dim3 grid((a.M + CV_BM - 1) / CV_BM, a.Cout / BN);
-  conv_bf16_kernel<BN, C4, SHORT><<<grid, CV_THREADS, CvSmem<BN, SHORT>::TOTAL, s>>>(map, a);
-  SAGE_CUDA(cudaGetLastError());
+  using Sm = CvSmem<BN, SHORT, PAIR>;
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<BN, C4, SHORT, PAIR>, Sm::TOTAL));
+  int mt = (a.M + CV_BM - 1) / CV_BM;
+  if (PAIR) mt += mt & 1;   // whole pairs (a trailing tile past M gathers zeros and stores nothing)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(mt, a.Cout / BN);
+  cfg.blockDim = dim3(CV_THREADS);
+  cfg.dynamicSmemBytes = Sm::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (PAIR) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  SAGE_CUDA(cudaLaunchKernelEx(&cfg, conv_bf16_kernel<BN, C4, SHORT, PAIR>, map, a));
   return SAGE_OK;
 }
 
@@ -453,14 +540,22 @@ int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame 
   const uint64_t ktot = c4 ? (uint64_t)((d->r * d->s + 15) / 16) * CV_BK : (uint64_t)d->r * d->s * d->cin;
   a.KB = (int)(ktot / CV_BK);
   const int bn = pick_bn((a.M + CV_BM - 1) / CV_BM, a.Cout, sms);
-  CUtensorMap map;
-  SAGE_TRY(filter_map(&map, d->w, (uint64_t)d->cout, ktot, (uint32_t)bn));
-  if (c4) return bn == 64 ? launch_conv<64, 1>(map, a, s) : launch_conv<128, 1>(map, a, s);
   // SAGE_CONV_SHORT_KB: layers with at most this many K-blocks take the
   // 2-stage BN = 256 kernel (two CTAs per SM)
   static const int short_kb = [] { const char *e = getenv("SAGE_CONV_SHORT_KB"); return e ? atoi(e) : 8; }();
   static const bool short_all = [] { const char *e = getenv("SAGE_CONV_SHORT_ALL"); return e && atoi(e) != 0; }();
   const bool shrt = a.KB <= short_kb;
+  // SAGE_CONV_PAIR=1: BN = 256 tiles as CTA pairs (cta_group::2, half the filter tile per SM).
+  // Opt-in: parity-tested but measured slower (16 concurrent forwards 27.8k vs
+  // 34.2k images/s; layer4 3x3 86 vs 40 us, profiles/r2_conv_pair_ab.txt) --
+  // the peer's readiness reaches the leader's MMA through a relay thread and a
+  // cluster-scope barrier, which the K loop does not hide
+  static const bool pair_on = [] { const char *e = getenv("SAGE_CONV_PAIR"); return e && atoi(e) != 0; }();
+  const bool pair = !c4 && bn == 256 && pair_on;
+  CUtensorMap map;   // a pair's CTA loads BN/2 filter rows per K-block
+  SAGE_TRY(filter_map(&map, d->w, (uint64_t)d->cout, ktot, (uint32_t)(pair ? bn / 2 : bn)));
+  if (c4) return bn == 64 ? launch_conv<64, 1>(map, a, s) : launch_conv<128, 1>(map, a, s);
+  if (pair) return shrt ? launch_conv<256, 0, 1, 1>(map, a, s) : launch_conv<256, 0, 0, 1>(map, a, s);
   if (bn == 256) return shrt ? launch_conv<256, 0, 1>(map, a, s) : launch_conv<256, 0>(map, a, s);
   if (bn == 128) return shrt && short_all ? launch_conv<128, 0, 1>(map, a, s) : launch_conv<128, 0>(map, a, s);
   return shrt && short_all ? launch_conv<64, 0, 1>(map, a, s) : launch_conv<64, 0>(map, a, s);
@@ -471,6 +566,8 @@ int conv_optin_all() {
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 0>, CvSmem<128>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0>, CvSmem<256>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0, 1>, CvSmem<256, 1>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0, 1, 1>, CvSmem<256, 1, 1>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<256, 0, 0, 1>, CvSmem<256, 0, 1>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 0, 1>, CvSmem<128, 1>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 0, 1>, CvSmem<64, 1>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 1>, CvSmem<64>::TOTAL));
@@ -484,6 +581,8 @@ int touch_conv_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 0>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0, 1>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0, 1, 1>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<256, 0, 0, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 0, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 0, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 1>));

@@ -138,3 +138,18 @@ def test_conv_rejects_bad_shapes(dp):
     import torch
     with pytest.raises(_lib.SageError):
         run_conv(torch.randn(1, 8, 8, 48), torch.randn(64, 1, 1, 48), None, None, 1, 0, False)   # Cin % 64
+
+
+def test_conv_cta_pair_variant():
+    """SAGE_CONV_PAIR=1 (BN = 256 tiles as cta_group::2 CTA pairs, half the
+    filter tile per SM; opt-in, measured slower): the same parity, in its own
+    process because the variant is chosen at library load."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_conv_gpu.py"), "-x", "-q",
+                        "-k", "matches_torch_cpu"], env={**os.environ, "SAGE_CONV_PAIR": "1"}, cwd=str(root),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
