@@ -218,7 +218,9 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
       A->va = it->second.first;
       A->ph = it->second.second;
       A->carved = A->ph == 0;
-      if (A->carved) P->chunk_of(A->va)->live++;
+      if (A->carved) {
+        if (Pool::Chunk *c = P->chunk_of(A->va)) c->live++;
+      }
       P->free_mapped.erase(it);
       P->cached -= A->phys;
       P->physical += A->phys;
@@ -244,9 +246,8 @@ static int map_segment(Gpu *G, Pool *P, Alloc *A) {
       A->va = P->carve_next;
       A->ph = 0;
       A->carved = true;
-      Pool::Chunk *ck = P->chunk_of(A->va);
-      ck->live++;
-      ck->used += A->phys;
+      Pool::Chunk *ck = P->chunk_of(A->va);   // the chunk just carved from
+      if (ck) { ck->live++; ck->used += A->phys; }
       P->carve_next += A->phys;
       P->carve_left -= A->phys;
       P->carved += A->phys;
@@ -270,7 +271,9 @@ static void unmap_segment(Pool *P, Alloc *A) {
   // cuMemCreate+Map / Unmap+Release (~150-250 us of host time each), which
   // halved cfg-3 throughput; a cuMemCreate that finds the HBM held by the
   // cache releases it and retries (map_segment)
-  if (A->carved) P->chunk_of(A->va)->live--;
+  if (A->carved) {
+    if (Pool::Chunk *c = P->chunk_of(A->va)) c->live--;
+  }
   if (A->carved || (!A->exported && P->cached + A->phys + P->physical <= P->capacity + (4ull << 30))) {
     P->free_mapped.emplace(A->phys, std::make_pair(A->va, A->ph));
     P->cached += A->phys;
