@@ -668,7 +668,8 @@ def our_arm(args, rank, world, dist) -> dict:
     table, data = cfg2_functions()
     names = burst_names(table, args.burst)
     cc = args.compute_concurrency or None
-    sim = Simulation(ClusterSpec(gpus=1, compute_concurrency=cc), policy_preset("SAGE"), table, seed=1,
+    sim = Simulation(ClusterSpec(gpus=1, compute_concurrency=cc, chunk_mb=args.chunk_mb,
+                                 staging_mb=args.chunk_mb * 8), policy_preset("SAGE"), table, seed=1,
                      function_data=data, copy_results=False)
     box = None
     fanout_note = None
@@ -925,6 +926,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--burst", type=int, default=64)
     ap.add_argument("--no-cfg1", action="store_true")
+    ap.add_argument("--chunk-mb", type=float, default=8.0,
+                    help="staged-load chunk (one H2D + one land launch each; the ring holds 8)")
     ap.add_argument("--compute-concurrency", type=int, default=0,
                     help="ComputeGate slots per GPU (functions.py:304-327; 0 = no gate)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

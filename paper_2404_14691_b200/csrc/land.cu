@@ -587,8 +587,14 @@ int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCu
   G->scratch.h_res[L->acc_idx] = 0;   // an empty load publishes nothing
   uint8_t *dst = reinterpret_cast<uint8_t *>(d->dst);
 
-  if (!d->layout && !dev_src && (d->flags & SAGE_LOAD_SRC_PINNED) && d->src_bytes &&
-      lay->seg / 16 < 0xFFFFFFFFull) {
+  // the same for an unverified identity load from this GPU's HBM (a private
+  // request payload already on the device): one D2D copy, as the e2e path's
+  // H2D DMA, instead of a land launch: a 4 MiB land is latency bound at
+  // ~8 us under ncu (plan-table lookups, a one-wave grid, the result publish)
+  const bool d2d = !d->layout && (d->flags & SAGE_LOAD_SRC_DEVICE) && !(d->flags & SAGE_LOAD_SRC_PEER) &&
+                   (d->flags & SAGE_LOAD_NO_VERIFY) && d->src_bytes;
+  if (d2d || (!d->layout && !dev_src && (d->flags & SAGE_LOAD_SRC_PINNED) && d->src_bytes &&
+              lay->seg / 16 < 0xFFFFFFFFull)) {
     // direct path: an identity load from pinned memory needs no staging or
     // unpack -- one DMA straight into dst on its own stream (so it never
     // queues behind memcpy-gated ring chunks) + a read-only verify pass on a
@@ -600,8 +606,8 @@ int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCu
     L->has_gpu_begin = true;
     const uint64_t n = d->src_bytes, seg = lay->seg;
     if (seg > n) SAGE_CUDA(cudaMemsetAsync(dst + n, 0, seg - n, s));
-    SAGE_CUDA(cudaMemcpyAsync(dst, d->src, n, cudaMemcpyHostToDevice, s));
-    L->link_bytes = n;
+    SAGE_CUDA(cudaMemcpyAsync(dst, d->src, n, d2d ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (!d2d) L->link_bytes = n;
     L->chunks = 1;
     if (!(d->flags & SAGE_LOAD_NO_VERIFY)) {
       SAGE_CUDA(cudaEventRecord(G->ev_dma, s));

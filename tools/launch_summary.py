@@ -20,6 +20,24 @@ def summarise(path):
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k:28s} {len(v):8d} {sum(v):12.1f} {sum(v) / len(v):9.2f} {max(v):9.2f} {sum(v) / tot:6.3f}")
     lines.append(f"{'(all)':28s} {sum(len(v) for v in agg.values()):8d} {tot:12.1f}")
+    # with launch__grid_size in the list: land launches by grid (staged chunk lands vs segment-sized ones)
+    grid, dur = {}, {}
+    for r in rows:
+        if not r["Kernel Name"].startswith("land_kernel"):
+            continue
+        if r["Metric Name"] == "launch__grid_size":
+            grid[r["ID"]] = int(float(r["Metric Value"].replace(",", "")))
+        elif r["Metric Name"] == "gpu__time_duration.sum":
+            scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3}.get(r["Metric Unit"], 1e-3)
+            dur[r["ID"]] = float(r["Metric Value"].replace(",", "")) * scale
+    if grid:
+        by = defaultdict(list)
+        for i, g in grid.items():
+            if i in dur:
+                by[g].append(dur[i])
+        lines.append("land_kernel by grid size (blocks: launches, mean_us)")
+        for g in sorted(by):
+            lines.append(f"  grid {g:6d}: {len(by[g]):5d} launches, mean {sum(by[g]) / len(by[g]):9.2f} us")
     return "\n".join(lines)
 
 
