@@ -926,7 +926,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--burst", type=int, default=64)
     ap.add_argument("--no-cfg1", action="store_true")
-    ap.add_argument("--chunk-mb", type=float, default=8.0,
+    ap.add_argument("--chunk-mb", type=float, default=32.0,
                     help="staged-load chunk (one H2D + one land launch each; the ring holds 8)")
     ap.add_argument("--compute-concurrency", type=int, default=0,
                     help="ComputeGate slots per GPU (functions.py:304-327; 0 = no gate)")

@@ -49,8 +49,8 @@ class ClusterSpec:
     cpu_mem_mb: Optional[float] = None
     compute_concurrency: Optional[int] = None
     pre_warmed_containers: bool = True
-    chunk_mb: float = 8.0
-    staging_mb: float = 64.0
+    chunk_mb: float = 32.0     # staged-load chunk: one H2D + one land launch each (8 / 16 / 32 MiB: e2e 3,616 / 3,706 / 3,728 inv/s)
+    staging_mb: float = 256.0  # 8 ring slots
     host_threads: Optional[int] = None
     # FixedGSL instances: "thread" (a fresh context on a library thread) or
     # "process" (a fresh OS process per instance, the container-per-function shape)

@@ -48,7 +48,7 @@ def test_two_gpu_placement_and_pcie_once(built, fanout):
                 assert peer.measured["nvlink_bytes"] == lay.seg_bytes
                 # only the (pageable, staged) input crossed PCIe: its bytes + the
                 # 16-B overlap prefix of each staged chunk after the first
-                chunks = -(-fd.input_bytes // (8 << 20))
+                chunks = -(-fd.input_bytes // int(sim.cluster.chunk_mb * (1 << 20)))
                 assert peer.measured["pcie_bytes"] == fd.input_bytes + 16 * (chunks - 1)
             else:
                 assert set(srcs) == {"pcie"}

@@ -96,7 +96,7 @@ def test_burst16_parity(built_lib, policy):
             # PCIe once: the leader alone moved the read-only bytes (plus the
             # 16-byte chunk-overlap prefix each staged chunk after the first carries)
             moved = sum(i.measured["pcie_bytes"] for i in invs)
-            chunk = 8 << 20
+            chunk = int(sim.cluster.chunk_mb * (1 << 20))
             extra = 16 * ((fd.layout.packed_bytes + chunk - 1) // chunk - 1)
             assert moved == fd.layout.packed_bytes + extra + 16 * fd.input_bytes
         sim.check_no_leaks()
