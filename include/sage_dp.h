@@ -96,6 +96,12 @@ int sage_pool_free_after_n(sage_handle h, const sage_handle *evs, int n);
 int sage_pool_effective(int gpu, uint64_t bytes, uint64_t *effective);
 int sage_pool_usage(int gpu, uint64_t by_class[4], uint64_t *ledger_total,
                     uint64_t *physical_total, uint64_t *capacity);
+/* give the pages of freed segments back to the device: the size-keyed cache
+ * of mapped free segments and every chunk (private writable segments are
+ * carved from 1 GiB chunks) none of whose pieces is live; what a cuMemCreate
+ * that finds the HBM full does by itself.  *released: bytes unmapped.
+ * (new: the reference's ledger holds no pages, resources.py:271-337)      */
+int sage_pool_trim(int gpu, uint64_t *released);
 /* map an existing segment into another GPU's address space is implicit when
  * SAGE_INIT_PEER_ACCESS is set; this returns the (shared) VA               */
 int sage_pool_dptr(sage_handle h, uint64_t *dptr, uint64_t *bytes);

@@ -173,6 +173,7 @@ _SIGS = {
     "sage_pool_free_after_n": (C.c_int, [H, C.POINTER(H), C.c_int]),
     "sage_pool_effective": (C.c_int, [C.c_int, u64, C.POINTER(u64)]),
     "sage_pool_usage": (C.c_int, [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+    "sage_pool_trim": (C.c_int, [C.c_int, C.POINTER(u64)]),
     "sage_pool_dptr": (C.c_int, [H, C.POINTER(u64), C.POINTER(u64)]),
     "sage_host_alloc": (C.c_int, [u64, C.POINTER(H), C.POINTER(C.c_void_p)]),
     "sage_host_free": (C.c_int, [H]),

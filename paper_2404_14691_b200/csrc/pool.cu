@@ -415,6 +415,21 @@ int sage_pool_configure(int gpu, uint64_t capacity, uint64_t granularity) {
   return SAGE_OK;
 }
 
+int sage_pool_trim(int gpu, uint64_t *released) {
+  SAGE_TRY(require_up());
+  Gpu *G = gpu_get(gpu);
+  if (!G) return fail(SAGE_ENODEV, "pool_trim: bad gpu");
+  Pool *P = G->pool;
+  std::lock_guard<std::mutex> lk(P->mu);
+  cudaSetDevice(dev_of(gpu));
+  reap(P, false);
+  const uint64_t before = P->cached + (uint64_t)P->chunks.size() * P->chunk_bytes;
+  release_cache(P);
+  const uint64_t after = P->cached + (uint64_t)P->chunks.size() * P->chunk_bytes;
+  if (released) *released = before - after;
+  return SAGE_OK;
+}
+
 int sage_pool_effective(int gpu, uint64_t bytes, uint64_t *effective) {
   SAGE_TRY(require_up());
   Gpu *G = gpu_get(gpu);

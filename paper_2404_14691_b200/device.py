@@ -116,6 +116,13 @@ def pool_usage(gpu: int) -> dict:
     return {"by_class": list(by), "ledger": tot.value, "physical": phys.value, "capacity": cap.value}
 
 
+def pool_trim(gpu: int) -> int:
+    """Unmap the pool's cached free segments and idle chunks; bytes released."""
+    r = C.c_uint64()
+    check(lib().sage_pool_trim(gpu, C.byref(r)), "sage_pool_trim")
+    return r.value
+
+
 # ------------------------------------------------------------ host buffers --
 class PinnedBuffer:
     """Pinned host memory owned by the library, viewable as numpy."""

@@ -151,3 +151,40 @@ def test_issuer_results_match_oracle(built):
                                   seg[o_col:o_col + 4 * nnz].view(np.int32), seg[o_val:o_val + 4 * nnz].view(np.float32),
                                   x.view(np.float32))
                 np.testing.assert_allclose(i.result.view(np.float32)[:rows], want, rtol=1e-3, atol=1e-4)
+
+
+def test_issuer_backlog_beyond_scan_window():
+    """A burst far larger than the issuer's pick window (256 waiting
+    invocations): two functions, so the window fills with followers while a
+    leader waits further back; every invocation completes, each function's
+    segment crosses PCIe once, every landed copy is the oracle's."""
+    code = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_2404_14691_b200.experiments import synthetic_function
+from paper_2404_14691_b200.policies import policy_preset
+from paper_2404_14691_b200.runtime import ClusterSpec, Simulation
+a, da = synthetic_function("fa", 8, 1, 0.0625, tensors=7)
+b, db = synthetic_function("fb", 24, 1, 0.0625, tensors=9)
+sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), {"fa": a, "fb": b}, seed=5,
+                 function_data={"fa": da, "fb": db}, copy_results=False)
+try:
+    names = ["fa"] * 400 + ["fb"] * 400
+    invs = sim.submit_many(names)
+    sim.drain()
+    assert all(i.outcome == "completed" for i in invs), [i.fail_reason for i in invs if i.outcome != "completed"][:3]
+    for fn, fd in (("fa", da), ("fb", db)):
+        lay = fd.layout
+        _, want = O.land_c(fd.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+        mine = [i for i in invs if i.spec.name == fn]
+        assert sim.sharing.ro_loads_performed[(fn, 0)] == 1   # PCIe once for the burst
+        assert any(i.ro_checksum == want for i in mine)
+        assert all(i.ro_checksum in (None, want) for i in mine)
+    sim.check_no_leaks()
+finally:
+    sim.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code, str(ROOT)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]

@@ -117,6 +117,40 @@ def test_pool_denied_and_usage(dp):
         D._lib.check(D.lib().sage_pool_free(s.h or 0x0300000000000001), "double free")
 
 
+def test_pool_chunk_carving_and_trim(dp):
+    """Private writable segments are carved from 1 GiB pool chunks: pieces
+    never overlap (each keeps its own bytes), are reused by size once freed,
+    cannot be exported (no handle of their own), and sage_pool_trim gives the
+    chunks back once no piece is live."""
+    import ctypes as Cc
+    D.pool_trim(0)
+    n, size = 24, 100 << 20                      # 2.4 GB: three chunks
+    segs, pats = [], []
+    for k in range(n):
+        s = D.pool_alloc(0, size, D._lib.CLASS_WRITABLE)
+        pat = np.full(size, (37 * k + 11) & 0xFF, dtype=np.uint8)
+        op = D.load(0, s.dptr, pat, None)
+        op.wait()
+        op.release()
+        segs.append(s)
+        pats.append(pat[0])
+    for s, v in zip(segs, pats):
+        got = D.read_device(0, s.dptr, size)
+        assert got[0] == v and got[-1] == v and np.all(got[::4096] == v)
+    fd, ph = Cc.c_int(), D._lib.u64()
+    rc = D.lib().sage_pool_export(segs[0].h, Cc.byref(fd), Cc.byref(ph))
+    assert rc == D._lib.SAGE_EINVAL           # a carved piece has no pages of its own to export
+    ptrs = {s.dptr for s in segs}
+    for s in segs:
+        s.free()
+    again = D.pool_alloc(0, size, D._lib.CLASS_WRITABLE)   # a freed piece of the same size
+    assert again.dptr in ptrs
+    again.free()
+    released = D.pool_trim(0)
+    assert released >= n * size                # every chunk idle: unmapped
+    assert D.pool_trim(0) == 0
+
+
 def test_direct_path_identity_pinned(dp):
     """Identity loads from pinned memory take the direct DMA + verify path;
     bytes and checksum equal the oracle's (incl. zero padding to 16)."""
