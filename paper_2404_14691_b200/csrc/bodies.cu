@@ -417,6 +417,7 @@ extern "C" int sage_launch_after(sage_handle slot, const sage_handle *wait, int 
 }
 
 int sage::launch_timed(Gpu *G, cudaStream_t s, const sage_body_desc *b) {
+  NvtxRange nv("sage.body");
   cudaEvent_t sb = stat_begin(G, s);
   SAGE_TRY(launch_body(b, s, G->sm_count));
   // algorithmic work per launch (bytes; FLOPs for sgemm)

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only: ranges cost a pointer test unless a profiler attaches
 
 #include <atomic>
 #include <condition_variable>
@@ -21,6 +22,15 @@
 #include "../../include/sage_dp.h"
 
 namespace sage {
+
+// host-side NVTX range for a data-plane phase (issue, load, body launch):
+// visible in nsys / ncu timelines, no cost without a profiler attached
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ---------------------------------------------------------------- errors ----
 void set_error(const std::string &msg);

@@ -481,6 +481,7 @@ static void flight_add(std::deque<Flight> &flights, sage_handle ev_alias_of, int
 // first piece of a staged RO load); an invocation with an open RO load gets
 // its next piece.  Returns true when I is fully issued (or failed).
 static bool issue_step(Inv *I, int64_t piece, std::deque<Flight> &flights) {
+  NvtxRange nv("sage.issue");
   const sage_invoke_desc &d = I->d;
   const bool fresh = I->G == nullptr && !I->ro_cur;
   int rc = SAGE_OK;

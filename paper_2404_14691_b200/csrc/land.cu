@@ -496,6 +496,7 @@ int sage::segment_load_step(LoadCursor *c, uint64_t budget, uint64_t *bytes, sag
 void sage::segment_load_close(LoadCursor *c) { delete c; }
 
 int sage::segment_load(const sage_load_desc *d, sage_handle *load_out, sage_handle *end_ev, sage_handle pre_end) {
+  NvtxRange nv("sage.segment_load");
   LoadCursor *c = nullptr;
   SAGE_TRY(segment_load_open(d, pre_end, &c, load_out, end_ev));
   if (!c) return SAGE_OK;
