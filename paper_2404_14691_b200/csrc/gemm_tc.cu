@@ -440,29 +440,35 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
         float4 acc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        // four partials x U outputs: 16 independent remote loads in flight
+        // before any add (one DSMEM round trip per group, not one per partial)
+        for (int q0 = 0; q0 < nz; q0 += 4) {
+          float4 v[4][U];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (q >= nz) break;
-          float4 v[U];
+          for (int qq = 0; qq < 4; ++qq) {
+            const int q = q0 + qq;
 #pragma unroll
-          for (int u = 0; u < U; ++u) {   // independent remote loads, issued back to back
-            const int f = f0 + u * NT;
-            const int row = r0 + f / (BN / 4), c4 = f % (BN / 4);
-            const uint32_t la = smem_u32(smem + (size_t)row * (BN * 4 + 16) + c4 * 16);
-            uint32_t ra;
-            // split-K peers: cluster rank q (PAIR: the same pair slot of pair q)
-            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(PAIR ? prank + 2u * q : (uint32_t)q));
-            if (f < rows * (BN / 4))
-              asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                           : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
-                           : "r"(ra));
-            else
-              v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u = 0; u < U; ++u) {
+              const int f = f0 + u * NT;
+              const int row = r0 + f / (BN / 4), c4 = f % (BN / 4);
+              const uint32_t la = smem_u32(smem + (size_t)row * (BN * 4 + 16) + c4 * 16);
+              uint32_t ra;
+              // split-K peers: cluster rank q (PAIR: the same pair slot of pair q)
+              asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(PAIR ? prank + 2u * q : (uint32_t)q));
+              if (q < nz && f < rows * (BN / 4))
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[qq][u].x), "=f"(v[qq][u].y), "=f"(v[qq][u].z), "=f"(v[qq][u].w)
+                             : "r"(ra));
+              else
+                v[qq][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
           }
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
-          }
+          for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              acc[u].x += v[qq][u].x; acc[u].y += v[qq][u].y; acc[u].z += v[qq][u].z; acc[u].w += v[qq][u].w;
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
