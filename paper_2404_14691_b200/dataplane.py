@@ -144,6 +144,9 @@ class _PinnedPool:
     SLAB = 64 << 20
 
     def __init__(self):
+        import os
+        if os.environ.get("SAGE_PINNED_SLABS") == "0":    # diagnostics: every buffer its own cudaHostAlloc
+            self.SMALL = 0
         self.free: dict[int, list] = {}
         self.small: dict[int, list] = {}
         self.slabs: list = []

@@ -249,7 +249,7 @@ def trace(path: str, workload: str = "cfg2", policy: str = "SAGE", time_scale: f
 
 
 def peak(workload: str = "cfg2", probe_s: float = 2.0, rate_min: float = 50.0, rate_ceiling: float = 65536.0,
-         resolution: float = 0.05, seed: int = 1) -> dict:
+         resolution: float = 0.05, seed: int = 1, prewarm: int = 256) -> dict:
     """Largest stable Poisson rate of a workload on one B200 (reference
     `gslsim peak`, experiments.py:128-155): doubling + bisection over
     `probe_s`-second probes on one warm plane."""
@@ -260,19 +260,29 @@ def peak(workload: str = "cfg2", probe_s: float = 2.0, rate_min: float = 50.0, r
     probes = []
     try:
         sim.prepare()
+        sim.prewarm(prewarm)
         dur = int(probe_s * 1e6)
 
         def probe(rate: float):
             arr = generate_arrivals(PoissonOpenSpec(rate, probe_s, {n: 1.0 for n in table}), seed)
+            n0 = len(sim.invocations)
+            loads0 = dict(sim.sharing.ro_loads_performed) if sim.sharing is not None else {}
             st = run_probe(sim, arr, dur)
+            warmth: dict = {}
+            for i in sim.invocations[n0:]:
+                w = i.warmth.name if i.warmth is not None else "none"
+                warmth[w] = warmth.get(w, 0) + 1
+            loads = ({k[0]: v - loads0.get(k, 0) for k, v in sim.sharing.ro_loads_performed.items()}
+                     if sim.sharing is not None else {})
             probes.append({"rate_per_s": rate, "arrivals": len(arr), "queue_early": st.queue_early,
                            "queue_end": st.queue_end, "p99_first_ms": st.p99_first_quartile_ms,
-                           "p99_last_ms": st.p99_last_quartile_ms})
+                           "p99_last_ms": st.p99_last_quartile_ms, "warmth": warmth, "ro_loads": loads})
             return st
 
         res = find_peak_throughput(probe, rate_min=rate_min, rate_ceiling=rate_ceiling, resolution=resolution,
                                    queue_slack=16, p99_slack_ms=5.0)
-        return {"workload": f"{workload} Poisson probes of {probe_s:g} s, SAGE, 1 GPU",
+        return {"workload": f"{workload} Poisson probes of {probe_s:g} s, SAGE, 1 GPU, plane pre-warmed with a "
+                            f"{prewarm}-invocation burst",
                 "stability": "reference rule (replay.is_stable) + slack: backlog +16 invocations, p99 +5 ms",
                 "peak_rate_per_s": res.rate_per_s, "hit_ceiling": res.hit_ceiling, "diagnostic": res.diagnostic,
                 "trajectory": [[r, ok] for r, ok in res.trajectory], "probes": probes}
