@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>   // header-only: ranges cost a pointer test unless a profiler attaches
 
+#include <pthread.h>
+
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>

@@ -245,6 +245,7 @@ struct MemcpyPool {
 MemcpyPool &mp = *new MemcpyPool;
 
 void memcpy_worker() {
+  pthread_setname_np(pthread_self(), "sage-memcpy");
   uint64_t seen = 0;
   for (;;) {
     {
