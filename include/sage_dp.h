@@ -427,6 +427,14 @@ int sage_event_elapsed(sage_handle a, sage_handle b, double *us);
  * Replaces the COMPUTE delay of the resnet50 record (functions.py:154, :276). */
 #define SAGE_CONV_NHWC  0
 #define SAGE_CONV_C4    1
+/* SAGE_CONV_S2D: the stem (7x7 stride 2 pad 3 over 3 channels) as a stride-1
+ * 4x4 convolution over its 2x2 space-to-depth input: NHWC with 16 channels
+ * (dr, ds, c; c padded to 4) of (H/2, W/2) pixels, filter [Cout][4][4][16]
+ * with w'[a][b][dr][ds][c] = w[2a+dr-1][2b+ds-1][c] (zero outside 7x7),
+ * cin = 16, r = s = 4, stride 1, pad 2; the output has the input's size.
+ * Every K-block is one filter row of 4 taps x 16 channels = 128 B per pixel,
+ * so the gather is the regular layers' coalesced one.                      */
+#define SAGE_CONV_S2D   2
 typedef struct {
   uint64_t x, w, out, residual;             /* device pointers (residual 0 = none) */
   uint64_t bn_gamma, bn_beta, bn_mean, bn_var;
@@ -445,6 +453,7 @@ int sage_conv(sage_handle slot, const sage_conv_desc *d);
 #define SAGE_NET_CONV       2   /* sage_conv on (src, filter, BN, res) -> dst  */
 #define SAGE_NET_MAXPOOL    3   /* 3x3 stride 2 pad 1                           */
 #define SAGE_NET_POOL_FC    4   /* avg pool into buffer `res` + classifier -> dst (fp32) */
+#define SAGE_NET_S2D_INPUT  5   /* NHWC3 (h, w) -> 2x2 space-to-depth NHWC16 (h/2, w/2) (SAGE_CONV_S2D stem) */
 #define SAGE_NET_BUF_INPUT  0
 #define SAGE_NET_BUF_OUT    1
 #define SAGE_NET_BUF_WS0    2

@@ -120,9 +120,9 @@ class ResidentInfo(C.Structure):
                 ("has_checksum", C.c_uint32), ("pad_", C.c_uint32), ("checksum", u64)]
 
 
-CONV_NHWC, CONV_C4 = 0, 1
+CONV_NHWC, CONV_C4, CONV_S2D = 0, 1, 2
 BODY_RESNET50 = 8
-NET_PAD_INPUT, NET_CONV, NET_MAXPOOL, NET_POOL_FC = 1, 2, 3, 4
+NET_PAD_INPUT, NET_CONV, NET_MAXPOOL, NET_POOL_FC, NET_S2D_INPUT = 1, 2, 3, 4, 5
 NET_BUF_INPUT, NET_BUF_OUT, NET_BUF_WS0 = 0, 1, 2
 
 

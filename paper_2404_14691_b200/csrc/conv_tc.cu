@@ -259,11 +259,11 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
     // 128-B pixel slices (full lines) instead of 16 B of 32 pixels
     const int row = threadIdx.x - 64;
     const int gw = row >> 5;
-    const int cslices = C4 ? 1 : a.C / CV_BK;
+    const int cslices = C4 ? 1 : a.C / CV_BK;   // (regular mode: 64-channel slices per tap)
     int n = 0, ih0 = 0, iw0 = 0;
     bool live = false;
-    int jn[8], jh[8], jw[8];   // per pixel row j of this lane (non-C4)
-    if constexpr (C4) {
+    int jn[8], jh[8], jw[8];   // per pixel row j of this lane (regular and S2D modes)
+    if constexpr (C4 == 1) {
       const int m = m0 + row;
       live = m < a.M;
       int p = 0, q = 0;
@@ -298,15 +298,19 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
     for (int kb = 0; kb < KB; ++kb) {
       const int s = kb % ST, round = kb / ST;
       cv_wait(&empty[s], (round & 1) ^ 1);
-      if constexpr (!C4) {
+      if constexpr (C4 != 1) {
         const uint32_t tile = cv_smem(sA + s * Sm::A_BYTES) + (uint32_t)gw * 32u * 128u;
+        // regular: K-block = one tap x 64 channels (chunk = 8 channels);
+        // S2D: K-block = filter row kb, 4 taps x 16 channels (chunk = half a tap)
         const int tap = kb / cslices, c0 = (kb - tap * cslices) * CV_BK;
-        const int r = tap / a.S, sx = tap - r * a.S;
+        const int r = C4 == 2 ? kb : tap / a.S;
+        const int sx = C4 == 2 ? (int)(chunk >> 1) : tap - r * a.S;
+        const int coff = C4 == 2 ? 8 * (int)(chunk & 1) : c0 + 8 * (int)chunk;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int ih = jh[j] + r, iw = jw[j] + sx;
           const bool ok = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-          const __nv_bfloat16 *src = ok ? X + ((size_t)(jn[j] * a.H + ih) * a.W + iw) * a.C + c0 + 8 * chunk : X;
+          const __nv_bfloat16 *src = ok ? X + ((size_t)(jn[j] * a.H + ih) * a.W + iw) * a.C + coff : X;
           const uint32_t prow = 4u * j + (uint32_t)(lane >> 3);     // row within the warp's 32
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tile + prow * 128u +
                                                                               ((chunk ^ (prow & 7u)) << 4)),
@@ -509,9 +513,12 @@ static int pick_bn(int m_tiles, int cout, int sms) {
 
 int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame *f) {
   if (!d || (!f && (!d->x || !d->out)) || !d->w) return fail(SAGE_EINVAL, "conv: null tensor");
-  const bool c4 = d->mode == SAGE_CONV_C4;
+  const bool c4 = d->mode == SAGE_CONV_C4, s2d = d->mode == SAGE_CONV_S2D;
+  if (d->mode < SAGE_CONV_NHWC || d->mode > SAGE_CONV_S2D) return fail(SAGE_EINVAL, "conv: unknown mode");
+  if (s2d && (d->cin != 16 || d->r != 4 || d->s != 4 || d->stride != 1 || d->pad != 2 || d->cout != 64))
+    return fail(SAGE_EINVAL, "conv: S2D mode is the stem: cin 16, 4x4 filter, stride 1, pad 2, cout 64");
   if (d->n <= 0 || d->h <= 0 || d->w_ <= 0 || d->cout % 64 || d->r <= 0 || d->s <= 0 || d->stride <= 0 ||
-      d->pad < 0 || (!c4 && d->cin % 64) || (c4 && d->cin != 4))
+      d->pad < 0 || (!c4 && !s2d && d->cin % 64) || (c4 && d->cin != 4))
     return fail(SAGE_EINVAL, "conv: Cout and Cin must be multiples of 64 (C4 mode: Cin == 4)");
   if (((d->x | d->w | d->out | d->residual) & 15))
     return fail(SAGE_EINVAL, "conv: tensors must be 16-byte aligned");
@@ -533,8 +540,8 @@ int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame 
   a.eps = d->bn_eps;
   a.N = d->n; a.H = d->h; a.W = d->w_; a.C = d->cin;
   a.R = d->r; a.S = d->s; a.stride = d->stride; a.pad = d->pad; a.Cout = d->cout;
-  a.P = (d->h + 2 * d->pad - d->r) / d->stride + 1;
-  a.Q = (d->w_ + 2 * d->pad - d->s) / d->stride + 1;
+  a.P = s2d ? d->h : (d->h + 2 * d->pad - d->r) / d->stride + 1;   // S2D: pad 2 before, 1 after
+  a.Q = s2d ? d->w_ : (d->w_ + 2 * d->pad - d->s) / d->stride + 1;
   a.M = a.N * a.P * a.Q;
   a.relu = d->relu;
   const uint64_t ktot = c4 ? (uint64_t)((d->r * d->s + 15) / 16) * CV_BK : (uint64_t)d->r * d->s * d->cin;
@@ -551,10 +558,14 @@ int conv_bf16(const sage_conv_desc *d, cudaStream_t s, int sms, const ConvFrame 
   // the peer's readiness reaches the leader's MMA through a relay thread and a
   // cluster-scope barrier, which the K loop does not hide
   static const bool pair_on = [] { const char *e = getenv("SAGE_CONV_PAIR"); return e && atoi(e) != 0; }();
-  const bool pair = !c4 && bn == 256 && pair_on;
+  const bool pair = !c4 && !s2d && bn == 256 && pair_on;
   CUtensorMap map;   // a pair's CTA loads BN/2 filter rows per K-block
   SAGE_TRY(filter_map(&map, d->w, (uint64_t)d->cout, ktot, (uint32_t)(pair ? bn / 2 : bn)));
   if (c4) return bn == 64 ? launch_conv<64, 1>(map, a, s) : launch_conv<128, 1>(map, a, s);
+  // the S2D stem: 4 K-blocks per tile, 784 tiles at batch 8 -- the 2-stage
+  // kernel (48 KB) lets three CTAs share an SM (SAGE_CONV_S2D_STAGES=4: 2 per SM)
+  static const bool s2d_deep = [] { const char *e = getenv("SAGE_CONV_S2D_STAGES"); return e && atoi(e) == 4; }();
+  if (s2d) return s2d_deep ? launch_conv<64, 2>(map, a, s) : launch_conv<64, 2, 1>(map, a, s);
   if (pair) return shrt ? launch_conv<256, 0, 1, 1>(map, a, s) : launch_conv<256, 0, 0, 1>(map, a, s);
   if (bn == 256) return shrt ? launch_conv<256, 0, 1>(map, a, s) : launch_conv<256, 0>(map, a, s);
   if (bn == 128) return shrt && short_all ? launch_conv<128, 0, 1>(map, a, s) : launch_conv<128, 0>(map, a, s);
@@ -572,6 +583,8 @@ int conv_optin_all() {
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 0, 1>, CvSmem<64, 1>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 1>, CvSmem<64>::TOTAL));
   SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<128, 1>, CvSmem<128>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 2>, CvSmem<64>::TOTAL));
+  SAGE_TRY(smem_optin((const void *)conv_bf16_kernel<64, 2, 1>, CvSmem<64, 1>::TOTAL));
   return SAGE_OK;
 }
 
@@ -587,6 +600,8 @@ int touch_conv_kernels() {
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 0, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 1>));
   SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<128, 1>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 2>));
+  SAGE_CUDA(cudaFuncGetAttributes(&at, conv_bf16_kernel<64, 2, 1>));
   return SAGE_OK;
 }
 

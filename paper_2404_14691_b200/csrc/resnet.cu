@@ -7,7 +7,9 @@
 // their offsets in the segment) and the invocation's writable segment (the
 // request image, the logits and the activation workspace).  One invocation's
 // COMPUTE runs the program on its stream:
-//   PAD_INPUT   NHWC 3-channel image -> 4-channel (the stem's C4 gather)
+//   S2D_INPUT   NHWC 3-channel image -> 2x2 space-to-depth, 16 channels (the
+//               stem as a 4x4 stride-1 conv, SAGE_CONV_S2D); PAD_INPUT -> 4
+//               channels for the older C4 stem
 //   CONV        tcgen05 implicit GEMM (conv_tc.cu), BN / residual / ReLU fused
 //   MAXPOOL     3x3 stride 2 pad 1 (the stem)
 //   POOL_FC     global average pool + the 1000-way classifier, fp32 logits
@@ -50,6 +52,33 @@ __global__ void pad_c4_kernel(const uint64_t *frame, BufRef src, BufRef dst, lon
     v.x = *reinterpret_cast<uint32_t *>(&lo);
     v.y = *reinterpret_cast<uint32_t *>(&hi);
     out[i] = v;
+  }
+}
+
+// NHWC bf16 [N, H, W, 3] -> 2x2 space-to-depth [N, H/2, W/2, 16]: channel
+// (dr * 2 + ds) * 4 + c of output pixel (i, j) is input (2i + dr, 2j + ds, c),
+// c = 3 zero (the SAGE_CONV_S2D stem); one thread = one output pixel (32 B)
+__global__ void s2d_kernel(const uint64_t *frame, BufRef src, BufRef dst, int N, int H, int W) {
+  const __nv_bfloat16 *in = reinterpret_cast<const __nv_bfloat16 *>(resolve(frame, src));
+  uint4 *out = reinterpret_cast<uint4 *>(resolve(frame, dst));
+  const int H2 = H / 2, W2 = W / 2;
+  const long long total = (long long)N * H2 * W2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % W2);
+    const long long t = i / W2;
+    const int r = (int)(t % H2), n = (int)(t / H2);
+    __nv_bfloat16 v[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int dr = q >> 1, ds = q & 1;
+      const __nv_bfloat16 *p = in + ((size_t)(n * H + 2 * r + dr) * W + 2 * j + ds) * 3;
+      v[4 * q] = p[0];
+      v[4 * q + 1] = p[1];
+      v[4 * q + 2] = p[2];
+      v[4 * q + 3] = __float2bfloat16(0.f);
+    }
+    out[2 * i] = *reinterpret_cast<const uint4 *>(&v[0]);
+    out[2 * i + 1] = *reinterpret_cast<const uint4 *>(&v[8]);
   }
 }
 
@@ -206,6 +235,12 @@ static int enqueue_ops(Net *net, uint64_t ro, const uint64_t *frame, const uint6
         pad_c4_kernel<<<grid_for(pix, sms), 256, 0, s>>>(frame, src, dst, pix);
         break;
       }
+      case SAGE_NET_S2D_INPUT: {
+        if ((op.h | op.w) & 1) return fail(SAGE_EINVAL, "resnet body: S2D_INPUT needs even height and width");
+        const long long pix = (long long)op.n * (op.h / 2) * (op.w / 2);
+        s2d_kernel<<<grid_for(pix, sms), 256, 0, s>>>(frame, src, dst, op.n, op.h, op.w);
+        break;
+      }
       case SAGE_NET_CONV: {
         sage_conv_desc d{};
         d.x = frame ? 16 : src.direct;        // direct pointers only validate alignment in frame mode
@@ -321,6 +356,7 @@ int net_run(const sage_body_desc *b, cudaStream_t s, int sms) {
 int touch_net_kernels() {
   cudaFuncAttributes a;
   SAGE_CUDA(cudaFuncGetAttributes(&a, pad_c4_kernel));
+  SAGE_CUDA(cudaFuncGetAttributes(&a, s2d_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, maxpool_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, avgpool_kernel));
   SAGE_CUDA(cudaFuncGetAttributes(&a, fc_kernel));
@@ -371,7 +407,7 @@ extern "C" int sage_net_create(const sage_net_op *ops, int n_ops, const uint64_t
   }
   N->workspace = off;
   for (const sage_net_op &op : N->ops)
-    if (op.kind < SAGE_NET_PAD_INPUT || op.kind > SAGE_NET_POOL_FC) {
+    if (op.kind < SAGE_NET_PAD_INPUT || op.kind > SAGE_NET_S2D_INPUT) {
       delete N;
       return fail(SAGE_EINVAL, "net_create: unknown op kind");
     }

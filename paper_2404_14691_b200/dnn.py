@@ -93,13 +93,46 @@ def resnet50(batch: int = 8, seed: int = 0, name: str = "resnet50_real", dtype: 
 _STAGES = ((64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2))   # (planes, blocks, stride) of layer1..4
 
 
+def stem_s2d_filter(w: np.ndarray) -> np.ndarray:
+    """The stem's 7x7 stride-2 pad-3 filter [64][3][7][7] (OIHW) as the 4x4
+    stride-1 filter over the 2x2 space-to-depth input (SAGE_CONV_S2D):
+    [64][a][b][dr][ds][c] = w[c][2a+dr-1][2b+ds-1], zero outside the 7x7
+    window and for the padded channel c = 3; flattened to [64][256]."""
+    o = w.shape[0]
+    out = np.zeros((o, 4, 4, 2, 2, 4), np.float32)
+    for a_ in range(4):
+        for dr in range(2):
+            r = 2 * a_ + dr - 1
+            if not 0 <= r < 7:
+                continue
+            for b_ in range(4):
+                for ds in range(2):
+                    sx = 2 * b_ + ds - 1
+                    if 0 <= sx < 7:
+                        out[:, a_, b_, dr, ds, :3] = w[:, :, r, sx]
+    return out.reshape(o, 256)
+
+
+def stem_s2d_input(x_nhwc: np.ndarray) -> np.ndarray:
+    """NHWC [N, H, W, 3] -> [N, H/2, W/2, 16] with channel (dr*2+ds)*4 + c
+    = x[2i+dr, 2j+ds, c] (c = 3 zero): what the program's S2D_INPUT op
+    computes on the device (numpy form for tests)."""
+    n, h, w, _ = x_nhwc.shape
+    out = np.zeros((n, h // 2, w // 2, 2, 2, 4), x_nhwc.dtype)
+    for dr in range(2):
+        for ds in range(2):
+            out[:, :, :, dr, ds, :3] = x_nhwc[:, dr::2, ds::2, :]
+    return out.reshape(n, h // 2, w // 2, 16)
+
+
 def resnet50_native(batch: int = 8, seed: int = 0, name: str = "resnet50_real"):
     """The BF16 ResNet-50 function whose body is a native program (no
     PyTorch at run time).  Record: every conv filter OHWI bf16 in place, the
-    stem's filter padded to 4 input channels and K = 256 ([64][7][7][4] + a
-    zero tail: the C4 gather of csrc/conv_tc.cu), batch-norm parameters and
-    the classifier in bf16.  Request: the images NHWC bf16.  Writable: the
-    image, the fp32 logits and the activation workspace of the program."""
+    stem's filter as the 4x4 stride-1 filter over its 2x2 space-to-depth
+    input ([64][4][4][16], `stem_s2d_filter`: the S2D mode of
+    csrc/conv_tc.cu), batch-norm parameters and the classifier in bf16.
+    Request: the images NHWC bf16.  Writable: the image, the fp32 logits and
+    the activation workspace of the program."""
     names, arrays = _state(seed)
     sd = dict(zip(names, arrays))
     rec_names, rec = [], []
@@ -108,9 +141,7 @@ def resnet50_native(batch: int = 8, seed: int = 0, name: str = "resnet50_real"):
         if a.dtype != np.float32:
             continue                    # num_batches_tracked: not used at inference
         if n == "conv1.weight":
-            w = np.zeros((64, 256), np.float32)
-            w[:, :196] = np.concatenate([a.transpose(0, 2, 3, 1), np.zeros((64, 7, 7, 1), np.float32)], 3).reshape(64, 196)
-            a = w
+            a = stem_s2d_filter(a)
         elif a.ndim == 4:
             a = a.transpose(0, 2, 3, 1)   # OIHW -> OHWI
         rec_names.append(n)
@@ -142,10 +173,10 @@ def _native_program(off: dict, batch: int):
     from . import _lib
     N = batch
     act = N * 112 * 112 * 64 * 2          # the largest activation (stem out = layer1 out)
-    bufs = [N * 224 * 224 * 4 * 2] + [act] * 5 + [N * 2048 * 4]
-    pad_in, feat = _lib.NET_BUF_WS0, _lib.NET_BUF_WS0 + 6
+    bufs = [N * 112 * 112 * 16 * 2] + [act] * 5 + [N * 2048 * 4]
+    s2d_in, feat = _lib.NET_BUF_WS0, _lib.NET_BUF_WS0 + 6
     A = [_lib.NET_BUF_WS0 + 1 + i for i in range(5)]
-    ops = [dict(kind=_lib.NET_PAD_INPUT, src=_lib.NET_BUF_INPUT, dst=pad_in, n=N, h=224, w=224)]
+    ops = [dict(kind=_lib.NET_S2D_INPUT, src=_lib.NET_BUF_INPUT, dst=s2d_in, n=N, h=224, w=224)]
 
     def conv(src, dst, prefix, bn, cin, cout, k, stride, pad, h, relu, res=-1, mode=0):
         g = bn + "."
@@ -154,7 +185,8 @@ def _native_program(off: dict, batch: int):
                         v_off=off[g + "running_var"], eps=1e-5, n=N, h=h, w=h, cin=cin, cout=cout, r=k, s=k,
                         stride=stride, pad=pad, relu=int(relu), mode=mode))
 
-    conv(pad_in, A[0], "conv1", "bn1", 4, 64, 7, 2, 3, 224, True, mode=_lib.CONV_C4)
+    # the stem: 7x7 stride 2 over 224^2 x 3 == 4x4 stride 1 over the 112^2 x 16 space-to-depth input
+    conv(s2d_in, A[0], "conv1", "bn1", 16, 64, 4, 1, 2, 112, True, mode=_lib.CONV_S2D)
     ops.append(dict(kind=_lib.NET_MAXPOOL, src=A[0], dst=A[1], n=N, h=112, w=112, cin=64))
     cur, h, cin = A[1], 56, 64
     for li, (planes, blocks, stride) in enumerate(_STAGES):

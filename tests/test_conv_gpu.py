@@ -38,6 +38,8 @@ def run_conv(x_nhwc, w_ohwi, bn, res_nhwc, stride, pad, relu, mode=_lib.CONV_NHW
     s = s or w_ohwi.shape[2]
     p = (h + 2 * pad - r) // stride + 1
     q = (w + 2 * pad - s) // stride + 1
+    if mode == _lib.CONV_S2D:      # pad 2 before, 1 after: the output keeps the input's size
+        p, q = h, w
     segs = [upload(bf16_bytes(x_nhwc)), upload(bf16_bytes(w_ohwi))]
     out = D.pool_alloc(0, n * p * q * cout * 2 + 256, _lib.CLASS_WRITABLE, unaccounted=True)
     d = _lib.ConvDesc()
@@ -132,6 +134,29 @@ def test_conv1_c4_mode_matches_torch_cpu(dp):
     got = run_conv(x4, wpad.view(cout, 1, 1, 256), bn, None, 2, 3, True, mode=_lib.CONV_C4, r=7, s=7, cin=4)
     want = reference(x3, w3, bn, None, 2, 3, True)
     np.testing.assert_allclose(got.numpy(), want.numpy(), rtol=1e-2, atol=1e-2 * float(want.abs().max()))
+
+
+def test_conv1_s2d_mode_matches_torch_cpu(dp):
+    """The stem as the S2D mode: the 7x7 stride-2 pad-3 convolution of a
+    3-channel image run as a 4x4 stride-1 implicit GEMM over its 2x2
+    space-to-depth input (16 channels), against torch-CPU fp32 of the
+    original convolution (BN + ReLU fused)."""
+    import torch
+    from paper_2404_14691_b200 import dnn
+    g = torch.Generator().manual_seed(11)
+    n, h = 2, 40
+    x = torch.randn(n, h, h, 3, generator=g)
+    w = torch.randn(64, 3, 7, 7, generator=g) * 0.1
+    bn = (torch.rand(64, generator=g) + 0.5, torch.randn(64, generator=g), torch.randn(64, generator=g) * 0.1,
+          torch.rand(64, generator=g) + 0.5)
+    rb = lambda t: t.to(torch.bfloat16).float()
+    xs = dnn.stem_s2d_input(rb(x).numpy())
+    ws = dnn.stem_s2d_filter(rb(w).numpy()).reshape(64, 4, 4, 16)
+    got = run_conv(torch.from_numpy(xs), torch.from_numpy(ws), bn, None, 1, 2, True, mode=_lib.CONV_S2D)
+    want = reference(x, w.permute(0, 2, 3, 1), bn, None, 2, 3, True)
+    assert got.shape == want.shape == (n, h // 2, h // 2, 64)
+    m = float(want.abs().max())
+    np.testing.assert_allclose(got.numpy(), want.numpy(), rtol=1e-2, atol=1e-2 * m)
 
 
 def test_conv_rejects_bad_shapes(dp):

@@ -15,7 +15,7 @@ def load(path):
     out = [(v["k"], v.get("launch__grid_size"), float(v["gpu__time_duration.sum"].replace(",", "")) / 1e3)
            for v in L.values()]
     # the last full forward: from the last pad_c4_kernel through fc_kernel
-    starts = [i for i, o in enumerate(out) if o[0].startswith("pad_c4")]
+    starts = [i for i, o in enumerate(out) if o[0].startswith(("pad_c4", "s2d_kernel"))]
     fw = out[starts[-2]:] if len(starts) > 1 else out
     ends = [i for i, o in enumerate(fw) if o[0].startswith("fc_kernel")]
     return fw[:ends[0] + 1] if ends else fw
