@@ -20,9 +20,12 @@
 //              + bias (+ residual), ReLU, bf16, 64-B stores (NHWC)
 // K-block order: filter tap (r, s) outer, 64-channel slice inner, so every
 // K-block is one shifted NHWC window: (kb / (Cin/64)) -> (r, s).
-// conv1 (Cin = 3) runs in the C4 mode: the input padded to 4 channels (8 B
-// per pixel) and the filter to [Cout][256] (16 taps x 4 channels per K-block,
-// 49 taps, zero tail), both prepared by small kernels (resnet.cu).
+// conv1 (7x7 stride 2, Cin = 3) runs in the S2D mode: a 4x4 stride-1
+// convolution over its 2x2 space-to-depth input (16 channels, prepared by
+// resnet.cu's s2d_kernel; filter repacked at registration, dnn.py), so a
+// K-block is one filter row of 4 taps x 16 channels = 128 B per pixel and the
+// regular coalesced gather applies.  The older C4 mode (input padded to 4
+// channels, 16 taps x 8 B per K-block) stays available and tested.
 // Batch-norm: scale = gamma * rsqrt(var + eps), bias = beta - mean * scale,
 // computed per CTA from the landed bf16 parameters (no folded copy).
 #include "common.h"
