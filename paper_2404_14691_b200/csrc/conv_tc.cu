@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
   uint64_t *empty = full + ST;
   uint64_t *tmem_full = empty + ST;
   uint64_t *pfull = tmem_full + 1;   // PAIR (leader): the peer's stage is ready
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pfull + ST);
+  uint64_t *res_bar = pfull + ST;    // the residual tile landed in the (drained) ring
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(res_bar + 1);
   float *s_scale = reinterpret_cast<float *>(smem + ST * Sm::STAGE + 512);
   float *s_bias = s_scale + 256;
 
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(&empty[s])), "r"(1));
       }
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(tmem_full)), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(res_bar)), "r"(1));
       if constexpr (PAIR)
         for (int s = 0; s < ST; ++s)
           asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cv_smem(&pfull[s])), "r"(1));
@@ -349,6 +351,27 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
     const int quad = warp & 3;
     const int orow = m0 + quad * 32 + lane;
     const bool olive = orow < a.M;
+    // residual: the whole [128 x BN] tile lands in the drained operand ring by
+    // bulk copies (one per row, one barrier) -- one memory round trip for the
+    // epilogue instead of one per 32-channel chunk
+    constexpr int RSTRIDE = BN * 2 + 16;   // padded rows: a warp's 16-B reads spread over the banks
+    constexpr bool RES_SMEM = CV_BM * RSTRIDE <= ST * Sm::STAGE;
+    const uint8_t *rrow = smem + (size_t)(quad * 32 + lane) * RSTRIDE;
+    if (RES_SMEM && RES) {
+      if (quad * 32 + lane == 0) {
+        const int live = a.M - m0 < CV_BM ? (a.M - m0 > 0 ? a.M - m0 : 0) : CV_BM;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cv_smem(res_bar)),
+                     "r"((uint32_t)live * BN * 2)
+                     : "memory");
+      }
+      if (olive)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                cv_smem(rrow)),
+            "l"(RES + (size_t)orow * a.Cout + n0), "r"((uint32_t)(BN * 2)), "r"(cv_smem(res_bar))
+            : "memory");
+      cv_wait(res_bar, 0);
+    }
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t v[32];
@@ -368,7 +391,8 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
 #pragma unroll
       for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]) * s_scale[c + j] + s_bias[c + j];
       if (RES) {
-        const uint4 *rp = reinterpret_cast<const uint4 *>(RES + base);
+        const uint4 *rp = RES_SMEM ? reinterpret_cast<const uint4 *>(rrow + 2 * c)
+                                   : reinterpret_cast<const uint4 *>(RES + base);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 w = rp[u];
@@ -385,7 +409,11 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = fmaxf(y[j], 0.f);
       }
-      uint4 *op = reinterpret_cast<uint4 *>(OUT + base);
+      // RES_SMEM: the output row is staged in the ring (in place of the
+      // residual chunk just read) and leaves as one 512-B bulk store per row
+      // below, instead of 16-B stores of 32 different rows per instruction
+      uint4 *op = RES_SMEM ? reinterpret_cast<uint4 *>(const_cast<uint8_t *>(rrow) + 2 * c)
+                           : reinterpret_cast<uint4 *>(OUT + base);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         uint4 w;
@@ -394,6 +422,15 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
         for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(y[8 * u + 2 * e], y[8 * u + 2 * e + 1]);
         op[u] = w;
       }
+    }
+    if (RES_SMEM && olive) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> bulk copy reads
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                       OUT + (size_t)orow * a.Cout + n0),
+                   "r"(cv_smem(rrow)), "r"((uint32_t)(BN * 2))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the row's smem is read: reusable
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
