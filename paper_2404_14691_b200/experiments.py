@@ -79,17 +79,21 @@ def cfg1(n: int = 16, reps: int = 5) -> dict:
 
 
 def cfg3(rate: float = 300.0, duration_s: float = 4.0, gpus_list=(1, 2, 4), seed: int = 1, dtype: str = "fp32",
-         engine: str | None = None) -> dict:
+         engine: str | None = None, prewarm: int = 64, window: int | None = None) -> dict:
     from .dnn import resnet50
     spec, data = resnet50(dtype=dtype, engine=engine)
     arrivals = generate_arrivals(PoissonOpenSpec(rate, duration_s, {spec.name: 1.0}), seed)
     out = {"engine": data.body, "workload": f"ResNet-50 (random init, {data.layout.seg_bytes} B {dtype} weights, batch 8) "
-                       f"Poisson {rate:g}/s for {duration_s:g} s ({len(arrivals)} arrivals)"}
+                       f"Poisson {rate:g}/s for {duration_s:g} s ({len(arrivals)} arrivals), plane pre-warmed with a "
+                       f"{prewarm}-invocation burst" + (f", admission window {window} per GPU" if window else "")}
     for g in gpus_list:
-        sim = Simulation(ClusterSpec(gpus=g), policy_preset("SAGE"), {spec.name: spec}, seed=seed,
-                         function_data={spec.name: data}, copy_results=False)
+        sim = Simulation(ClusterSpec(gpus=g, admission_window=window), policy_preset("SAGE"), {spec.name: spec},
+                         seed=seed, function_data={spec.name: data}, copy_results=False)
         try:
             sim.prepare()
+            # deployment warm-up: graph instances of the program, streams, pool
+            # chunks and pinned buffers exist before the first arrival
+            sim.prewarm(prewarm)
             src = OpenLoopSource(arrivals)
             t0 = time.perf_counter()
             src.attach(sim)
@@ -298,6 +302,7 @@ def main(argv=None):
     ap.add_argument("configs", nargs="*", choices=sorted(RUNNERS))
     ap.add_argument("--out", default=None)
     ap.add_argument("--rate", type=float, default=None, help="cfg3: Poisson rate (/s)")
+    ap.add_argument("--window", type=int, default=None, help="cfg3: admission window per GPU (default none)")
     ap.add_argument("--gpus", default=None, help="cfg3: comma-separated logical GPU counts")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg3_bf16"],
                     help="peak / trace: function set")
@@ -325,6 +330,7 @@ def main(argv=None):
                 kw["gpus_list"] = tuple(int(g) for g in args.gpus.split(","))
             kw["dtype"] = args.dtype
             kw["engine"] = args.engine
+            kw["window"] = args.window
         res = RUNNERS[c](**kw)
         res["elapsed_s"] = round(time.perf_counter() - t0, 1)
         line = json.dumps({c: res})

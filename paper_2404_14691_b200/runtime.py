@@ -49,6 +49,12 @@ class ClusterSpec:
     cpu_mem_mb: Optional[float] = None
     compute_concurrency: Optional[int] = None
     pre_warmed_containers: bool = True
+    # admission window: at most this many started, unfinished invocations per
+    # GPU; later arrivals wait in the dispatcher's FIFO (None: unlimited, the
+    # reference's rule -- admission is bounded by memory only).  A window keeps
+    # a backlog above capacity on the host instead of growing device-side
+    # state for it (streams, segments, pinned buffers)
+    admission_window: Optional[int] = None
     chunk_mb: float = 32.0     # staged-load chunk: one H2D + one land launch each (8 / 16 / 32 MiB: e2e 3,616 / 3,706 / 3,728 inv/s)
     staging_mb: float = 256.0  # 8 ring slots
     host_threads: Optional[int] = None
@@ -200,6 +206,8 @@ class Simulation:
         self.completion_listeners = []
         self._ids = itertools.count()
         self._in_flight = 0
+        self._in_flight_gpu = [0] * cluster.gpus
+        self._window = cluster.admission_window
         self.source = source
         # a serving process: move everything allocated so far (torch, function
         # data) out of the cyclic collector's reach so a full collection
@@ -284,6 +292,7 @@ class Simulation:
         inv.host_bytes_umb += moved[0]
         inv.pcie_bytes_umb += moved[1]
         self._in_flight += 1
+        self._in_flight_gpu[inv.gpu] += 1
         self.dataplane.start(inv, plan, wait_tokens, stage_hooks, fresh_context=fresh_context)
 
     def fail_invocation(self, inv: Invocation, reason: str) -> None:
@@ -295,9 +304,16 @@ class Simulation:
         inv.outcome = OUTCOME_COMPLETED
         inv.completion_us = now
         self._in_flight -= 1
+        self._in_flight_gpu[inv.gpu] -= 1
         self.policy.complete(inv)
+        if self._window is not None:
+            self.policy.on_memory_freed(inv.gpu)   # a window slot opened: start the next waiting
         for cb in self.completion_listeners:
             cb(inv, now)
+
+    def window_open(self, gpu: int) -> bool:
+        """Room in GPU `gpu`'s admission window (ClusterSpec.admission_window)."""
+        return self._window is None or self._in_flight_gpu[gpu] < self._window
 
     # -- run -------------------------------------------------------------------------------
     @property

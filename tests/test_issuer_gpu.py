@@ -188,3 +188,43 @@ print("ok")
 """
     r = subprocess.run([sys.executable, "-c", code, str(ROOT)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_admission_window_bounds_concurrency():
+    """ClusterSpec.admission_window: no more than the window's invocations of
+    a GPU are started and unfinished at once; the rest wait in the
+    dispatcher's FIFO and every invocation completes, in arrival order of
+    admission, with the same landed bytes."""
+    code = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_2404_14691_b200.experiments import synthetic_function
+from paper_2404_14691_b200.policies import policy_preset
+from paper_2404_14691_b200.runtime import ClusterSpec, Simulation
+a, da = synthetic_function("fa", 4, 1, 0.0625, tensors=5)
+sim = Simulation(ClusterSpec(gpus=1, admission_window=3), policy_preset("SAGE"), {"fa": a}, seed=5,
+                 function_data={"fa": da}, copy_results=False)
+peak = [0]
+orig = sim.start_invocation
+def start(inv, *x, **k):
+    orig(inv, *x, **k)
+    peak[0] = max(peak[0], sim._in_flight_gpu[inv.gpu])
+sim.start_invocation = start
+try:
+    invs = sim.submit_many(["fa"] * 40)
+    sim.drain()
+    assert all(i.outcome == "completed" for i in invs)
+    assert peak[0] == 3, peak[0]
+    starts = [i.start_us for i in invs]
+    assert starts == sorted(starts)          # FIFO admission
+    lay = da.layout
+    _, want = O.land_c(da.db, lay.src_off, lay.dst_off, lay.length, lay.seg_bytes)
+    assert any(i.ro_checksum == want for i in invs)
+    sim.check_no_leaks()
+finally:
+    sim.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code, str(ROOT)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
