@@ -146,6 +146,7 @@ __global__ void fc_kernel(const uint64_t *frame, BufRef src, BufRef dst, const _
   for (int n = 0; n < N; ++n) {
     const float *f = feat + (size_t)n * C;
     float s = 0.f;
+#pragma unroll 8   // (C = 2048: the whole row in flight, not one 16-B chunk per round trip)
     for (int c = lane * 8; c < C; c += 256) {
       uint4 v = *reinterpret_cast<const uint4 *>(wr + c);
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
