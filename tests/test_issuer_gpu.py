@@ -228,3 +228,32 @@ print("ok")
 """
     r = subprocess.run([sys.executable, "-c", code, str(ROOT)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_prewarm_leaves_a_cold_plane():
+    """Simulation.prewarm(n): the warm-up burst runs and is forgotten -- no
+    invocation records, no resident segment (the next arrival is cold and
+    loads its RO bytes over PCIe), no memory held."""
+    code = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+from paper_2404_14691_b200.experiments import synthetic_function
+from paper_2404_14691_b200.policies import policy_preset
+from paper_2404_14691_b200.runtime import ClusterSpec, Simulation
+a, da = synthetic_function("fa", 4, 1, 0.0625, tensors=5)
+sim = Simulation(ClusterSpec(gpus=1), policy_preset("SAGE"), {"fa": a}, seed=5, function_data={"fa": da},
+                 copy_results=False)
+try:
+    sim.prepare()
+    sim.prewarm(24)
+    assert sim.invocations == [] and not sim.sharing.residents
+    sim.check_no_leaks()
+    inv = sim.submit_many(["fa"])[0]
+    sim.drain()
+    assert inv.outcome == "completed" and inv.warmth.name == "COLD" and inv.ro_source == "pcie"
+finally:
+    sim.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code, str(ROOT)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
