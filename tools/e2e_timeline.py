@@ -29,7 +29,8 @@ out = []
 spans = []                                     # (first H2D begin, last return end) per burst
 walls = []
 import time  # noqa: E402
-for rep in range(6):
+REPS = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+for rep in range(REPS):
     for r in list(sim.sharing.residents.values()):
         sim.sharing.evict(r)
     t_sub = time.perf_counter()
@@ -39,7 +40,7 @@ for rep in range(6):
     t_drained = time.perf_counter()
     walls.append([round((t_done - t_sub) * 1e6), round((t_drained - t_sub) * 1e6)])
     spans.append([min(i.stages[Stage.GPU_LOAD][0] for i in invs), max(i.stages[Stage.RETURN][1] for i in invs)])
-    if rep == 5:
+    if rep == REPS - 1:
         t0 = min(i.arrival_us for i in invs)
         for i in invs:
             st = {s.name.lower(): [b - t0, e - t0] for s, (b, e) in i.stages.items()}
