@@ -189,8 +189,9 @@ int sage_slot_stream(sage_handle slot, uint64_t *stream);
 #define SAGE_LOAD_SRC_PINNED   0x1u  /* src is pinned/registered: skip the staging memcpy */
 #define SAGE_LOAD_SRC_DEVICE   0x2u  /* src is a device pointer (HBM-resident): no PCIe   */
 #define SAGE_LOAD_SRC_PEER     0x4u  /* src is a device pointer on another GPU: NVLink    */
-#define SAGE_LOAD_NO_VERIFY    0x8u  /* pinned identity loads: DMA only, no checksum pass
-                                        (private payloads; shared segments always verify)  */
+#define SAGE_LOAD_NO_VERIFY    0x8u  /* identity loads from pinned memory or this GPU's HBM:
+                                        one DMA / D2D copy, no checksum pass (private
+                                        payloads; shared segments always verify)           */
 typedef struct {
   int32_t gpu;
   uint32_t flags;

@@ -191,8 +191,10 @@ def _ptr(src) -> tuple[int, int, object]:
 
 
 def load(gpu: int, dst: int, src, layout=None, *, pinned: bool = False, device_src: int = 0,
-         device_src_bytes: int = 0, peer_gpu: int = -1, wait: Sequence[Event] = ()) -> LoadOp:
-    """Land `src` (packed stream) into `dst` through `layout` (None = identity)."""
+         device_src_bytes: int = 0, peer_gpu: int = -1, wait: Sequence[Event] = (), verify: bool = True) -> LoadOp:
+    """Land `src` (packed stream) into `dst` through `layout` (None = identity).
+    verify=False: no checksum (a private payload; an identity load from this
+    GPU's HBM or pinned memory is then a plain DMA / D2D copy)."""
     d = _lib.LoadDesc()
     d.gpu = gpu
     d.dst = dst
@@ -208,6 +210,8 @@ def load(gpu: int, dst: int, src, layout=None, *, pinned: bool = False, device_s
         d.flags = _lib.LOAD_SRC_PINNED if (pinned or isinstance(src, PinnedBuffer)) else 0
         d.src = addr
         d.src_bytes = n
+    if not verify:
+        d.flags |= _lib.LOAD_NO_VERIFY
     arr, nw = handles([e.h for e in wait])
     d.wait = arr
     d.n_wait = nw

@@ -151,6 +151,32 @@ def test_pool_chunk_carving_and_trim(dp):
     assert D.pool_trim(0) == 0
 
 
+def test_identity_load_from_hbm_verified_and_unverified(dp):
+    """An identity load from this GPU's HBM: verified, it is a land with the
+    oracle's checksum; unverified (a private payload, SAGE_LOAD_NO_VERIFY),
+    it is one D2D copy -- the same bytes, zero padding to 16 B, no checksum."""
+    n = 5 * (1 << 20) + 7
+    src_bytes = O.db_bytes(21, n)
+    src = D.pool_alloc(0, n + 64, D._lib.CLASS_WRITABLE, unaccounted=True)
+    op = D.load(0, src.dptr, src_bytes, None)
+    op.wait()
+    op.release()
+    seg = -(-n // 16) * 16
+    want_seg, want_sum = O.land_c(src_bytes, np.array([0], np.uint64), np.array([0], np.uint64),
+                                  np.array([n], np.uint64), seg)
+    for verify in (True, False):
+        dst = D.pool_alloc(0, seg + 256, D._lib.CLASS_WRITABLE, unaccounted=True)
+        D._lib.check(D.lib().sage_device_sync(0), "sync")
+        op = D.load(0, dst.dptr, None, None, device_src=src.dptr, device_src_bytes=n, verify=verify)
+        res = op.wait()
+        got = D.read_device(0, dst.dptr, seg)
+        assert np.array_equal(got, want_seg)
+        assert res.checksum == (want_sum if verify else 0)
+        op.release()
+        dst.free()
+    src.free()
+
+
 def test_direct_path_identity_pinned(dp):
     """Identity loads from pinned memory take the direct DMA + verify path;
     bytes and checksum equal the oracle's (incl. zero padding to 16)."""
