@@ -411,7 +411,9 @@ struct sage::LoadCursor {
   uint8_t *dst = nullptr;
   int gpu = -1;
   bool pinned = false;
-  size_t next = 0;   // first chunk not yet enqueued
+  bool direct = false;   // unverified identity: H2D from the pinned slot straight into dst, no land
+  uint64_t seg = 0;      // landed bytes (direct: zero padding past the packed end)
+  size_t next = 0;       // first chunk not yet enqueued
 };
 
 // Register a finished load: END on the land stream, handles out.
@@ -431,6 +433,14 @@ static int load_finish(Load *L, Gpu *G, sage_handle *load_out, sage_handle *end_
 // Enqueue the ring chunks of a staged (packed / pageable) load from
 // c->next on until at least `budget` bytes crossed the link or the plan is
 // done: CPU_LOAD (pageable only) -> H2D into a ring slot -> land.
+static bool staged_land_forced() {
+  static const bool v = [] {
+    const char *e = getenv("SAGE_STAGED_LAND");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
 static int cursor_advance(LoadCursor *c, uint64_t budget, uint64_t *enq) {
   Gpu *G = c->G;
   Load *L = c->L;
@@ -446,15 +456,29 @@ static int cursor_advance(LoadCursor *c, uint64_t budget, uint64_t *enq) {
     uint8_t *dslot = G->dstage + r * slot_bytes;
     uint8_t *pslot = G->pin + r * slot_bytes;
     const uint8_t *src = c->src + C.sb;
-    if (n) {
-      if (!c->pinned) {
-        // CPU_LOAD: DB record -> pinned staging, once the slot's last H2D is done
-        SAGE_CUDA(cudaStreamWaitEvent(G->host, G->ev_h2d[r], 0));
-        SAGE_CUDA(cudaLaunchHostFunc(G->host, host_copy_fn, new HostCopyArg{L, pslot, src, (size_t)n}));
-        SAGE_CUDA(cudaEventRecord(G->ev_cpu[r], G->host));
-        SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_cpu[r], 0));
-        L->host_bytes += n;
-      }
+    if (n && !c->pinned) {
+      // CPU_LOAD: DB record -> pinned staging, once the slot's last H2D is done
+      SAGE_CUDA(cudaStreamWaitEvent(G->host, G->ev_h2d[r], 0));
+      SAGE_CUDA(cudaLaunchHostFunc(G->host, host_copy_fn, new HostCopyArg{L, pslot, src, (size_t)n}));
+      SAGE_CUDA(cudaEventRecord(G->ev_cpu[r], G->host));
+      SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_cpu[r], 0));
+      L->host_bytes += n;
+    }
+    if (!n) {
+      if (!L->has_gpu_begin) { SAGE_TRY(event_record(L->eb, G->land)); L->has_gpu_begin = true; }
+    } else if (c->direct) {
+      // unverified identity: the staged bytes go straight to their place in
+      // dst (less the 16 B overlap only the land's funnel shift needs); the
+      // device slot is untouched, so ev_land[r] keeps marking its last land
+      const uint64_t off = k == 0 ? 0 : C.sb + 16;
+      if (!L->has_gpu_begin) { SAGE_TRY(event_record(L->eb, G->copy)); L->has_gpu_begin = true; }
+      SAGE_CUDA(cudaMemcpyAsync(c->dst + off, (c->pinned ? src : pslot) + (off - C.sb), C.se - off,
+                                cudaMemcpyHostToDevice, G->copy));
+      SAGE_CUDA(cudaEventRecord(G->ev_h2d[r], G->copy));
+      SAGE_CUDA(cudaStreamWaitEvent(G->land, G->ev_h2d[r], 0));   // END (on land) covers it
+      L->link_bytes += C.se - off;
+      moved += n;
+    } else {
       // GPU_LOAD: H2D into the device slot once its last land is done
       SAGE_CUDA(cudaStreamWaitEvent(G->copy, G->ev_land[r], 0));
       if (!L->has_gpu_begin) { SAGE_TRY(event_record(L->eb, G->copy)); L->has_gpu_begin = true; }
@@ -463,9 +487,11 @@ static int cursor_advance(LoadCursor *c, uint64_t budget, uint64_t *enq) {
       SAGE_CUDA(cudaStreamWaitEvent(G->land, G->ev_h2d[r], 0));
       L->link_bytes += n;
       moved += n;
-    } else if (!L->has_gpu_begin) {
-      SAGE_TRY(event_record(L->eb, G->land));
-      L->has_gpu_begin = true;
+    }
+    if (c->direct) {   // no land: zero the padding past the packed end
+      if (k + 1 == P.chunks.size() && c->seg > C.se)
+        SAGE_CUDA(cudaMemsetAsync(c->dst + C.se, 0, c->seg - C.se, G->land));
+      continue;
     }
     if ((rc = enqueue_land(G, P, C, c->gpu, dslot, c->dst, L->acc_idx, k + 1 == P.chunks.size())) != SAGE_OK)
       return rc;
@@ -668,6 +694,10 @@ int sage::segment_load_open(const sage_load_desc *d, sage_handle pre_end, LoadCu
     c->dst = dst;
     c->gpu = d->gpu;
     c->pinned = pinned;
+    // an unverified identity load needs no land: each staged chunk is DMA'd
+    // into its final place (SAGE_STAGED_LAND=1 keeps the land for A/B runs)
+    c->direct = !d->layout && (d->flags & SAGE_LOAD_NO_VERIFY) && !staged_land_forced();
+    c->seg = lay->seg;
     *cur = c;   // the chunks are enqueued by segment_load_step
     return SAGE_OK;
   }

@@ -177,6 +177,35 @@ def test_identity_load_from_hbm_verified_and_unverified(dp):
     src.free()
 
 
+def test_staged_identity_unverified_interleaved(dp):
+    """Pageable identity loads: verified ones land through the device slot;
+    unverified ones (SAGE_LOAD_NO_VERIFY) DMA each staged chunk straight into
+    dst, skipping the land. Interleaved through the 8-slot ring, all enqueued
+    before any completes, into dirtied destinations: every segment equals the
+    oracle's bytes (zero padding to 16 B), checksums only where verified."""
+    sizes = [1, 15, 4097, (8 << 20) - 3, (8 << 20) + 16, (21 << 20) + 9, 3 << 20, (17 << 20) + 1]
+    jobs = []
+    for i, n in enumerate(sizes * 2):
+        verify = i % 2 == 0
+        db = O.db_bytes(300 + i, n)
+        seg_bytes = -(-n // 16) * 16
+        seg = D.pool_alloc(0, seg_bytes, D._lib.CLASS_WRITABLE)
+        junk = D.PinnedBuffer(seg_bytes)
+        junk.view()[:] = 0xCD
+        D.load(0, seg.dptr, junk, None).wait()
+        junk.free()
+        jobs.append((n, db, seg_bytes, seg, verify, D.load(0, seg.dptr, db, None, verify=verify)))
+    for n, db, seg_bytes, seg, verify, op in jobs:
+        res = op.wait()
+        want = np.zeros(seg_bytes, np.uint8)
+        want[:n] = db
+        assert np.array_equal(D.read_device(0, seg.dptr, seg_bytes), want), (n, verify)
+        assert res.checksum == (O.checksum_c(want) if verify else 0), (n, verify)
+        assert res.host_bytes >= n and res.landed_bytes == seg_bytes
+        op.release()
+        seg.free()
+
+
 def test_direct_path_identity_pinned(dp):
     """Identity loads from pinned memory take the direct DMA + verify path;
     bytes and checksum equal the oracle's (incl. zero padding to 16)."""
