@@ -96,23 +96,31 @@ __global__ void maxpool_kernel(const uint64_t *frame, BufRef src, BufRef dst, in
     t /= Q;
     const int p = (int)(t % P);
     const int n = (int)(t / P);
+    // all nine window loads in flight at once; out-of-image taps read as
+    // bf16 -inf (0xFF80), which never wins the max
+    uint4 v[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int ih = 2 * p - 1 + r;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int iw = 2 * q - 1 + s;
+        v[3 * r + s] = (ih >= 0 && ih < H && iw >= 0 && iw < W)
+                           ? __ldg(reinterpret_cast<const uint4 *>(in + ((size_t)(n * H + ih) * W + iw) * C + cg * 8))
+                           : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      }
+    }
     float m[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) m[e] = -INFINITY;
-    for (int r = 0; r < 3; ++r) {
-      const int ih = 2 * p - 1 + r;
-      if (ih < 0 || ih >= H) continue;
-      for (int s = 0; s < 3; ++s) {
-        const int iw = 2 * q - 1 + s;
-        if (iw < 0 || iw >= W) continue;
-        uint4 v = *reinterpret_cast<const uint4 *>(in + ((size_t)(n * H + ih) * W + iw) * C + cg * 8);
-        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h[e]);
-          m[2 * e] = fmaxf(m[2 * e], f.x);
-          m[2 * e + 1] = fmaxf(m[2 * e + 1], f.y);
-        }
+    for (int k = 0; k < 9; ++k) {
+      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[k]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        m[2 * e] = fmaxf(m[2 * e], f.x);
+        m[2 * e + 1] = fmaxf(m[2 * e + 1], f.y);
       }
     }
     uint4 o;
