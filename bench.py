@@ -820,6 +820,10 @@ def our_arm(args, rank, world, dist) -> dict:
         "setup_p50_ms": round(percentile(setups_val, 50) / 1e3, 3),
         "setup_p99_ms": round(percentile(setups_val, 99) / 1e3, 3),
         "step_ms": val_steps,
+        # diagnostic only (value above is the mean over all timed steps): the
+        # same throughput at the median step, so a rare host stall on a box
+        # (a 20-30 ms step among ~3.5 ms ones) is visible as such
+        "value_at_median_step": round(per_step * world / (statistics.median(val_steps) / 1e3), 2) if val_steps else None,
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": round(e2e_us / 1e3 / args.steps, 3),
                 "setup_p50_ms": round(percentile(setups_e2e, 50) / 1e3, 3),
